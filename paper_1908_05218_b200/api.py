@@ -1,0 +1,250 @@
+"""Python mirror of the reference's public MMP API (proj/core/include/h2mmp):
+
+    build_cluster_tree(points, leafsize)          cluster_tree.hpp:43
+    build_block_tree(rows, cols, eta)             block_tree.hpp:75-77
+    mmp(a, b, eps_trunc) -> MmpResult             mmp.hpp:60-61
+    formatted_mmp(a, b) -> MmpResult              mmp.hpp:66-67
+
+plus the synthetic-input constructors of the BASELINE configs.  Every call
+goes through the C-ABI of libh2mmp_b200.so; the product runs on the GPU only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from typing import Optional
+
+import numpy as np
+
+from . import h2c
+from .h2c import (BlockTree, ClusterTree, ConfigError, H2Matrix, MmpReport, MmpResult, h2c_blocks, h2c_matrix,
+                  h2c_report, h2c_tree, raise_for)
+
+_ctx_lock = threading.Lock()
+_default_ctx: Optional["Context"] = None
+
+
+class Context:
+    """A device, a CUDA stream and the structure-plan cache (h2c_create)."""
+
+    def __init__(self, device: int = 0):
+        self._h = h2c.lib().h2c_create(device)
+        if not self._h:
+            raise h2c.DeviceError(h2c.last_error())
+
+    @property
+    def handle(self):
+        return self._h
+
+    def kernel_launches(self) -> int:
+        return int(h2c.lib().h2c_kernel_launches(self._h))
+
+    def close(self):
+        if self._h:
+            h2c.lib().h2c_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def default_context() -> Context:
+    global _default_ctx
+    with _ctx_lock:
+        if _default_ctx is None:
+            _default_ctx = Context(0)
+        return _default_ctx
+
+
+# ---------------------------------------------------------------------------
+def _structure(points: np.ndarray, leafsize: int, eta: float):
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    L = h2c.lib()
+    h = L.h2c_build_structure(pts.ctypes.data_as(h2c.P_f64), len(pts), int(leafsize), float(eta))
+    if not h:
+        msg = h2c.last_error()
+        raise ConfigError(msg) if ("must" in msg or "cannot" in msg) else h2c.InvariantError(msg)
+    try:
+        td, bd = h2c_tree(), h2c_blocks()
+        L.h2c_structure_tree(h, C.byref(td))
+        L.h2c_structure_blocks(h, C.byref(bd))
+        tree = ClusterTree.from_desc(td)
+        tree.points = pts
+        blocks = BlockTree.from_desc(tree, bd)
+    finally:
+        L.h2c_structure_free(h)
+    return tree, blocks
+
+
+def build_cluster_tree(points: np.ndarray, leafsize: int) -> ClusterTree:
+    """cluster_tree.cpp:66-93 (longest-axis median bisection to uniform depth)."""
+    tree, _ = _structure(points, leafsize, 1.0)
+    return tree
+
+
+def build_block_tree(rows: ClusterTree, cols: ClusterTree, eta: float) -> BlockTree:
+    """block_tree.cpp:9-53; the MMP path uses a single shared tree (rows is cols)."""
+    if rows is not cols:
+        raise ConfigError("build_block_tree: the B200 path requires one shared cluster tree")
+    if eta <= 0:
+        raise ConfigError("eta must be positive")
+    if rows.points is None:
+        raise ConfigError("build_block_tree: tree was not built from points")
+    t2, blocks = _structure(rows.points, rows.leafsize, eta)
+    if not t2.same_as(rows):
+        raise h2c.InvariantError("block tree rebuilt a different cluster tree")
+    blocks.tree = rows
+    return blocks
+
+
+def target_status(structure: BlockTree, t: int, s: int) -> int:
+    """BlockTree::target_status (block_tree.cpp:61-85): 0 full, 1 adm, 2 sub, 3 inside."""
+    r = h2c.lib().h2c_target_status(C.byref(structure.tree.desc()), C.byref(structure.desc()), int(t), int(s))
+    if r < 0:
+        raise h2c.InvariantError(h2c.last_error())
+    return r
+
+
+def _take_h2(handle, tree: ClusterTree, structure: BlockTree) -> H2Matrix:
+    L = h2c.lib()
+    if not handle:
+        raise ConfigError(h2c.last_error())
+    try:
+        d = h2c_matrix()
+        L.h2c_h2_desc(handle, C.byref(d))
+        return H2Matrix.from_desc(tree, structure, d)
+    finally:
+        L.h2c_h2_free(handle)
+
+
+def build_chebyshev(tree: ClusterTree, structure: BlockTree, points: np.ndarray, order: int, kernel: str = "laplace",
+                    kappa: float = 0.0, diagonal: float = 0.0, eps_recompress: float = 0.0,
+                    threads: int = 0) -> H2Matrix:
+    """Nested tensor-Chebyshev H^2 matrix with orthonormal bases (input side)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    k = {"laplace": 0, "helmholtz": 1}[kernel]
+    h = h2c.lib().h2c_build_chebyshev(C.byref(tree.desc()), C.byref(structure.desc()),
+                                      pts.ctypes.data_as(h2c.P_f64), k, float(kappa), float(diagonal), int(order),
+                                      float(eps_recompress), int(threads))
+    return _take_h2(h, tree, structure)
+
+
+def build_fd_laplacian(tree: ClusterTree, structure: BlockTree, points: np.ndarray, h: float) -> H2Matrix:
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    hd = h2c.lib().h2c_build_fd_laplacian(C.byref(tree.desc()), C.byref(structure.desc()),
+                                          pts.ctypes.data_as(h2c.P_f64), float(h))
+    return _take_h2(hd, tree, structure)
+
+
+# ---------------------------------------------------------------------------
+def _result(handle, a: H2Matrix) -> MmpResult:
+    L = h2c.lib()
+    try:
+        d = h2c_matrix()
+        L.h2c_result_matrix(handle, C.byref(d))
+        prod = H2Matrix.from_desc(a.tree, a.structure, d)
+        r = h2c_report()
+        L.h2c_result_report(handle, C.byref(r))
+        rep = MmpReport.from_desc(r)
+    finally:
+        L.h2c_result_free(handle)
+    return MmpResult(prod, rep)
+
+
+def mmp(a: H2Matrix, b: H2Matrix, eps_trunc: float, ctx: Optional[Context] = None) -> MmpResult:
+    """Accuracy-controlled product C = A*B (mmp.cpp:688-691) on the B200."""
+    ctx = ctx or default_context()
+    out = C.c_void_p()
+    rc = h2c.lib().h2c_mmp(ctx.handle, C.byref(a.desc()), C.byref(b.desc()), float(eps_trunc), C.byref(out))
+    raise_for(rc, h2c.last_error(ctx.handle))
+    return _result(out, a)
+
+
+def formatted_mmp(a: H2Matrix, b: H2Matrix, ctx: Optional[Context] = None) -> MmpResult:
+    """Baseline formatted product with unchanged bases (mmp.cpp:716-719)."""
+    ctx = ctx or default_context()
+    out = C.c_void_p()
+    rc = h2c.lib().h2c_formatted_mmp(ctx.handle, C.byref(a.desc()), C.byref(b.desc()), C.byref(out))
+    raise_for(rc, h2c.last_error(ctx.handle))
+    return _result(out, a)
+
+
+def count_report(a: H2Matrix, b: H2Matrix, c: H2Matrix, adaptive: bool = True, eps_trunc: float = 0.0) -> MmpReport:
+    """Host-side MmpReport counters of C = A*B from structure and ranks (h2c_count_report)."""
+    out = C.c_void_p()
+    rc = h2c.lib().h2c_count_report(C.byref(a.desc()), C.byref(b.desc()), C.byref(c.desc()), int(adaptive),
+                                    float(eps_trunc), C.byref(out))
+    raise_for(rc, h2c.last_error())
+    try:
+        r = h2c_report()
+        h2c.lib().h2c_result_report(out, C.byref(r))
+        return MmpReport.from_desc(r)
+    finally:
+        h2c.lib().h2c_result_free(out)
+
+
+class ResidentOperand:
+    """An operand uploaded once to HBM (h2c_upload) for repeated products."""
+
+    def __init__(self, m: H2Matrix, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.matrix = m
+        h = C.c_void_p()
+        rc = h2c.lib().h2c_upload(self.ctx.handle, C.byref(m.desc()), C.byref(h))
+        raise_for(rc, h2c.last_error(self.ctx.handle))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if self._h:
+                h2c.lib().h2c_operand_free(self._h)
+        except Exception:
+            pass
+
+
+def mmp_resident(a: ResidentOperand, b: ResidentOperand, eps_trunc: float, adaptive: bool = True,
+                 want_report: bool = False):
+    """Runs the product on resident operands; returns (device_seconds, report|None)."""
+    ctx = a.ctx
+    secs = C.c_double()
+    out = C.c_void_p() if want_report else None
+    rc = h2c.lib().h2c_mmp_resident(ctx.handle, a._h, b._h, float(eps_trunc), int(adaptive), C.byref(secs),
+                                    C.byref(out) if want_report else None)
+    raise_for(rc, h2c.last_error(ctx.handle))
+    rep = None
+    if want_report:
+        r = h2c_report()
+        h2c.lib().h2c_result_report(out, C.byref(r))
+        rep = MmpReport.from_desc(r)
+        h2c.lib().h2c_result_free(out)
+    return secs.value, rep
+
+
+class PinnedArray:
+    """numpy view over pinned host memory (h2c_host_alloc)."""
+
+    def __init__(self, n: int, dtype=np.float64):
+        self.nbytes = max(1, int(n) * np.dtype(dtype).itemsize)
+        self._p = h2c.lib().h2c_host_alloc(self.nbytes)
+        if not self._p:
+            raise MemoryError(h2c.last_error())
+        buf = (C.c_char * self.nbytes).from_address(self._p)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(n))
+
+    def __del__(self):
+        try:
+            if self._p:
+                h2c.lib().h2c_host_free(self._p)
+                self._p = None
+        except Exception:
+            pass
+
+
+def pin_matrix(m: H2Matrix) -> tuple[H2Matrix, PinnedArray]:
+    """Copy of `m` whose value array lives in pinned host memory."""
+    pa = PinnedArray(len(m.values), m.values.dtype)
+    pa.array[:] = m.values
+    return m.copy_with(pa.array), pa

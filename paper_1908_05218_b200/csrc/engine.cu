@@ -1,0 +1,1273 @@
+// Level-synchronous B200 pipeline of the accuracy-controlled H^2-MMP
+// (the reference's ProductEngine, proj/core/src/mmp.cpp:13-684), restated as
+// batched products over padded per-level device arrays.
+//
+// Data layout in HBM (per operand X in {A, B, C}, level l, padded ranks
+// K = round_up(max rank at l, 8), leaf size NL = round_up(max #t, 8)):
+//   leaf bases      V  [n_L][NL x K_L]            column-major, zero padded
+//   transfers       T_l[n_l][2K_{l+1} x K_l]      child 0 rows [0,K_{l+1}), child 1 rows [K_{l+1},2K_{l+1})
+//   couplings       S_l[n_adm,l][Kr_l x Kc_l]     admissible blocks in (row,col) order
+//   full blocks     F  [n_full][NL x NL]
+// Zero padding is exact under every product, so padded rows/columns never
+// leak into results; ranks are tracked per cluster on the host.
+//
+// Reassociation (value-neutral up to rounding, counted separately as
+// flops_exec): the four product cases are evaluated as
+//   sum_j LA_ij * YB_jk  (B_jk admissible; LA = coll_a or P^A S^A B_j)
+//   sum_j XA_ij * RB_jk  (A_ij admissible, B_jk near; XA = P^A S^A, RB = coll_b)
+//   sum_j WA_ij * WB_jk  (leaf full x full; WA = V^C^H F, WB = F conj(V^C))
+// and the leaf Gram G1 = sum_{j,k} (F F)(F F)^H as sum_j F_ij (sum_k F_jk F_jk^H) F_ij^H.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <tuple>
+
+#include "counters.hpp"
+#include "engine.hpp"
+#include "kernels.cuh"
+
+namespace h2b {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ConfigErr : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " __FILE__ \
+                      ":" + std::to_string(__LINE__));                                         \
+  } while (0)
+
+static inline int pad8(int64_t r) { return static_cast<int>(std::max<int64_t>(8, (r + 7) / 8 * 8)); }
+
+// ---------------------------------------------------------------------------
+// stream-ordered device buffers
+struct DBuf {
+  double* p = nullptr;
+  size_t n = 0;  // doubles
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t doubles, cudaStream_t st, bool zero = false) { alloc(doubles, st, zero); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      s = o.s;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t doubles, cudaStream_t st, bool zero = false) {
+    release();
+    s = st;
+    n = std::max<size_t>(doubles, 2);
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(double), s));
+    if (zero) CK(cudaMemsetAsync(p, 0, n * sizeof(double), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  operator double*() const { return p; }
+};
+
+template <class T>
+struct DVec {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DVec() = default;
+  DVec(const DVec&) = delete;
+  DVec& operator=(const DVec&) = delete;
+  DVec(DVec&& o) noexcept { *this = std::move(o); }
+  DVec& operator=(DVec&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      s = o.s;
+      o.p = nullptr;
+    }
+    return *this;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    release();
+    s = st;
+    n = v.size();
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(1, n) * sizeof(T), s));
+    if (n) CK(cudaMemcpyAsync(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void alloc(size_t cnt, cudaStream_t st) {
+    release();
+    s = st;
+    n = cnt;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(1, n) * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+  }
+  ~DVec() { release(); }
+};
+
+// ---------------------------------------------------------------------------
+// device copy of the plan
+struct DevCsr {
+  const int* ptr = nullptr;
+  const int* li = nullptr;
+  const int* ri = nullptr;
+  int n_out = 0;
+  int64_t entries = 0;
+};
+
+struct DevLevel {
+  DevCsr ly, xr, ww, ff, fr, rf, rr, mg, hq, hqc, row_near, col_near, row_merged, col_merged;
+  const int *near_row = nullptr, *near_col = nullptr, *adm_row = nullptr, *adm_col = nullptr;
+  const int *nearb = nullptr, *adm = nullptr, *merged_row = nullptr, *merged_quad = nullptr;
+  const int *sub_child = nullptr, *nl_col = nullptr;
+  // split from this level into level+1, per quadrant
+  const int *sp_src[4] = {}, *sp_prow[4] = {}, *sp_omap[4] = {};
+  int sp_n[4] = {0, 0, 0, 0};
+  const int *sf_src[4] = {}, *sf_prow[4] = {}, *sf_near[4] = {}, *sf_crow[4] = {}, *sf_ccol[4] = {};
+  int sf_n[4] = {0, 0, 0, 0};
+};
+
+struct DevPlan {
+  std::vector<DevLevel> lv;
+  const int* even = nullptr;  // p -> 2p
+  const int* odd = nullptr;   // p -> 2p+1
+  DVec<int32_t> blob;
+};
+
+static std::unique_ptr<DevPlan> upload_plan(const Plan& P, cudaStream_t s) {
+  auto D = std::make_unique<DevPlan>();
+  std::vector<int32_t> blob;
+  std::vector<std::pair<const int**, size_t>> fix;
+  auto put = [&](const int** dst, const std::vector<int32_t>& v) {
+    fix.push_back({dst, blob.size()});
+    blob.insert(blob.end(), v.begin(), v.end());
+    blob.push_back(0);  // keep every array non-empty
+  };
+  auto put_csr = [&](DevCsr& d, const Csr& c) {
+    put(&d.ptr, c.ptr);
+    put(&d.li, c.li);
+    put(&d.ri, c.ri);
+    d.n_out = c.ptr.empty() ? 0 : static_cast<int>(c.ptr.size()) - 1;
+    d.entries = c.entries();
+  };
+  D->lv.resize(P.depth + 1);
+  int maxn = 1;
+  for (int l = 0; l <= P.depth; ++l) {
+    const LevelPlan& L = P.lv[l];
+    DevLevel& Q = D->lv[l];
+    maxn = std::max(maxn, L.n);
+    put_csr(Q.ly, L.ly);
+    put_csr(Q.xr, L.xr);
+    put_csr(Q.ww, L.ww);
+    put_csr(Q.ff, L.ff);
+    put_csr(Q.fr, L.fr);
+    put_csr(Q.rf, L.rf);
+    put_csr(Q.rr, L.rr);
+    put_csr(Q.mg, L.mg);
+    put_csr(Q.hq, L.hq);
+    put_csr(Q.hqc, L.hqc);
+    put_csr(Q.row_near, L.row_near);
+    put_csr(Q.col_near, L.col_near);
+    put_csr(Q.row_merged, L.row_merged);
+    put_csr(Q.col_merged, L.col_merged);
+    std::vector<int32_t> nr, nc, ar, ac, nlc;
+    for (int b : L.nearb) {
+      nr.push_back(L.brow[b]);
+      nc.push_back(L.bcol[b]);
+    }
+    for (int b : L.adm) {
+      ar.push_back(L.brow[b]);
+      ac.push_back(L.bcol[b]);
+    }
+    for (int b : L.nl_block) nlc.push_back(L.bcol[b]);
+    put(&Q.near_row, nr);
+    put(&Q.near_col, nc);
+    put(&Q.adm_row, ar);
+    put(&Q.adm_col, ac);
+    put(&Q.nearb, L.nearb);
+    put(&Q.adm, L.adm);
+    put(&Q.merged_row, L.merged_row);
+    put(&Q.merged_quad, L.merged_quad);
+    put(&Q.sub_child, L.sub_child);
+    put(&Q.nl_col, nlc);
+    if (l < P.depth) {
+      const LevelPlan& C = P.lv[l + 1];
+      const int cna = static_cast<int>(C.adm.size()), cnp = static_cast<int>(C.pend_row.size());
+      for (int q = 0; q < 4; ++q) {
+        std::vector<int32_t> src, prow, omap, fsrc, fprow, fnear, fcrow, fccol;
+        for (size_t e = 0; e < L.split_src[q].size(); ++e) {
+          const int nl = L.split_src[q][e];
+          const int cb = L.split_dst[q][e];
+          const int pr = L.brow[L.nl_block[nl]];
+          if (C.bkind[cb] == kFull) {
+            fsrc.push_back(nl);
+            fprow.push_back(pr);
+            fnear.push_back(C.kidx[cb]);
+            fcrow.push_back(C.brow[cb]);
+            fccol.push_back(C.bcol[cb]);
+          } else {
+            src.push_back(nl);
+            prow.push_back(pr);
+            omap.push_back(C.bkind[cb] == kAdm ? C.kidx[cb] : cna + cnp + C.nl_of_block[cb]);
+          }
+        }
+        Q.sp_n[q] = static_cast<int>(src.size());
+        Q.sf_n[q] = static_cast<int>(fsrc.size());
+        put(&Q.sp_src[q], src);
+        put(&Q.sp_prow[q], prow);
+        put(&Q.sp_omap[q], omap);
+        put(&Q.sf_src[q], fsrc);
+        put(&Q.sf_prow[q], fprow);
+        put(&Q.sf_near[q], fnear);
+        put(&Q.sf_crow[q], fcrow);
+        put(&Q.sf_ccol[q], fccol);
+      }
+    }
+  }
+  std::vector<int32_t> ev(maxn), od(maxn);
+  for (int p = 0; p < maxn; ++p) {
+    ev[p] = 2 * p;
+    od[p] = 2 * p + 1;
+  }
+  put(&D->even, ev);
+  put(&D->odd, od);
+  D->blob.upload(blob, s);
+  for (auto& [dst, off] : fix) *dst = D->blob.p + off;
+  return D;
+}
+
+// ---------------------------------------------------------------------------
+// operands resident on the device
+struct DevOperand {
+  uint64_t key = 0;
+  int scalar = 0;
+  int depth = 0, NL = 8;
+  std::vector<int> Kr, Kc;                          // padded ranks per level
+  std::vector<std::vector<int64_t>> rr, rc;         // ranks per level / position
+  std::vector<std::vector<uint8_t>> dgr, dgc;       // degenerate flags
+  std::vector<DVec<uint8_t>> dgr_d, dgc_d;
+  std::vector<DVec<int32_t>> rr_d, rc_d;
+  DBuf Vr, Vc, F;
+  std::vector<DBuf> Tr, Tc, S;
+};
+
+struct CopyList {
+  std::vector<CopyJob> jobs;
+  void add(const double* src, double* dst, int rows, int cols, int sld, int dld) {
+    if (rows > 0 && cols > 0) jobs.push_back({src, dst, rows, cols, sld, dld});
+  }
+  void run(cudaStream_t s, int W, int64_t* launches) {
+    if (jobs.empty()) return;
+    DVec<CopyJob> d;
+    d.upload(jobs, s);
+    const size_t chunk = 1u << 30;
+    for (size_t o = 0; o < jobs.size(); o += chunk) {
+      const unsigned nb = static_cast<unsigned>(std::min(chunk, jobs.size() - o));
+      copy_jobs_kernel<<<nb, 128, 0, s>>>(d.p + o, W);
+      CK(cudaGetLastError());
+      (*launches)++;
+    }
+  }
+};
+
+static std::shared_ptr<DevOperand> upload_operand(const Plan& P, const h2c_matrix& m,
+                                                  cudaStream_t s, int64_t* launches) {
+  auto X = std::make_shared<DevOperand>();
+  const int D = P.depth;
+  const int W = m.scalar == H2C_COMPLEX ? 2 : 1;
+  X->scalar = m.scalar;
+  X->depth = D;
+  int maxleaf = 1;
+  for (int p = 0; p < P.lv[D].n; ++p) maxleaf = std::max(maxleaf, P.lv[D].size[p]);
+  X->NL = pad8(maxleaf);
+  X->Kr.assign(D + 1, 8);
+  X->Kc.assign(D + 1, 8);
+  X->rr.resize(D + 1);
+  X->rc.resize(D + 1);
+  X->dgr.resize(D + 1);
+  X->dgc.resize(D + 1);
+  for (int l = 0; l <= D; ++l) {
+    const LevelPlan& L = P.lv[l];
+    int64_t mr = 0, mc = 0;
+    for (int p = 0; p < L.n; ++p) {
+      const int id = L.id[p];
+      X->rr[l].push_back(m.row_rank[id]);
+      X->rc[l].push_back(m.col_rank[id]);
+      X->dgr[l].push_back(m.row_degenerate ? m.row_degenerate[id] : 0);
+      X->dgc[l].push_back(m.col_degenerate ? m.col_degenerate[id] : 0);
+      mr = std::max<int64_t>(mr, m.row_rank[id]);
+      mc = std::max<int64_t>(mc, m.col_rank[id]);
+    }
+    X->Kr[l] = pad8(mr);
+    X->Kc[l] = pad8(mc);
+  }
+  X->dgr_d.resize(D + 1);
+  X->dgc_d.resize(D + 1);
+  X->rr_d.resize(D + 1);
+  X->rc_d.resize(D + 1);
+  for (int l = 0; l <= D; ++l) {
+    X->dgr_d[l].upload(X->dgr[l], s);
+    X->dgc_d[l].upload(X->dgc[l], s);
+    std::vector<int32_t> a(X->rr[l].begin(), X->rr[l].end()), b(X->rc[l].begin(), X->rc[l].end());
+    X->rr_d[l].upload(a, s);
+    X->rc_d[l].upload(b, s);
+  }
+  const int NL = X->NL;
+  const LevelPlan& LL = P.lv[D];
+  X->Vr.alloc(size_t(LL.n) * NL * X->Kr[D] * W, s, true);
+  X->Vc.alloc(size_t(LL.n) * NL * X->Kc[D] * W, s, true);
+  X->F.alloc(size_t(LL.nearb.size()) * NL * NL * W, s, true);
+  X->Tr.resize(D + 1);
+  X->Tc.resize(D + 1);
+  X->S.resize(D + 1);
+  for (int l = 1; l < D; ++l) {
+    X->Tr[l].alloc(size_t(P.lv[l].n) * 2 * X->Kr[l + 1] * X->Kr[l] * W, s, true);
+    X->Tc[l].alloc(size_t(P.lv[l].n) * 2 * X->Kc[l + 1] * X->Kc[l] * W, s, true);
+  }
+  for (int l = 0; l <= D; ++l)
+    X->S[l].alloc(size_t(P.lv[l].adm.size()) * X->Kr[l] * X->Kc[l] * W, s, true);
+
+  DBuf raw(size_t(m.n_values) * W, s);
+  if (m.n_values)
+    CK(cudaMemcpyAsync(raw.p, m.values, size_t(m.n_values) * W * sizeof(double), cudaMemcpyHostToDevice, s));
+  CopyList cl;
+  auto src = [&](int64_t off) { return raw.p + off * W; };
+  for (int p = 0; p < LL.n; ++p) {
+    const int id = LL.id[p];
+    if (m.row_offset[id] >= 0)
+      cl.add(src(m.row_offset[id]), X->Vr.p + size_t(p) * NL * X->Kr[D] * W, LL.size[p], m.row_rank[id], LL.size[p], NL);
+    if (m.col_offset[id] >= 0)
+      cl.add(src(m.col_offset[id]), X->Vc.p + size_t(p) * NL * X->Kc[D] * W, LL.size[p], m.col_rank[id], LL.size[p], NL);
+  }
+  for (int l = 1; l < D; ++l) {
+    const LevelPlan& L = P.lv[l];
+    for (int p = 0; p < L.n; ++p) {
+      for (int side = 0; side < 2; ++side) {
+        const int id = L.id[p];
+        const int32_t* rk = side == 0 ? m.row_rank : m.col_rank;
+        const int64_t off = side == 0 ? m.row_offset[id] : m.col_offset[id];
+        if (off < 0) continue;
+        const int K1 = side == 0 ? X->Kr[l + 1] : X->Kc[l + 1];
+        const int K0 = side == 0 ? X->Kr[l] : X->Kc[l];
+        double* base = (side == 0 ? X->Tr[l].p : X->Tc[l].p) + size_t(p) * 2 * K1 * K0 * W;
+        const int c0 = rk[P.lv[l + 1].id[2 * p]], c1 = rk[P.lv[l + 1].id[2 * p + 1]];
+        cl.add(src(off), base, c0, rk[id], c0 + c1, 2 * K1);
+        cl.add(src(off + c0), base + size_t(K1) * W, c1, rk[id], c0 + c1, 2 * K1);
+      }
+    }
+  }
+  for (int l = 0; l <= D; ++l) {
+    const LevelPlan& L = P.lv[l];
+    for (size_t a = 0; a < L.adm.size(); ++a) {
+      const int b = L.adm[a];
+      const int64_t off = m.block_offset[L.bglobal[b]];
+      const int rr = m.row_rank[L.id[L.brow[b]]], rc = m.col_rank[L.id[L.bcol[b]]];
+      if (off >= 0) cl.add(src(off), X->S[l].p + a * size_t(X->Kr[l]) * X->Kc[l] * W, rr, rc, rr, X->Kr[l]);
+    }
+  }
+  for (size_t q = 0; q < LL.nearb.size(); ++q) {
+    const int b = LL.nearb[q];
+    const int64_t off = m.block_offset[LL.bglobal[b]];
+    const int nr = LL.size[LL.brow[b]], nc = LL.size[LL.bcol[b]];
+    if (off >= 0) cl.add(src(off), X->F.p + q * size_t(NL) * NL * W, nr, nc, nr, NL);
+  }
+  cl.run(s, W, launches);
+  CK(cudaStreamSynchronize(s));  // `raw` and the job list die here
+  return X;
+}
+
+// ---------------------------------------------------------------------------
+struct Ref {
+  const double* p;
+  long long s;    // stride between matrices (scalars)
+  long long off;  // view offset (scalars)
+  int ld;
+  int op;
+};
+struct Grp {
+  Ref L, R;
+  int K;
+  const DevCsr* csr;
+  const int* li;
+  const int* ri;
+};
+
+struct EngineRun {
+  Context& ctx;
+  const Plan& P;
+  const DevPlan& DP;
+  const DevOperand& A;
+  const DevOperand& B;
+  double eps;
+  bool adaptive;
+  bool cplx;
+  int W;
+  cudaStream_t s;
+  int D, NL;
+  int64_t exec_macs = 0;
+  int64_t launches = 0;
+
+  // C
+  std::vector<int> KCr, KCc;
+  std::vector<std::vector<int64_t>> rcr, rcc;
+  std::vector<DVec<uint8_t>> dgr, dgc;
+  DBuf Vr, Vc, F;
+  std::vector<DBuf> Tr, Tc, Tg;
+  // per-level intermediates
+  std::vector<DBuf> Bp, PA, PB, LA, RB;
+
+  EngineRun(Context& c, const Plan& p, const DevPlan& dp, const DevOperand& a, const DevOperand& b,
+            double e, bool ad, cudaStream_t st)
+      : ctx(c), P(p), DP(dp), A(a), B(b), eps(e), adaptive(ad), s(st) {
+    cplx = a.scalar == H2C_COMPLEX;
+    W = cplx ? 2 : 1;
+    D = P.depth;
+    NL = A.NL;
+    KCr.assign(D + 1, 8);
+    KCc.assign(D + 1, 8);
+    rcr.resize(D + 1);
+    rcc.resize(D + 1);
+    dgr.resize(D + 1);
+    dgc.resize(D + 1);
+    Tr.resize(D + 1);
+    Tc.resize(D + 1);
+    Tg.resize(D + 1);
+    Bp.resize(D + 1);
+    PA.resize(D + 1);
+    PB.resize(D + 1);
+    LA.resize(D + 2);
+    RB.resize(D + 2);
+  }
+
+  size_t sz(size_t count, int r, int c) const { return count * size_t(r) * c * W; }
+
+  // ---- launchers -----------------------------------------------------------
+  template <int TM, int TN>
+  void launch_seg(const SegParams& sp, int tiles) {
+    dim3 grid(sp.n_out, tiles);
+    if (cplx) {
+      seg_gemm_kernel<TM, TN, true><<<grid, 128, SegCfg<TM, TN, true>::SMEM, s>>>(sp);
+    } else {
+      seg_gemm_kernel<TM, TN, false><<<grid, 128, SegCfg<TM, TN, false>::SMEM, s>>>(sp);
+    }
+    CK(cudaGetLastError());
+    launches++;
+  }
+
+  void seg(double* out, long long Os, long long Ooff, int Old, const int* omap, int M, int N, int n_out,
+           bool acc, std::initializer_list<Grp> gs) {
+    if (n_out <= 0) return;
+    SegParams sp{};
+    sp.out = out;
+    sp.Os = Os;
+    sp.Ooff = Ooff;
+    sp.Old = Old;
+    sp.omap = omap;
+    sp.M = M;
+    sp.N = N;
+    sp.n_out = n_out;
+    sp.accumulate = acc ? 1 : 0;
+    int ng = 0;
+    for (const Grp& g : gs) {
+      const int64_t entries = g.csr ? g.csr->entries : n_out;
+      if (entries == 0) continue;
+      if (ng >= kMaxGroups) throw std::logic_error("seg: too many groups");
+      SegGroup& G = sp.g[ng++];
+      G.L = g.L.p;
+      G.Ls = g.L.s;
+      G.Loff = g.L.off;
+      G.Lld = g.L.ld;
+      G.opL = g.L.op;
+      G.R = g.R.p;
+      G.Rs = g.R.s;
+      G.Roff = g.R.off;
+      G.Rld = g.R.ld;
+      G.opR = g.R.op;
+      G.K = g.K;
+      if (g.csr) {
+        G.ptr = g.csr->ptr;
+        G.li = g.csr->li;
+        G.ri = g.csr->ri;
+      } else {
+        G.ptr = nullptr;
+        G.li = g.li;
+        G.ri = g.ri;
+      }
+      exec_macs += entries * int64_t(M) * N * g.K;
+    }
+    sp.ngroups = ng;
+    if (ng == 0 && acc) return;
+    const int TM = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
+    const int TN = N <= 16 ? 16 : (N <= 32 ? 32 : 64);
+    const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
+    if (TM == 16 && TN == 16) launch_seg<16, 16>(sp, tiles);
+    else if (TM == 16 && TN == 32) launch_seg<16, 32>(sp, tiles);
+    else if (TM == 16 && TN == 64) launch_seg<16, 64>(sp, tiles);
+    else if (TM == 32 && TN == 16) launch_seg<32, 16>(sp, tiles);
+    else if (TM == 32 && TN == 32) launch_seg<32, 32>(sp, tiles);
+    else if (TM == 32 && TN == 64) launch_seg<32, 64>(sp, tiles);
+    else if (TM == 64 && TN == 16) launch_seg<64, 16>(sp, tiles);
+    else if (TM == 64 && TN == 32) launch_seg<64, 32>(sp, tiles);
+    else launch_seg<64, 64>(sp, tiles);
+  }
+  // convenience: densely stored output [n_out][M x N]
+  void segd(double* out, int M, int N, int n_out, std::initializer_list<Grp> gs) {
+    seg(out, (long long)M * N, 0, M, nullptr, M, N, n_out, false, gs);
+  }
+
+  static Ref ref(const double* p, long long stride, int ld, int op, long long off = 0) {
+    return Ref{p, stride, off, ld, op};
+  }
+
+  void seg_add(double* out, long long Os, const double* in, long long Is, const DevCsr& c, long long elems) {
+    if (c.n_out <= 0) return;
+    const int chunks = static_cast<int>(std::min<long long>(8, (elems / 2 + 255) / 256));
+    seg_add_kernel<<<dim3(c.n_out, std::max(1, chunks)), 256, 0, s>>>(out, Os * W, in, Is * W, c.ptr, c.li,
+                                                                      elems * W, 0);
+    CK(cudaGetLastError());
+    launches++;
+  }
+
+  // combine three Grams and truncate; returns device arrays of ranks/flags and
+  // the sorted eigenvector buffer (n x n per cluster)
+  struct Trunc {
+    DBuf vec, val;
+    DVec<int32_t> rank;
+    DVec<uint8_t> degen;
+  };
+  Trunc truncate(DBuf& g1, DBuf& g2, DBuf& g3, int count, int n, const DVec<uint8_t>& opdeg) {
+    Trunc t;
+    DBuf G(sz(count, n, n), s);
+    t.degen.alloc(count, s);
+    if (cplx)
+      gram_combine_kernel<true><<<count, 256, 0, s>>>(g1, g2, g3, G, (long long)n * n, n * n, opdeg.p, nullptr, t.degen.p);
+    else
+      gram_combine_kernel<false><<<count, 256, 0, s>>>(g1, g2, g3, G, (long long)n * n, n * n, opdeg.p, nullptr, t.degen.p);
+    CK(cudaGetLastError());
+    launches++;
+    g1.release();
+    g2.release();
+    g3.release();
+    t.vec.alloc(sz(count, n, n), s);
+    t.val.alloc(size_t(count) * n, s);
+    t.rank.alloc(count, s);
+    JacobiParams jp{};
+    jp.G = G;
+    jp.vec_out = t.vec;
+    jp.val_out = t.val;
+    jp.rank_out = t.rank.p;
+    jp.degen_io = t.degen.p;
+    jp.n = n;
+    jp.eps = adaptive ? eps : 0.5;
+    jp.max_sweeps = 40;
+    const size_t smem = size_t(2) * n * (n + 1) * W * sizeof(double);
+    DBuf scratch;
+    if (smem <= 200 * 1024) {
+      if (cplx) {
+        CK(cudaFuncSetAttribute(jacobi_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        jacobi_kernel<true, true><<<count, 256, smem, s>>>(jp);
+      } else {
+        CK(cudaFuncSetAttribute(jacobi_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        jacobi_kernel<false, true><<<count, 256, smem, s>>>(jp);
+      }
+    } else {
+      scratch.alloc(size_t(count) * 2 * n * (n + 1) * W, s);
+      jp.scratch = scratch;
+      if (cplx) jacobi_kernel<true, false><<<count, 256, 0, s>>>(jp);
+      else jacobi_kernel<false, false><<<count, 256, 0, s>>>(jp);
+    }
+    CK(cudaGetLastError());
+    launches++;
+    return t;
+  }
+
+  // ranks to host, padded width
+  int fetch_ranks(const DVec<int32_t>& r, int count, std::vector<int64_t>& out) {
+    std::vector<int32_t> h(count);
+    CK(cudaMemcpyAsync(h.data(), r.p, count * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    out.assign(h.begin(), h.end());
+    int64_t mx = 0;
+    for (auto v : out) mx = std::max(mx, v);
+    return pad8(mx);
+  }
+
+  void pack(const Trunc& t, int count, int n, DBuf& out, int rows, int kc) {
+    out.alloc(sz(count, rows, kc), s);
+    pack_basis_kernel<<<count, 256, 0, s>>>(t.vec, n, out, rows, kc, t.rank.p, W);
+    CK(cudaGetLastError());
+    launches++;
+  }
+
+  void identity(DBuf& out, int count, int n, const DVec<int32_t>& rank) {
+    out.alloc(sz(count, n, n), s);
+    set_identity_kernel<<<count, 256, 0, s>>>(out, n, n, rank.p, W);
+    CK(cudaGetLastError());
+    launches++;
+  }
+
+  void gather(DBuf& out, int count, const double* src, long long Ss, int R, int Cc, const int* idx) {
+    out.alloc(sz(count, 2 * R, 2 * Cc), s);
+    if (count <= 0) return;
+    gather_quad_kernel<<<count, 256, 0, s>>>(out, src, Ss, R, Cc, idx, nullptr, W);
+    CK(cudaGetLastError());
+    launches++;
+  }
+
+  void copy_dev(DBuf& dst, const DBuf& src) {
+    dst.alloc(src.n, s);
+    CK(cudaMemcpyAsync(dst.p, src.p, src.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+
+  // ---- basis products B_j = (V^A_col,j)^T V^B_row,j (mmp.cpp:106-124) --------
+  void basis_products() {
+    const LevelPlan& LL = P.lv[D];
+    Bp[D].alloc(sz(LL.n, A.Kc[D], B.Kr[D]), s);
+    segd(Bp[D], A.Kc[D], B.Kr[D], LL.n,
+         {Grp{ref(A.Vc, (long long)NL * A.Kc[D], NL, OP_T), ref(B.Vr, (long long)NL * B.Kr[D], NL, OP_N), NL,
+              nullptr, nullptr, nullptr}});
+    for (int l = D - 1; l >= 1; --l) {
+      const int n = P.lv[l].n;
+      const int ka1 = A.Kc[l + 1], kb1 = B.Kr[l + 1], ka = A.Kc[l], kb = B.Kr[l];
+      DBuf tmp(sz(2 * size_t(n), ka, kb1), s);
+      for (int c = 0; c < 2; ++c)  // tmp_c = (T^A_col[c])^T B_child(c)
+        seg(tmp.p, (long long)ka * kb1, (long long)c * n * ka * kb1, ka, nullptr, ka, kb1, n, false,
+            {Grp{ref(A.Tc[l], 2LL * ka1 * ka, 2 * ka1, OP_T, (long long)c * ka1),
+                 ref(Bp[l + 1], (long long)ka1 * kb1, ka1, OP_N), ka1, nullptr, nullptr, c ? DP.odd : DP.even}});
+      Bp[l].alloc(sz(n, ka, kb), s);
+      segd(Bp[l], ka, kb, n,
+           {Grp{ref(tmp, (long long)ka * kb1, ka, OP_N), ref(B.Tr[l], 2LL * kb1 * kb, 2 * kb1, OP_N), kb1, nullptr,
+                nullptr, nullptr},
+            Grp{ref(tmp, (long long)ka * kb1, ka, OP_N, (long long)n * ka * kb1),
+                ref(B.Tr[l], 2LL * kb1 * kb, 2 * kb1, OP_N, kb1), kb1, nullptr, nullptr, nullptr}});
+    }
+  }
+
+  // ---- admissible-block factors shared by leaf and upper levels --------------
+  // XA = P^A S^A, LA = XA B_j ; YB = S^B P^B, RB = B_j YB   (mmp.cpp:325-332,389-390)
+  void adm_factors(int l, DBuf& XA, DBuf& YB) {
+    const LevelPlan& L = P.lv[l];
+    const DevLevel& Q = DP.lv[l];
+    const int na = static_cast<int>(L.adm.size());
+    const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l], Kr = KCr[l], Kc = KCc[l];
+    XA.alloc(sz(na, Kr, KAc), s);
+    segd(XA, Kr, KAc, na,
+         {Grp{ref(PA[l], (long long)Kr * KAr, Kr, OP_N), ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), KAr, nullptr,
+              Q.adm_row, nullptr}});
+    seg(LA[l], (long long)Kr * KBr, 0, Kr, Q.adm, Kr, KBr, na, false,
+        {Grp{ref(XA, (long long)Kr * KAc, Kr, OP_N), ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), KAc, nullptr,
+             nullptr, Q.adm_col}});
+    YB.alloc(sz(na, KBr, Kc), s);
+    segd(YB, KBr, Kc, na,
+         {Grp{ref(B.S[l], (long long)KBr * KBc, KBr, OP_N), ref(PB[l], (long long)KBc * Kc, KBc, OP_N), KBc, nullptr,
+              nullptr, Q.adm_col}});
+    seg(RB[l], (long long)KAc * Kc, 0, KAc, Q.adm, KAc, Kc, na, false,
+        {Grp{ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), ref(YB, (long long)KBr * Kc, KBr, OP_N), KBr, nullptr,
+             Q.adm_row, nullptr}});
+  }
+
+  // ---- leaf level (mmp.cpp:245-340) ------------------------------------------
+  void leaf_phase() {
+    const int l = D;
+    const LevelPlan& L = P.lv[l];
+    const DevLevel& Q = DP.lv[l];
+    const int n = L.n, nn = static_cast<int>(L.nearb.size()), na = static_cast<int>(L.adm.size());
+    const int nb = static_cast<int>(L.brow.size());
+    const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l];
+    const long long NN = (long long)NL * NL;
+    const Ref AF = ref(A.F, NN, NL, OP_N), BF = ref(B.F, NN, NL, OP_N);
+    auto op = [](Ref r, int o) { r.op = o; return r; };
+
+    // F^A V^B_row,j and (V^A_col,i)^T F^B (reused by Grams, collects, full targets)
+    DBuf FV(sz(nn, NL, KBr), s), VF(sz(nn, KAc, NL), s);
+    segd(FV, NL, KBr, nn, {Grp{AF, ref(B.Vr, (long long)NL * KBr, NL, OP_N), NL, nullptr, nullptr, Q.near_col}});
+    segd(VF, KAc, NL, nn, {Grp{ref(A.Vc, (long long)NL * KAc, NL, OP_T), BF, NL, nullptr, Q.near_row, nullptr}});
+
+    if (adaptive) {
+      // row Grams (mmp.cpp:164-200)
+      DBuf g1(sz(n, NL, NL), s), g2(sz(n, NL, NL), s), g3(sz(n, NL, NL), s);
+      {
+        DBuf O(sz(nn, NL, NL), s);
+        segd(O, NL, NL, nn, {Grp{BF, op(BF, OP_H), NL, nullptr, nullptr, nullptr}});
+        DBuf H(sz(nn, NL, NL), s);
+        seg_add(H, NN, O, NN, Q.hq, NN);
+        O.release();
+        DBuf Y(sz(nn, NL, NL), s);
+        segd(Y, NL, NL, nn, {Grp{AF, ref(H, NN, NL, OP_N), NL, nullptr, nullptr, nullptr}});
+        segd(g1, NL, NL, n, {Grp{ref(Y, NN, NL, OP_N), op(AF, OP_H), NL, &Q.row_near, nullptr, nullptr}});
+      }
+      segd(g2, NL, NL, n,
+           {Grp{ref(FV, (long long)NL * KBr, NL, OP_N), ref(FV, (long long)NL * KBr, NL, OP_H), KBr, &Q.row_near,
+                nullptr, nullptr}});
+      segd(g3, NL, NL, n,
+           {Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(A.Vr, (long long)NL * KAr, NL, OP_H), KAr, nullptr,
+                nullptr, nullptr}});
+      Trunc tr = truncate(g1, g2, g3, n, NL, A.dgr_d[l]);
+      // column Grams (mmp.cpp:202-238)
+      DBuf c1(sz(n, NL, NL), s), c2(sz(n, NL, NL), s), c3(sz(n, NL, NL), s);
+      {
+        DBuf Kb(sz(nn, NL, NL), s);
+        segd(Kb, NL, NL, nn, {Grp{op(AF, OP_T), op(AF, OP_C), NL, nullptr, nullptr, nullptr}});
+        DBuf H(sz(nn, NL, NL), s);
+        seg_add(H, NN, Kb, NN, Q.hqc, NN);
+        Kb.release();
+        DBuf Y(sz(nn, NL, NL), s);
+        segd(Y, NL, NL, nn, {Grp{op(BF, OP_T), ref(H, NN, NL, OP_N), NL, nullptr, nullptr, nullptr}});
+        segd(c1, NL, NL, n, {Grp{ref(Y, NN, NL, OP_N), op(BF, OP_C), NL, &Q.col_near, nullptr, nullptr}});
+      }
+      segd(c2, NL, NL, n,
+           {Grp{ref(VF, (long long)KAc * NL, KAc, OP_T), ref(VF, (long long)KAc * NL, KAc, OP_C), KAc, &Q.col_near,
+                nullptr, nullptr}});
+      segd(c3, NL, NL, n,
+           {Grp{ref(B.Vc, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_H), KBc, nullptr,
+                nullptr, nullptr}});
+      Trunc tc = truncate(c1, c2, c3, n, NL, B.dgc_d[l]);
+      KCr[l] = fetch_ranks(tr.rank, n, rcr[l]);
+      KCc[l] = fetch_ranks(tc.rank, n, rcc[l]);
+      pack(tr, n, NL, Vr, NL, KCr[l]);
+      pack(tc, n, NL, Vc, NL, KCc[l]);
+      dgr[l] = std::move(tr.degen);
+      dgc[l] = std::move(tc.degen);
+      // projections (mmp.cpp:275-279)
+      PA[l].alloc(sz(n, KCr[l], KAr), s);
+      segd(PA[l], KCr[l], KAr, n,
+           {Grp{ref(Vr, (long long)NL * KCr[l], NL, OP_H), ref(A.Vr, (long long)NL * KAr, NL, OP_N), NL, nullptr,
+                nullptr, nullptr}});
+      PB[l].alloc(sz(n, KBc, KCc[l]), s);
+      segd(PB[l], KBc, KCc[l], n,
+           {Grp{ref(B.Vc, (long long)NL * KBc, NL, OP_T), ref(Vc, (long long)NL * KCc[l], NL, OP_C), NL, nullptr,
+                nullptr, nullptr}});
+    } else {
+      // formatted product: C keeps A's row and B's column bases (mmp.cpp:253-256,265-268)
+      formatted_bases(l);
+      copy_dev(Vr, A.Vr);
+      copy_dev(Vc, B.Vc);
+      identity(PA[l], n, KAr, A.rr_d[l]);
+      identity(PB[l], n, KBc, B.rc_d[l]);
+    }
+    const int Kr = KCr[l], Kc = KCc[l];
+
+    // collected full blocks (mmp.cpp:287-298) and W factors of the F x F case
+    LA[l].alloc(sz(nb, Kr, KBr), s);
+    RB[l].alloc(sz(nb, KAc, Kc), s);
+    seg(LA[l], (long long)Kr * KBr, 0, Kr, Q.nearb, Kr, KBr, nn, false,
+        {Grp{ref(Vr, (long long)NL * Kr, NL, OP_H), ref(FV, (long long)NL * KBr, NL, OP_N), NL, nullptr, Q.near_row,
+             nullptr}});
+    seg(RB[l], (long long)KAc * Kc, 0, KAc, Q.nearb, KAc, Kc, nn, false,
+        {Grp{ref(VF, (long long)KAc * NL, KAc, OP_N), ref(Vc, (long long)NL * Kc, NL, OP_C), NL, nullptr, nullptr,
+             Q.near_col}});
+    DBuf WA(sz(nn, Kr, NL), s), WB(sz(nn, NL, Kc), s);
+    segd(WA, Kr, NL, nn, {Grp{ref(Vr, (long long)NL * Kr, NL, OP_H), AF, NL, nullptr, Q.near_row, nullptr}});
+    segd(WB, NL, Kc, nn, {Grp{BF, ref(Vc, (long long)NL * Kc, NL, OP_C), NL, nullptr, nullptr, Q.near_col}});
+    DBuf XA, YB;
+    adm_factors(l, XA, YB);
+
+    // coupling targets: admissible C blocks + pending pairs (mmp.cpp:319-334)
+    const int nt = L.n_targets();
+    Tg[l].alloc(sz(nt, Kr, Kc), s);
+    segd(Tg[l], Kr, Kc, nt,
+         {Grp{ref(LA[l], (long long)Kr * KBr, Kr, OP_N), ref(YB, (long long)KBr * Kc, KBr, OP_N), KBr, &Q.ly, nullptr,
+              nullptr},
+          Grp{ref(XA, (long long)Kr * KAc, Kr, OP_N), ref(RB[l], (long long)KAc * Kc, KAc, OP_N), KAc, &Q.xr,
+              nullptr, nullptr},
+          Grp{ref(WA, (long long)Kr * NL, Kr, OP_N), ref(WB, (long long)NL * Kc, NL, OP_N), NL, &Q.ww,
+              nullptr, nullptr}});
+    WA.release();
+    WB.release();
+    XA.release();
+    YB.release();
+
+    // full targets (mmp.cpp:310-317): C.full = FF + (sum FV S^B) V^B^T + V^A (sum S^A VF + (sum S^A B S^B) V^B^T)
+    {
+      DBuf SB(sz(na, KAr, KBr), s);
+      segd(SB, KAr, KBr, na,
+           {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), KAc,
+                nullptr, nullptr, Q.adm_col}});
+      const Ref BS = ref(B.S[l], (long long)KBr * KBc, KBr, OP_N);
+      DBuf T2(sz(nn, NL, KBc), s), T4(sz(nn, KAr, KBc), s), U(sz(nn, KAr, NL), s);
+      segd(T2, NL, KBc, nn, {Grp{ref(FV, (long long)NL * KBr, NL, OP_N), BS, KBr, &Q.fr, nullptr, nullptr}});
+      segd(T4, KAr, KBc, nn, {Grp{ref(SB, (long long)KAr * KBr, KAr, OP_N), BS, KBr, &Q.rr, nullptr, nullptr}});
+      segd(U, KAr, NL, nn,
+           {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(VF, (long long)KAc * NL, KAc, OP_N), KAc, &Q.rf,
+                nullptr, nullptr},
+            Grp{ref(T4, (long long)KAr * KBc, KAr, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
+                nullptr, Q.near_col}});
+      F.alloc(sz(nn, NL, NL), s);
+      segd(F, NL, NL, nn,
+           {Grp{AF, BF, NL, &Q.ff, nullptr, nullptr},
+            Grp{ref(T2, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
+                nullptr, Q.near_col},
+            Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(U, (long long)KAr * NL, KAr, OP_N), KAr, nullptr,
+                Q.near_row, nullptr}});
+    }
+  }
+
+  void formatted_bases(int l) {
+    KCr[l] = A.Kr[l];
+    KCc[l] = B.Kc[l];
+    rcr[l] = A.rr[l];
+    rcc[l] = B.rc[l];
+    dgr[l].upload(A.dgr[l], s);
+    dgc[l].upload(B.dgc[l], s);
+  }
+
+  // ---- upper levels (mmp.cpp:555-613) ----------------------------------------
+  void upper_level(int l) {
+    const LevelPlan& L = P.lv[l];
+    const LevelPlan& Lc = P.lv[l + 1];
+    const DevLevel& Q = DP.lv[l];
+    const int n = L.n, ns = static_cast<int>(L.nearb.size());
+    const int nm = static_cast<int>(L.merged_row.size()), nb = static_cast<int>(L.brow.size());
+    const int Kn = KCr[l + 1], Kq = KCc[l + 1];
+    const int KAr1 = A.Kr[l + 1], KAc1 = A.Kc[l + 1], KBr1 = B.Kr[l + 1], KBc1 = B.Kc[l + 1];
+    const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l];
+    const long long MM = 4LL * Kn * Kq;
+
+    // merged children couplings and assembled collected blocks (mmp.cpp:344-404)
+    DBuf Mg, Aa, Ab;
+    gather(Mg, nm, Tg[l + 1].p + size_t(Lc.adm.size()) * Kn * Kq * W, (long long)Kn * Kq, Kn, Kq, Q.merged_quad);
+    gather(Aa, ns, LA[l + 1], (long long)Kn * KBr1, Kn, KBr1, Q.sub_child);
+    gather(Ab, ns, RB[l + 1], (long long)KAc1 * Kq, KAc1, Kq, Q.sub_child);
+    LA[l + 1].release();
+    RB[l + 1].release();
+
+    // X = asm_a T^B_row (row Gram term 2, collect); Xc = asm_b^T T^A_col
+    DBuf X(sz(ns, 2 * Kn, KBr), s), Xc(sz(ns, 2 * Kq, KAc), s);
+    segd(X, 2 * Kn, KBr, ns,
+         {Grp{ref(Aa, 4LL * Kn * KBr1, 2 * Kn, OP_N), ref(B.Tr[l], 2LL * KBr1 * KBr, 2 * KBr1, OP_N), 2 * KBr1,
+              nullptr, nullptr, Q.near_col}});
+    segd(Xc, 2 * Kq, KAc, ns,
+         {Grp{ref(Ab, 4LL * KAc1 * Kq, 2 * KAc1, OP_T), ref(A.Tc[l], 2LL * KAc1 * KAc, 2 * KAc1, OP_N), 2 * KAc1,
+              nullptr, nullptr, Q.near_row}});
+    Aa.release();
+    Ab.release();
+
+    if (adaptive) {
+      // X3 = blkdiag(P^A_children) T^A_row ; X3c = blkdiag(P^B)^T conj(T^B_col) ; Y3 = blkdiag(P^B)^T T^B_col
+      DBuf X3(sz(n, 2 * Kn, KAr), s), X3c(sz(n, 2 * Kq, KBc), s), Y3;
+      for (int c = 0; c < 2; ++c) {
+        seg(X3, 2LL * Kn * KAr, (long long)c * Kn, 2 * Kn, nullptr, Kn, KAr, n, false,
+            {Grp{ref(PA[l + 1], (long long)Kn * KAr1, Kn, OP_N),
+                 ref(A.Tr[l], 2LL * KAr1 * KAr, 2 * KAr1, OP_N, (long long)c * KAr1), KAr1, nullptr,
+                 c ? DP.odd : DP.even, nullptr}});
+        seg(X3c, 2LL * Kq * KBc, (long long)c * Kq, 2 * Kq, nullptr, Kq, KBc, n, false,
+            {Grp{ref(PB[l + 1], (long long)KBc1 * Kq, KBc1, OP_T),
+                 ref(B.Tc[l], 2LL * KBc1 * KBc, 2 * KBc1, OP_C, (long long)c * KBc1), KBc1, nullptr,
+                 c ? DP.odd : DP.even, nullptr}});
+      }
+      if (cplx) {
+        Y3.alloc(sz(n, 2 * Kq, KBc), s);
+        for (int c = 0; c < 2; ++c)
+          seg(Y3, 2LL * Kq * KBc, (long long)c * Kq, 2 * Kq, nullptr, Kq, KBc, n, false,
+              {Grp{ref(PB[l + 1], (long long)KBc1 * Kq, KBc1, OP_T),
+                   ref(B.Tc[l], 2LL * KBc1 * KBc, 2 * KBc1, OP_N, (long long)c * KBc1), KBc1, nullptr,
+                   c ? DP.odd : DP.even, nullptr}});
+      }
+      // row transfer Gram (mmp.cpp:406-457)
+      DBuf g1(sz(n, 2 * Kn, 2 * Kn), s), g2(sz(n, 2 * Kn, 2 * Kn), s), g3(sz(n, 2 * Kn, 2 * Kn), s);
+      segd(g1, 2 * Kn, 2 * Kn, n,
+           {Grp{ref(Mg, MM, 2 * Kn, OP_N), ref(Mg, MM, 2 * Kn, OP_H), 2 * Kq, &Q.row_merged, nullptr, nullptr}});
+      segd(g2, 2 * Kn, 2 * Kn, n,
+           {Grp{ref(X, 2LL * Kn * KBr, 2 * Kn, OP_N), ref(X, 2LL * Kn * KBr, 2 * Kn, OP_H), KBr, &Q.row_near,
+                nullptr, nullptr}});
+      segd(g3, 2 * Kn, 2 * Kn, n,
+           {Grp{ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_N), ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_H), KAr, nullptr, nullptr,
+                nullptr}});
+      Trunc tr = truncate(g1, g2, g3, n, 2 * Kn, A.dgr_d[l]);
+      // column transfer Gram (mmp.cpp:459-512)
+      DBuf c1(sz(n, 2 * Kq, 2 * Kq), s), c2(sz(n, 2 * Kq, 2 * Kq), s), c3(sz(n, 2 * Kq, 2 * Kq), s);
+      segd(c1, 2 * Kq, 2 * Kq, n,
+           {Grp{ref(Mg, MM, 2 * Kn, OP_T), ref(Mg, MM, 2 * Kn, OP_C), 2 * Kn, &Q.col_merged, nullptr, nullptr}});
+      segd(c2, 2 * Kq, 2 * Kq, n,
+           {Grp{ref(Xc, 2LL * Kq * KAc, 2 * Kq, OP_N), ref(Xc, 2LL * Kq * KAc, 2 * Kq, OP_H), KAc, &Q.col_near,
+                nullptr, nullptr}});
+      segd(c3, 2 * Kq, 2 * Kq, n,
+           {Grp{ref(X3c, 2LL * Kq * KBc, 2 * Kq, OP_N), ref(X3c, 2LL * Kq * KBc, 2 * Kq, OP_H), KBc, nullptr, nullptr,
+                nullptr}});
+      Trunc tc = truncate(c1, c2, c3, n, 2 * Kq, B.dgc_d[l]);
+      KCr[l] = fetch_ranks(tr.rank, n, rcr[l]);
+      KCc[l] = fetch_ranks(tc.rank, n, rcc[l]);
+      pack(tr, n, 2 * Kn, Tr[l], 2 * Kn, KCr[l]);
+      pack(tc, n, 2 * Kq, Tc[l], 2 * Kq, KCc[l]);
+      dgr[l] = std::move(tr.degen);
+      dgc[l] = std::move(tc.degen);
+      // projections (mmp.cpp:515-537): P^A = T^C^H X3, P^B = Y3^T conj(T^C_col)
+      PA[l].alloc(sz(n, KCr[l], KAr), s);
+      segd(PA[l], KCr[l], KAr, n,
+           {Grp{ref(Tr[l], 2LL * Kn * KCr[l], 2 * Kn, OP_H), ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_N), 2 * Kn, nullptr,
+                nullptr, nullptr}});
+      PB[l].alloc(sz(n, KBc, KCc[l]), s);
+      const double* y3 = cplx ? Y3.p : X3c.p;
+      segd(PB[l], KBc, KCc[l], n,
+           {Grp{ref(y3, 2LL * Kq * KBc, 2 * Kq, OP_T), ref(Tc[l], 2LL * Kq * KCc[l], 2 * Kq, OP_C), 2 * Kq, nullptr,
+                nullptr, nullptr}});
+    } else {
+      formatted_bases(l);
+      copy_dev(Tr[l], A.Tr[l]);
+      copy_dev(Tc[l], B.Tc[l]);
+      identity(PA[l], n, KAr, A.rr_d[l]);
+      identity(PB[l], n, KBc, B.rc_d[l]);
+    }
+    PA[l + 1].release();
+    PB[l + 1].release();
+    Bp[l + 1].release();
+    const int Kr = KCr[l], Kc = KCc[l];
+
+    // collects of subdivided blocks (mmp.cpp:544-552)
+    LA[l].alloc(sz(nb, Kr, KBr), s);
+    RB[l].alloc(sz(nb, KAc, Kc), s);
+    seg(LA[l], (long long)Kr * KBr, 0, Kr, Q.nearb, Kr, KBr, ns, false,
+        {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), ref(X, 2LL * Kn * KBr, 2 * Kn, OP_N), 2 * Kn, nullptr,
+             Q.near_row, nullptr}});
+    seg(RB[l], (long long)KAc * Kc, 0, KAc, Q.nearb, KAc, Kc, ns, false,
+        {Grp{ref(Xc, 2LL * Kq * KAc, 2 * Kq, OP_T), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, nullptr,
+             nullptr, Q.near_col}});
+    X.release();
+    Xc.release();
+    DBuf XA, YB;
+    adm_factors(l, XA, YB);
+
+    // targets: case 1 over merged (T^C^H M conj(T^C)), cases 2-4 (mmp.cpp:573-612)
+    DBuf Z(sz(nm, Kr, 2 * Kq), s);
+    segd(Z, Kr, 2 * Kq, nm,
+         {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), ref(Mg, MM, 2 * Kn, OP_N), 2 * Kn, nullptr, Q.merged_row,
+              nullptr}});
+    Mg.release();
+    const int nt = L.n_targets();
+    Tg[l].alloc(sz(nt, Kr, Kc), s);
+    segd(Tg[l], Kr, Kc, nt,
+         {Grp{ref(Z, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, &Q.mg, nullptr,
+              nullptr},
+          Grp{ref(LA[l], (long long)Kr * KBr, Kr, OP_N), ref(YB, (long long)KBr * Kc, KBr, OP_N), KBr, &Q.ly, nullptr,
+              nullptr},
+          Grp{ref(XA, (long long)Kr * KAc, Kr, OP_N), ref(RB[l], (long long)KAc * Kc, KAc, OP_N), KAc, &Q.xr,
+              nullptr, nullptr}});
+  }
+
+  // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------
+  void split() {
+    for (int l = 1; l < D; ++l) {
+      const LevelPlan& L = P.lv[l];
+      const LevelPlan& Lc = P.lv[l + 1];
+      const DevLevel& Q = DP.lv[l];
+      const int nnl = static_cast<int>(L.nl_block.size());
+      if (nnl == 0) continue;
+      const int Kr = KCr[l], Kc = KCc[l], Kn = KCr[l + 1], Kq = KCc[l + 1];
+      const long long first = (long long)(L.adm.size() + L.pend_row.size()) * Kr * Kc;
+      DBuf Qb(sz(nnl, Kr, 2 * Kq), s);  // NL * T^C_col^T
+      segd(Qb, Kr, 2 * Kq, nnl,
+           {Grp{ref(Tg[l], (long long)Kr * Kc, Kr, OP_N, first), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_T), Kc, nullptr,
+                nullptr, Q.nl_col}});
+      for (int q = 0; q < 4; ++q) {
+        const int ri = q >> 1, ci = q & 1;
+        const Ref TL = ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_N, (long long)ri * Kn);
+        const Ref QR = ref(Qb, 2LL * Kr * Kq, Kr, OP_N, (long long)ci * Kq * Kr);
+        if (Q.sp_n[q] > 0)
+          seg(Tg[l + 1], (long long)Kn * Kq, 0, Kn, Q.sp_omap[q], Kn, Kq, Q.sp_n[q], true,
+              {Grp{TL, QR, Kr, nullptr, Q.sp_prow[q], Q.sp_src[q]}});
+        if (Q.sf_n[q] > 0) {  // leaf children: C.full += V^C_row contrib V^C_col^T
+          const int m = Q.sf_n[q];
+          DBuf Dn(sz(m, Kn, Kq), s), E(sz(m, Kn, NL), s);
+          segd(Dn, Kn, Kq, m, {Grp{TL, QR, Kr, nullptr, Q.sf_prow[q], Q.sf_src[q]}});
+          segd(E, Kn, NL, m,
+               {Grp{ref(Dn, (long long)Kn * Kq, Kn, OP_N), ref(Vc, (long long)NL * Kq, NL, OP_T), Kq, nullptr, nullptr,
+                    Q.sf_ccol[q]}});
+          seg(F, (long long)NL * NL, 0, NL, Q.sf_near[q], NL, NL, m, true,
+              {Grp{ref(Vr, (long long)NL * Kn, NL, OP_N), ref(E, (long long)Kn * NL, Kn, OP_N), Kn, nullptr,
+                   Q.sf_crow[q], nullptr}});
+        }
+      }
+      (void)Lc;
+    }
+  }
+
+  void run() {
+    basis_products();
+    leaf_phase();
+    for (int l = D - 1; l >= 1; --l) upper_level(l);
+    split();
+  }
+
+  // ---- output in the flat layout (row bases, col bases by id, then blocks) ----
+  void download(const h2c_blocks& blocks, HostResult& out, std::vector<double*>& pinned_pool) {
+    (void)pinned_pool;
+    const int nc = static_cast<int>(P.n_clusters);
+    out.scalar = cplx ? H2C_COMPLEX : H2C_REAL;
+    out.row_rank.assign(nc, 0);
+    out.col_rank.assign(nc, 0);
+    out.row_dg.assign(nc, 0);
+    out.col_dg.assign(nc, 0);
+    out.row_off.assign(nc, -1);
+    out.col_off.assign(nc, -1);
+    out.block_off.assign(blocks.n_blocks, -1);
+    std::vector<std::vector<uint8_t>> hr(D + 1), hc(D + 1);
+    for (int l = (D == 0 ? 0 : 1); l <= D; ++l) {
+      const int n = P.lv[l].n;
+      hr[l].resize(n);
+      hc[l].resize(n);
+      CK(cudaMemcpyAsync(hr[l].data(), dgr[l].p, n, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(hc[l].data(), dgc[l].p, n, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    int64_t total = 0;
+    CopyList cl;
+    struct Job {
+      const double* src;
+      int64_t dst;
+      int rows, cols, sld, dld;
+    };
+    std::vector<Job> jobs;
+    std::vector<int> lev(nc, 0);
+    for (int m = 0; m <= D; ++m)
+      for (int id : P.lv[m].id) lev[id] = m;
+    for (int side = 0; side < 2; ++side)
+      for (int id = 0; id < nc; ++id) {
+        const int m = lev[id], p = P.pos_of[id];
+        if (m == 0 && D > 0) continue;  // the non-leaf root carries no basis
+        auto& rk = side == 0 ? rcr : rcc;
+        const int r = static_cast<int>(rk[m][p]);
+        (side == 0 ? out.row_rank : out.col_rank)[id] = r;
+        (side == 0 ? out.row_dg : out.col_dg)[id] = (side == 0 ? hr : hc)[m][p];
+        (side == 0 ? out.row_off : out.col_off)[id] = total;
+        if (m == D) {
+          const int K = side == 0 ? KCr[D] : KCc[D];
+          const double* src = (side == 0 ? Vr.p : Vc.p) + size_t(p) * NL * K * W;
+          const int rows = P.lv[D].size[p];
+          jobs.push_back({src, total, rows, r, NL, rows});
+          total += int64_t(rows) * r;
+        } else {
+          const int K1 = side == 0 ? KCr[m + 1] : KCc[m + 1];
+          const int K0 = side == 0 ? KCr[m] : KCc[m];
+          const int c0 = static_cast<int>(rk[m + 1][2 * p]), c1 = static_cast<int>(rk[m + 1][2 * p + 1]);
+          const double* base = (side == 0 ? Tr[m].p : Tc[m].p) + size_t(p) * 2 * K1 * K0 * W;
+          // stacked [T_c1; T_c2] of shape (c0 + c1) x r from the two padded row slots
+          jobs.push_back({base, total, c0, r, 2 * K1, c0 + c1});
+          jobs.push_back({base + size_t(K1) * W, total + c0, c1, r, 2 * K1, c0 + c1});
+          total += int64_t(c0 + c1) * r;
+        }
+      }
+    // blocks in global order
+    std::vector<std::pair<int, int>> where(blocks.n_blocks, {-1, -1});
+    for (int m = 0; m <= D; ++m)
+      for (size_t b = 0; b < P.lv[m].bglobal.size(); ++b) where[P.lv[m].bglobal[b]] = {m, static_cast<int>(b)};
+    for (int64_t g = 0; g < blocks.n_blocks; ++g) {
+      const auto [m, b] = where[g];
+      const LevelPlan& L = P.lv[m];
+      if (L.bkind[b] == kAdm) {
+        const int a = L.kidx[b];
+        const int rr = static_cast<int>(rcr[m][L.brow[b]]), rc = static_cast<int>(rcc[m][L.bcol[b]]);
+        out.block_off[g] = total;
+        jobs.push_back({Tg[m].p + size_t(a) * KCr[m] * KCc[m] * W, total, rr, rc, KCr[m], rr});
+        total += int64_t(rr) * rc;
+      } else if (L.bkind[b] == kFull) {
+        const int q = L.kidx[b];
+        const int nr = L.size[L.brow[b]], ncl = L.size[L.bcol[b]];
+        out.block_off[g] = total;
+        jobs.push_back({F.p + size_t(q) * NL * NL * W, total, nr, ncl, NL, nr});
+        total += int64_t(nr) * ncl;
+      }
+    }
+    DBuf flat(size_t(total) * W, s);
+    for (const Job& j : jobs) cl.add(j.src, flat.p + j.dst * W, j.rows, j.cols, j.sld, j.dld);
+    cl.run(s, W, &launches);
+    out.n_values = total;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&out.values), std::max<size_t>(1, size_t(total) * W * sizeof(double))));
+    if (total)
+      CK(cudaMemcpyAsync(out.values, flat.p, size_t(total) * W * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+};
+
+HostResult::~HostResult() {
+  if (values) cudaFreeHost(values);
+}
+
+// ---------------------------------------------------------------------------
+uint64_t structure_hash(const h2c_tree& t, const h2c_blocks& b) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+  };
+  mix(&t.n_points, sizeof(int32_t));
+  mix(&t.depth, sizeof(int32_t));
+  mix(&t.n_clusters, sizeof(int32_t));
+  mix(t.parent, sizeof(int32_t) * t.n_clusters);
+  mix(t.begin, sizeof(int32_t) * t.n_clusters);
+  mix(t.end, sizeof(int32_t) * t.n_clusters);
+  mix(t.level, sizeof(int32_t) * t.n_clusters);
+  mix(&b.n_blocks, sizeof(int64_t));
+  mix(b.row, sizeof(int32_t) * b.n_blocks);
+  mix(b.col, sizeof(int32_t) * b.n_blocks);
+  mix(b.kind, b.n_blocks);
+  mix(b.level_ptr, sizeof(int64_t) * (b.depth + 2));
+  return h;
+}
+
+Context::Context(int device) : device_(device) {
+  CK(cudaSetDevice(device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  stream_ = st;
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+}
+
+Context::~Context() {
+  dplan_.reset();
+  if (stream_) {
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
+    cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+  }
+}
+
+const Plan& Context::plan_for(const h2c_tree& t, const h2c_blocks& b, double* build_seconds) {
+  const uint64_t key = structure_hash(t, b);
+  if (plan_ && key == plan_key_) {
+    if (build_seconds) *build_seconds = 0.0;
+    return *plan_;
+  }
+  CK(cudaSetDevice(device_));
+  dplan_.reset();
+  plan_ = std::make_unique<Plan>(build_plan(t, b, std::max(1u, std::thread::hardware_concurrency())));
+  dplan_ = upload_plan(*plan_, static_cast<cudaStream_t>(stream_));
+  plan_key_ = key;
+  if (build_seconds) *build_seconds = plan_->build_seconds;
+  return *plan_;
+}
+
+std::shared_ptr<DevOperand> Context::upload(const h2c_matrix& m) {
+  double bs = 0;
+  const Plan& P = plan_for(*m.tree, *m.blocks, &bs);
+  auto X = upload_operand(P, m, static_cast<cudaStream_t>(stream_), &launches_);
+  X->key = plan_key_;
+  return X;
+}
+
+static void fill_report(const Plan& P, const DevOperand& A, const DevOperand& B, EngineRun& R, bool adaptive,
+                        double eps, HostResult& out) {
+  RankSet rs;
+  rs.ar = A.rr;
+  rs.ac = A.rc;
+  rs.br = B.rr;
+  rs.bc = B.rc;
+  rs.cr = R.rcr;
+  rs.cc = R.rcc;
+  for (int l = 0; l <= P.depth; ++l) {
+    const size_t n = P.lv[l].n;
+    if (rs.cr[l].size() != n) rs.cr[l].assign(n, 0);
+    if (rs.cc[l].size() != n) rs.cc[l].assign(n, 0);
+  }
+  CountOut co;
+  count_report(P, rs, adaptive, co);
+  out.eps_trunc = adaptive ? eps : 0.0;
+  out.adaptive = adaptive ? 1 : 0;
+  out.flops = co.flops;
+  out.case_flops = co.case_flops;
+  out.flops_exec = R.exec_macs;
+  out.max_row.clear();
+  out.max_col.clear();
+  out.case_products.clear();
+  out.t1.clear();
+  out.t2.clear();
+  out.t3.clear();
+  for (const LevelCount& c : co.levels) {
+    out.max_row.push_back(c.max_row_rank);
+    out.max_col.push_back(c.max_col_rank);
+    for (int k = 0; k < 4; ++k) out.case_products.push_back(c.case_products[k]);
+    out.t1.push_back(c.max_case1_terms);
+    out.t2.push_back(c.max_case2_terms);
+    out.t3.push_back(c.max_case3_terms);
+  }
+}
+
+double Context::run_resident(const std::shared_ptr<DevOperand>& a, const std::shared_ptr<DevOperand>& b,
+                             double eps, int adaptive, HostResult* out) {
+  if (!plan_ || a->key != plan_key_ || b->key != plan_key_)
+    throw ConfigErr("mmp: operands were uploaded for another structure");
+  if (a->scalar != b->scalar) throw ConfigErr("mmp: operands must share the scalar type");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  CK(cudaSetDevice(device_));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(cudaEventRecord(e0, s));
+  EngineRun R(*this, *plan_, *dplan_, *a, *b, eps, adaptive != 0, s);
+  R.run();
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  launches_ = R.launches;
+  if (out) {
+    h2c_blocks dummy{};
+    (void)dummy;
+    fill_report(*plan_, *a, *b, R, adaptive != 0, eps, *out);
+    out->device_seconds = ms * 1e-3;
+    out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return ms * 1e-3;
+}
+
+void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adaptive, HostResult& out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (a.tree != b.tree || a.blocks != b.blocks)  // mmp.cpp:58-63
+    throw ConfigErr("mmp: operands must share cluster trees and block structure");
+  if (a.scalar != b.scalar) throw ConfigErr("mmp: operands must share the scalar type");
+  if (adaptive && !(eps > 0.0 && eps < 1.0)) throw ConfigErr("mmp: eps_trunc must be in (0,1)");
+  CK(cudaSetDevice(device_));
+  double plan_s = 0;
+  const Plan& P = plan_for(*a.tree, *a.blocks, &plan_s);
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  int64_t up_launches = 0;
+  auto A = upload_operand(P, a, s, &up_launches);
+  std::shared_ptr<DevOperand> B = (&a == &b || a.values == b.values) ? A : upload_operand(P, b, s, &up_launches);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  EngineRun R(*this, P, *dplan_, *A, *B, eps, adaptive != 0, s);
+  R.run();
+  CK(cudaEventRecord(e1, s));
+  std::vector<double*> pool;
+  R.download(*a.blocks, out, pool);
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  launches_ = R.launches + up_launches;
+  fill_report(P, *A, *B, R, adaptive != 0, eps, out);
+  out.device_seconds = ms * 1e-3;
+  out.plan_seconds = plan_s;
+  out.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace h2b

@@ -1,0 +1,75 @@
+// B200 MMP engine: level-synchronous device pipeline (see engine.cu).
+#pragma once
+
+#include <array>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace h2b {
+
+struct DevPlan;  // device copies of the plan's index lists
+
+// Host-side result of one product (flat layout of include/h2c_types.h).
+struct HostResult {
+  int32_t scalar = 0;
+  std::vector<int32_t> row_rank, col_rank;
+  std::vector<uint8_t> row_dg, col_dg;
+  std::vector<int64_t> row_off, col_off, block_off;
+  double* values = nullptr;  // pinned host memory owned by the result
+  int64_t n_values = 0;
+  // report
+  double eps_trunc = 0;
+  int adaptive = 1;
+  int64_t flops = 0, flops_exec = 0;
+  std::array<int64_t, 4> case_flops{0, 0, 0, 0};
+  double wall_seconds = 0, device_seconds = 0, plan_seconds = 0;
+  std::vector<int64_t> max_row, max_col, case_products;
+  std::vector<int32_t> t1, t2, t3;
+  ~HostResult();
+};
+
+// Operand already resident on the device (padded per-level layout).
+struct DevOperand;
+struct DevResult;
+
+class Context {
+ public:
+  explicit Context(int device);
+  ~Context();
+  const std::string& error() const { return err_; }
+  void set_error(const std::string& e) { err_ = e; }
+
+  // plan cache keyed by the structure descriptors' content
+  const Plan& plan_for(const h2c_tree& t, const h2c_blocks& b, double* build_seconds);
+
+  // full drop-in call: host descriptors in, host result out
+  void mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adaptive, HostResult& out);
+
+  // device-resident path (bench `value`): upload once, run many times
+  std::shared_ptr<DevOperand> upload(const h2c_matrix& m);
+  // runs the pipeline on resident operands; returns device seconds (CUDA events)
+  double run_resident(const std::shared_ptr<DevOperand>& a, const std::shared_ptr<DevOperand>& b,
+                      double eps, int adaptive, HostResult* download_to);
+  void* stream() const { return stream_; }
+  int64_t last_kernel_launches() const { return launches_; }
+  // per-kernel-family timings of the last run (name, ms), filled when profiling is on
+  std::vector<std::pair<std::string, double>> last_timings;
+  bool profile = false;
+
+ private:
+  friend struct EngineRun;
+  int device_;
+  void* stream_ = nullptr;
+  std::string err_;
+  uint64_t plan_key_ = 0;
+  std::unique_ptr<Plan> plan_;
+  std::unique_ptr<DevPlan> dplan_;
+  int64_t launches_ = 0;
+};
+
+uint64_t structure_hash(const h2c_tree& t, const h2c_blocks& b);
+
+}  // namespace h2b

@@ -1,0 +1,624 @@
+// sm_100a kernels of the B200 H^2-MMP.
+//
+// FP64 has no tcgen05 kind on sm_100a: the tensor path for
+// double is mma.sync m8n8k4 f64 -> DMMA.8x8x4, measured at 37.1 TFLOP/s on the
+// pool's B200 (profiles/FP64_PEAKS.json).  Every product of the pipeline goes
+// through ONE segmented batched small-GEMM kernel (seg_gemm): for each output
+// block t it accumulates sum_e op(L_e) * op(R_e) over a CSR segment of entries
+// (one CTA per output tile, fixed entry order -> deterministic, no atomics),
+// which covers the per-block products, the Gram sums and the triple sums of
+// the reference's four product cases.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace h2b {
+
+enum OpCode : int { OP_N = 0, OP_T = 1, OP_H = 2, OP_C = 3 };  // none, transpose, adjoint, conjugate
+
+struct SegGroup {
+  const double* L;
+  long long Ls, Loff;  // element stride between matrices, element offset (view)
+  int Lld, opL;
+  const double* R;
+  long long Rs, Roff;
+  int Rld, opR;
+  int K;               // inner dimension (padded)
+  const int* ptr;      // CSR over outputs, or nullptr: exactly one entry per output
+  const int* li;       // entry (or per-output, if ptr==nullptr) left index; nullptr = output index
+  const int* ri;
+};
+
+constexpr int kMaxGroups = 4;
+
+struct SegParams {
+  double* out;
+  long long Os, Ooff;
+  int Old;
+  const int* omap;     // storage index of output t (nullptr = t)
+  int M, N;            // output dims (padded)
+  int n_out;
+  int accumulate;      // out (+)= sum
+  int ngroups;
+  SegGroup g[kMaxGroups];
+};
+
+// ---------------------------------------------------------------------------
+// scalar helpers (complex values are interleaved re, im)
+template <bool CPLX>
+struct Sc;
+template <>
+struct Sc<false> {
+  static constexpr int W = 1;
+};
+template <>
+struct Sc<true> {
+  static constexpr int W = 2;
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// seg_gemm: CTA = 4 warps (2x2), CTA tile TM x TN, k-chunk KC staged in smem
+// as [k][m] / [k][n] (leading dim T+4 -> conflict-free fragment loads), next
+// chunk prefetched into registers while the current one is multiplied.
+template <int TM, int TN, bool CPLX>
+struct SegCfg {
+  static constexpr int KC = CPLX ? 16 : 32;
+  static constexpr int LDL = TM + 4;
+  static constexpr int LDR = TN + 4;
+  static constexpr int PL = (TM * KC) / 128;  // L elements per thread per chunk
+  static constexpr int PR = (TN * KC) / 128;
+  static constexpr int FM = TM / 16;          // 8x8 fragments per warp along m
+  static constexpr int FN = TN / 16;
+  static constexpr int W = CPLX ? 2 : 1;
+  static constexpr int SMEM = (KC * LDL + KC * LDR) * W * 8;
+};
+
+struct Cursor {
+  int g, e, e1, k0;
+  int l, r;
+};
+
+template <int TM, int TN, bool CPLX>
+__global__ void __launch_bounds__(128) seg_gemm_kernel(const SegParams p) {
+  using C = SegCfg<TM, TN, CPLX>;
+  constexpr int KC = C::KC;
+  extern __shared__ __align__(16) double smem[];
+  double* Ls = smem;                          // [W][KC][LDL]
+  double* Rs = smem + C::W * KC * C::LDL;     // [W][KC][LDR]
+
+  const int t = blockIdx.x;
+  const int tilesM = (p.M + TM - 1) / TM;
+  const int m0 = (blockIdx.y % tilesM) * TM;
+  const int n0 = (blockIdx.y / tilesM) * TN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = (warp & 1) * (TM / 2), wn = (warp >> 1) * (TN / 2);
+
+  double acc[C::FM][C::FN][2];
+  double acci[CPLX ? C::FM : 1][CPLX ? C::FN : 1][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if constexpr (CPLX) {
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) acci[i][j][0] = acci[i][j][1] = 0.0;
+  }
+
+  // ---- iteration cursor over (group, entry, k-chunk)
+  auto entry_range = [&](int g, int& e0, int& e1) {
+    const SegGroup& G = p.g[g];
+    if (G.ptr) {
+      e0 = G.ptr[t];
+      e1 = G.ptr[t + 1];
+    } else {
+      e0 = 0;
+      e1 = 1;
+    }
+  };
+  auto load_entry = [&](Cursor& c) {
+    const SegGroup& G = p.g[c.g];
+    if (G.ptr) {
+      c.l = G.li[c.e];
+      c.r = G.ri[c.e];
+    } else {
+      c.l = G.li ? G.li[t] : t;
+      c.r = G.ri ? G.ri[t] : t;
+    }
+  };
+  // advance to the first valid position at or after c (returns false at end)
+  auto settle = [&](Cursor& c) -> bool {
+    while (c.g < p.ngroups) {
+      if (c.e < c.e1 && c.k0 < p.g[c.g].K) return true;
+      if (c.e < c.e1) {  // next entry
+        c.e++;
+        c.k0 = 0;
+        if (c.e < c.e1) {
+          load_entry(c);
+          continue;
+        }
+      }
+      c.g++;
+      if (c.g < p.ngroups) {
+        entry_range(c.g, c.e, c.e1);
+        c.k0 = 0;
+        if (c.e < c.e1) load_entry(c);
+      }
+    }
+    return false;
+  };
+
+  double rl[C::PL * C::W], rr[C::PR * C::W];
+  auto fetch = [&](const Cursor& c) {
+    const SegGroup& G = p.g[c.g];
+    const double* Lp = G.L + (G.Ls * c.l + G.Loff) * C::W;
+    const double* Rp = G.R + (G.Rs * c.r + G.Roff) * C::W;
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+#pragma unroll
+    for (int u = 0; u < C::PL; ++u) {
+      const int e = tid + u * 128;
+      int m, k;
+      if (!lt) { m = e % TM; k = e / TM; }
+      else { k = e % KC; m = e / KC; }
+      const int gm = m0 + m, gk = c.k0 + k;
+      const bool ok = gm < p.M && gk < G.K;
+      const long long off = lt ? (gk + (long long)gm * G.Lld) : (gm + (long long)gk * G.Lld);
+      if constexpr (CPLX) {
+        double2 v = ok ? *reinterpret_cast<const double2*>(Lp + 2 * off) : make_double2(0.0, 0.0);
+        rl[2 * u] = v.x;
+        rl[2 * u + 1] = (G.opL == OP_H || G.opL == OP_C) ? -v.y : v.y;
+      } else {
+        rl[u] = ok ? Lp[off] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < C::PR; ++u) {
+      const int e = tid + u * 128;
+      int n, k;
+      if (rt) { n = e % TN; k = e / TN; }
+      else { k = e % KC; n = e / KC; }
+      const int gn = n0 + n, gk = c.k0 + k;
+      const bool ok = gn < p.N && gk < G.K;
+      const long long off = rt ? (gn + (long long)gk * G.Rld) : (gk + (long long)gn * G.Rld);
+      if constexpr (CPLX) {
+        double2 v = ok ? *reinterpret_cast<const double2*>(Rp + 2 * off) : make_double2(0.0, 0.0);
+        rr[2 * u] = v.x;
+        rr[2 * u + 1] = (G.opR == OP_H || G.opR == OP_C) ? -v.y : v.y;
+      } else {
+        rr[u] = ok ? Rp[off] : 0.0;
+      }
+    }
+  };
+  auto stash = [&](const Cursor& c) {
+    const SegGroup& G = p.g[c.g];
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+#pragma unroll
+    for (int u = 0; u < C::PL; ++u) {
+      const int e = tid + u * 128;
+      int m, k;
+      if (!lt) { m = e % TM; k = e / TM; }
+      else { k = e % KC; m = e / KC; }
+      if constexpr (CPLX) {
+        Ls[k * C::LDL + m] = rl[2 * u];
+        Ls[KC * C::LDL + k * C::LDL + m] = rl[2 * u + 1];
+      } else {
+        Ls[k * C::LDL + m] = rl[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < C::PR; ++u) {
+      const int e = tid + u * 128;
+      int n, k;
+      if (rt) { n = e % TN; k = e / TN; }
+      else { k = e % KC; n = e / KC; }
+      if constexpr (CPLX) {
+        Rs[k * C::LDR + n] = rr[2 * u];
+        Rs[KC * C::LDR + k * C::LDR + n] = rr[2 * u + 1];
+      } else {
+        Rs[k * C::LDR + n] = rr[u];
+      }
+    }
+  };
+
+  Cursor cur;
+  cur.g = 0;
+  cur.k0 = 0;
+  entry_range(0, cur.e, cur.e1);
+  if (cur.e < cur.e1) load_entry(cur);
+  bool have = settle(cur);
+  if (have) fetch(cur);
+  while (have) {
+    __syncthreads();
+    stash(cur);
+    __syncthreads();
+    Cursor nxt = cur;
+    nxt.k0 += KC;
+    const bool more = settle(nxt);
+    if (more) fetch(nxt);  // global loads in flight during the MMAs below
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      double a[C::FM], b[C::FN];
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i) a[i] = Ls[(kk + tq) * C::LDL + wm + 8 * i + gq];
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) b[j] = Rs[(kk + tq) * C::LDR + wn + 8 * j + gq];
+      if constexpr (CPLX) {
+        double ai[C::FM], bi[C::FN];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i) ai[i] = Ls[KC * C::LDL + (kk + tq) * C::LDL + wm + 8 * i + gq];
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) bi[j] = Rs[KC * C::LDR + (kk + tq) * C::LDR + wn + 8 * j + gq];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) {
+            dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            dmma(acc[i][j][0], acc[i][j][1], -ai[i], bi[j]);
+            dmma(acci[i][j][0], acci[i][j][1], a[i], bi[j]);
+            dmma(acci[i][j][0], acci[i][j][1], ai[i], b[j]);
+          }
+      } else {
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    }
+    cur = nxt;
+    have = more;
+  }
+
+  // ---- epilogue: out (+)= acc
+  const int o = p.omap ? p.omap[t] : t;
+  double* Op = p.out + (p.Os * o + p.Ooff) * C::W;
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int m = m0 + wm + 8 * i + gq;
+        const int n = n0 + wn + 8 * j + 2 * tq + q;
+        if (m < p.M && n < p.N) {
+          const long long off = m + (long long)n * p.Old;
+          if constexpr (CPLX) {
+            double re = acc[i][j][q], im = acci[i][j][q];
+            if (p.accumulate) {
+              re += Op[2 * off];
+              im += Op[2 * off + 1];
+            }
+            Op[2 * off] = re;
+            Op[2 * off + 1] = im;
+          } else {
+            double v = acc[i][j][q];
+            if (p.accumulate) v += Op[off];
+            Op[off] = v;
+          }
+        }
+      }
+}
+
+// ---------------------------------------------------------------------------
+// seg_add: out_t = sum_{e in seg(t)} in[idx_e]   (elements = matrix size in doubles)
+__global__ void seg_add_kernel(double* out, long long Os, const double* in, long long Is,
+                               const int* ptr, const int* idx, long long elems, int accumulate) {
+  const int t = blockIdx.x;
+  const int e0 = ptr[t], e1 = ptr[t + 1];
+  for (long long x = (blockIdx.y * (long long)blockDim.x + threadIdx.x) * 2; x < elems;
+       x += (long long)gridDim.y * blockDim.x * 2) {
+    double2 s = make_double2(0.0, 0.0);
+    if (accumulate) s = *reinterpret_cast<const double2*>(out + Os * t + x);
+    for (int e = e0; e < e1; ++e) {
+      const double2 v = *reinterpret_cast<const double2*>(in + Is * idx[e] + x);
+      s.x += v.x;
+      s.y += v.y;
+    }
+    *reinterpret_cast<double2*>(out + Os * t + x) = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gram_combine (mmp.cpp:82-85,192-198): G = sum_i g_i/||g_i||_F (zero terms
+// skipped); pre_degenerate = ||g1|| == 0 && ||g2|| == 0 && operand flag.
+template <bool CPLX>
+__global__ void gram_combine_kernel(const double* g1, const double* g2, const double* g3, double* G,
+                                    long long stride, int elems, const uint8_t* op_degen,
+                                    const int* op_map, uint8_t* pre_degen) {
+  constexpr int W = CPLX ? 2 : 1;
+  const int t = blockIdx.x;
+  const double* src[3] = {g1 + stride * t * W, g2 + stride * t * W, g3 + stride * t * W};
+  __shared__ double red[3][32];
+  double s[3] = {0, 0, 0};
+  for (int x = threadIdx.x; x < elems * W; x += blockDim.x)
+    for (int q = 0; q < 3; ++q) s[q] += src[q][x] * src[q][x];
+  for (int q = 0; q < 3; ++q)
+    for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0)
+    for (int q = 0; q < 3; ++q) red[q][warp] = s[q];
+  __syncthreads();
+  __shared__ double nrm[3];
+  if (threadIdx.x < 3) {
+    double v = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
+    nrm[threadIdx.x] = sqrt(v);
+  }
+  __syncthreads();
+  double* out = G + stride * t * W;
+  for (int x = threadIdx.x; x < elems * W; x += blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < 3; ++q)
+      if (nrm[q] > 0.0) v += src[q][x] / nrm[q];
+    out[x] = v;
+  }
+  if (threadIdx.x == 0) {
+    const int c = op_map ? op_map[t] : t;
+    pre_degen[t] = (nrm[0] == 0.0 && nrm[1] == 0.0 && op_degen[c]) ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batched Hermitian eigensolver for the truncation (truncation.cpp:9-47):
+// two-sided cyclic Jacobi, round-robin parallel ordering (n/2 disjoint
+// rotations per step), one CTA per Gram.  Storage in shared memory when it
+// fits, else in a global scratch (L2-resident).  Output: eigenvectors sorted
+// by descending eigenvalue, rank = #{lambda_i > eps*lambda_max} (>= 1), and
+// the e_1 / degenerate rule for zero Grams.
+struct JacobiParams {
+  const double* G;      // [batch][n*n]
+  double* scratch;      // global storage when !SMEM: [batch][2][n*(n+1)]
+  double* vec_out;      // [batch][n*n] sorted eigenvectors
+  double* val_out;      // [batch][n] sorted clamped eigenvalues
+  int* rank_out;
+  uint8_t* degen_io;    // in: pre-degenerate flag, out: final degenerate flag
+  int n;
+  double eps;
+  int max_sweeps;
+};
+
+template <bool CPLX, bool SMEM>
+__global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
+  constexpr int W = CPLX ? 2 : 1;
+  const int n = p.n, ld = n + 1;
+  const int b = blockIdx.x;
+  extern __shared__ __align__(16) double jsm[];
+  double* A;
+  double* V;
+  if constexpr (SMEM) {
+    A = jsm;
+    V = jsm + (size_t)n * ld * W;
+  } else {
+    A = p.scratch + (size_t)b * 2 * n * ld * W;
+    V = A + (size_t)n * ld * W;
+  }
+  __shared__ double cs_c[256], cs_s[256], cs_pr[256], cs_pi[256];
+  __shared__ int pp[256], qq[256];
+  __shared__ int any_rot, nonzero;
+  __shared__ double fro;
+  const double* G = p.G + (size_t)b * n * n * W;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) { any_rot = 0; nonzero = 0; fro = 0.0; }
+  __syncthreads();
+  double ss = 0.0;
+  int nz = 0;
+  for (int x = tid; x < n * n; x += nt) {
+    const int r = x % n, c = x / n;
+    // Hermitian: use the lower triangle like Eigen's SelfAdjointEigenSolver
+    const int rr = r >= c ? r : c, cc = r >= c ? c : r;
+    const double re = G[(rr + cc * n) * W];
+    const double im = CPLX ? (r >= c ? G[(rr + cc * n) * W + 1] : -G[(rr + cc * n) * W + 1]) : 0.0;
+    if (G[x * W] != 0.0 || (CPLX && G[x * W + 1] != 0.0)) nz = 1;
+    A[(r * ld + c) * W] = re;
+    if (CPLX) A[(r * ld + c) * W + 1] = (r == c) ? 0.0 : im;
+    V[(r * ld + c) * W] = r == c ? 1.0 : 0.0;
+    if (CPLX) V[(r * ld + c) * W + 1] = 0.0;
+    ss += re * re + im * im;
+  }
+  // A is stored row-major A[r*ld + c] = a_rc
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+  }
+  if ((tid & 31) == 0) {
+    atomicAdd(&fro, ss);
+    if (nz) nonzero = 1;
+  }
+  __syncthreads();
+  const double tol_abs = 1e-22 * sqrt(fro);
+  const int half = n / 2;
+  if (nonzero) {
+    for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
+      if (tid == 0) any_rot = 0;
+      __syncthreads();
+      for (int step = 0; step < n - 1; ++step) {
+        for (int i = tid; i < half; i += nt) {
+          auto idx = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + step) % (n - 1)); };
+          int a = idx(i), c = idx(n - 1 - i);
+          const int pq = a < c ? a : c, qv = a < c ? c : a;
+          pp[i] = pq;
+          qq[i] = qv;
+          const double app = A[(pq * ld + pq) * W], aqq = A[(qv * ld + qv) * W];
+          const double br = A[(pq * ld + qv) * W], bi = CPLX ? A[(pq * ld + qv) * W + 1] : 0.0;
+          const double babs = CPLX ? hypot(br, bi) : fabs(br);
+          double c_ = 1.0, s_ = 0.0, pr = 1.0, pi = 0.0;
+          if (babs > tol_abs && babs > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
+            const double tau = (aqq - app) / (2.0 * babs);
+            const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c_ = 1.0 / sqrt(1.0 + tt * tt);
+            s_ = tt * c_;
+            if (CPLX) { pr = br / babs; pi = bi / babs; }  // e^{i phi}
+            else pr = br >= 0 ? 1.0 : -1.0;
+            any_rot = 1;
+          }
+          cs_c[i] = c_;
+          cs_s[i] = s_;
+          cs_pr[i] = pr;
+          cs_pi[i] = pi;
+        }
+        __syncthreads();
+        // rows: row_p <- c row_p - s e^{i phi} row_q ; row_q <- s row_p + c e^{i phi} row_q
+        for (int x = tid; x < half * n; x += nt) {
+          const int i = x / n, k = x % n;
+          const int pq = pp[i], qv = qq[i];
+          const double c_ = cs_c[i], s_ = cs_s[i];
+          if (s_ == 0.0) continue;
+          if constexpr (CPLX) {
+            const double pr = cs_pr[i], pi = cs_pi[i];
+            const double apr = A[(pq * ld + k) * 2], api = A[(pq * ld + k) * 2 + 1];
+            const double aqr = A[(qv * ld + k) * 2], aqi = A[(qv * ld + k) * 2 + 1];
+            const double er = pr * aqr - pi * aqi, ei = pr * aqi + pi * aqr;  // e^{i phi} a_q
+            A[(pq * ld + k) * 2] = c_ * apr - s_ * er;
+            A[(pq * ld + k) * 2 + 1] = c_ * api - s_ * ei;
+            A[(qv * ld + k) * 2] = s_ * apr + c_ * er;
+            A[(qv * ld + k) * 2 + 1] = s_ * api + c_ * ei;
+          } else {
+            const double sg = cs_pr[i];
+            const double ap = A[pq * ld + k], aq = sg * A[qv * ld + k];
+            A[pq * ld + k] = c_ * ap - s_ * aq;
+            A[qv * ld + k] = s_ * ap + c_ * aq;
+          }
+        }
+        __syncthreads();
+        // columns (and V): col_p <- c col_p - s e^{-i phi} col_q ; col_q <- s col_p + c e^{-i phi} col_q
+        for (int x = tid; x < half * n * 2; x += nt) {
+          const int which = x / (half * n);
+          const int y = x % (half * n);
+          const int i = y / n, k = y % n;
+          const int pq = pp[i], qv = qq[i];
+          const double c_ = cs_c[i], s_ = cs_s[i];
+          if (s_ == 0.0) continue;
+          double* M = which == 0 ? A : V;
+          if constexpr (CPLX) {
+            const double pr = cs_pr[i], pi = -cs_pi[i];  // e^{-i phi}
+            const double apr = M[(k * ld + pq) * 2], api = M[(k * ld + pq) * 2 + 1];
+            const double aqr = M[(k * ld + qv) * 2], aqi = M[(k * ld + qv) * 2 + 1];
+            const double er = pr * aqr - pi * aqi, ei = pr * aqi + pi * aqr;
+            M[(k * ld + pq) * 2] = c_ * apr - s_ * er;
+            M[(k * ld + pq) * 2 + 1] = c_ * api - s_ * ei;
+            M[(k * ld + qv) * 2] = s_ * apr + c_ * er;
+            M[(k * ld + qv) * 2 + 1] = s_ * api + c_ * ei;
+          } else {
+            const double sg = cs_pr[i];
+            const double ap = M[k * ld + pq], aq = sg * M[k * ld + qv];
+            M[k * ld + pq] = c_ * ap - s_ * aq;
+            M[k * ld + qv] = s_ * ap + c_ * aq;
+          }
+        }
+        __syncthreads();
+      }
+      if (!any_rot) break;
+    }
+  }
+  __syncthreads();
+  // eigenvalues, descending stable order, rank (truncation.cpp:29-45)
+  __shared__ double top_s;
+  double* vals = p.val_out + (size_t)b * n;
+  if (tid == 0) {
+    double top = 0.0;
+    for (int i = 0; i < n; ++i) top = fmax(top, fmax(A[(i * ld + i) * W], 0.0));
+    top_s = top;
+  }
+  __syncthreads();
+  const double top = top_s;
+  const bool unit = !nonzero || !(top > 0.0);
+  double* vo = p.vec_out + (size_t)b * n * n * W;
+  __shared__ int rank_s;
+  if (tid == 0) rank_s = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) {
+    const double li = fmax(A[(i * ld + i) * W], 0.0);
+    int pos = 0;
+    for (int j = 0; j < n; ++j) {
+      const double lj = fmax(A[(j * ld + j) * W], 0.0);
+      pos += (lj > li) || (lj == li && j < i);
+    }
+    vals[pos] = li;
+    if (li > p.eps * top) atomicAdd(&rank_s, 1);
+    for (int r = 0; r < n; ++r) {
+      vo[(r + (size_t)pos * n) * W] = unit ? (r == 0 && pos == 0 ? 1.0 : 0.0) : V[(r * ld + i) * W];
+      if (CPLX) vo[(r + (size_t)pos * n) * W + 1] = unit ? 0.0 : V[(r * ld + i) * W + 1];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // the count of eigenvalues above the threshold equals the leading run in
+    // descending order, as in the reference's early-exit loop
+    p.rank_out[b] = unit ? 1 : (rank_s < 1 ? 1 : rank_s);
+    p.degen_io[b] = (unit ? 1 : 0) | p.degen_io[b];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pack sorted eigenvectors (n x n) into a padded basis (rows x KC), zeroing
+// columns at and beyond the rank
+__global__ void pack_basis_kernel(const double* vec, int n, double* out, int rows, int kc,
+                                  const int* rank, int W) {
+  const int b = blockIdx.x;
+  const int r = rank[b];
+  const double* src = vec + (size_t)b * n * n * W;
+  double* dst = out + (size_t)b * rows * kc * W;
+  for (int x = threadIdx.x; x < rows * kc * W; x += blockDim.x) {
+    const int e = x / W, w = x % W;
+    const int row = e % rows, col = e / rows;
+    dst[x] = (col < r && row < n) ? src[(row + (size_t)col * n) * W + w] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gather 2x2 quadrants into a dense (2R x 2C) matrix; idx[4*t+q] (q = 2*ri+ci)
+__global__ void gather_quad_kernel(double* out, const double* src, long long Ss, int R, int Cc,
+                                   const int* idx, const int* remap, int W) {
+  const int t = blockIdx.x;
+  const int ld = 2 * R;
+  double* o = out + (size_t)t * 4 * R * Cc * W;
+  for (int x = threadIdx.x; x < 4 * R * Cc * W; x += blockDim.x) {
+    const int e = x / W, w = x % W;
+    const int row = e % ld, col = e / ld;
+    const int q = 2 * (row / R) + (col / Cc);
+    int s = idx[4 * t + q];
+    if (s >= 0 && remap) s = remap[s];
+    o[x] = s < 0 ? 0.0 : src[(Ss * s + (row % R) + (size_t)(col % Cc) * R) * W + w];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// strided matrix copy jobs (input unpack / output pack)
+struct CopyJob {
+  const double* src;
+  double* dst;
+  int rows, cols, sld, dld;
+};
+__global__ void copy_jobs_kernel(const CopyJob* jobs, int W) {
+  const CopyJob j = jobs[blockIdx.x];
+  const long long total = (long long)j.rows * j.cols * W;
+  for (long long x = threadIdx.x; x < total; x += blockDim.x) {
+    const long long e = x / W;
+    const int w = (int)(x % W);
+    const int r = (int)(e % j.rows), c = (int)(e / j.rows);
+    j.dst[(r + (long long)c * j.dld) * W + w] = j.src[(r + (long long)c * j.sld) * W + w];
+  }
+}
+
+// identity matrices (formatted product: P = I, mmp.cpp:280-283)
+__global__ void set_identity_kernel(double* out, int n, int ld, const int* rank, int W) {
+  const int b = blockIdx.x;
+  double* o = out + (size_t)b * n * ld * W;
+  for (int x = threadIdx.x; x < n * ld * W; x += blockDim.x) {
+    const int e = x / W, w = x % W;
+    const int r = e % ld, c = e / ld;
+    o[x] = (w == 0 && r == c && r < rank[b]) ? 1.0 : 0.0;
+  }
+}
+
+}  // namespace h2b
