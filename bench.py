@@ -1,0 +1,314 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 H^2-MMP on the BASELINE.json workload.
+
+A "step" is one accuracy-controlled product C = A*A (h2mmp::mmp,
+mmp.cpp:688-691) of the configs[1] workload: Laplace 1/(4 pi r) on N=65,536
+seeded uniform points (reference RNG, geometry.cpp:39-52, seed 1), leaf size
+64, eta = 1, nested tensor-Chebyshev bases of order 4 (k = 64), eps = 1e-8.
+
+  value : FP64 GFLOP/s = 2 * MmpReport.flops (the reference's MAC counter,
+          mmp.cpp:67-80; identical to the oracle's) / device time per product,
+          operands resident in HBM, CUDA events on the library's stream.
+  e2e   : same metric through the drop-in C-ABI call h2c_mmp with pinned host
+          buffers (H2D of A, D2H of C inside the timed region).
+
+`--impl reference` times the CPU oracle (a C++ restatement of the reference,
+whose Eigen build cannot be compiled here) on a bounded sample of the same
+workload with every host core running an independent product.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (N, leaf, order, eps, description)
+    "cfg1": (4096, 32, 3, 1e-6, "Laplace 1/(4 pi r), N=4096 cloud seed 1, leaf 32, eta 1, Chebyshev order 3 (k=27), eps 1e-6"),
+    "cfg2": (65536, 64, 4, 1e-8, "Laplace 1/(4 pi r), N=65536 cloud seed 1, leaf 64, eta 1, Chebyshev order 4 (k=64), eps 1e-8"),
+}
+# bounded CPU sample of the same construction (oracle single-thread ~10-30 s)
+CPU_SAMPLE = {"cfg1": 4096, "cfg2": 4096}
+
+
+def build_workload(name: str):
+    import paper_1908_05218_b200 as P
+    n, leaf, order, eps, desc = CONFIGS[name]
+    pts = points_for(n)
+    t0 = time.perf_counter()
+    tree = P.build_cluster_tree(pts, leaf)
+    st = P.build_block_tree(tree, tree, 1.0)
+    A = P.build_chebyshev(tree, st, pts, order)
+    return dict(name=name, points=pts, tree=tree, structure=st, A=A, eps=eps, desc=desc,
+                build_seconds=time.perf_counter() - t0, n=n, leaf=leaf, order=order)
+
+
+def points_for(n: int) -> np.ndarray:
+    """make_random_cloud (geometry.cpp:39-52) through the product library."""
+    import paper_1908_05218_b200 as P
+    return P.random_cloud(n, 1)
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._loop, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def fp64_peak_tflops() -> tuple[float, str]:
+    p = os.path.join(ROOT, "profiles", "FP64_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["fp64_dmma_tflops"]), "measured DMMA m8n8k4 (profiles/FP64_PEAKS.json)"
+    except Exception:
+        return 40.0, "fallback: nominal B200 FP64"
+
+
+def cpu_sample(name: str, threads_note: int = 1) -> dict:
+    """Single-thread oracle on the bounded sample; returns GFLOP/s and details."""
+    from oracle import pyoracle as O
+    import paper_1908_05218_b200 as P
+    n_full, leaf, order, eps, _ = CONFIGS[name]
+    n = CPU_SAMPLE[name]
+    pts = P.random_cloud(n, 1)
+    tree = P.build_cluster_tree(pts, leaf)
+    st = P.build_block_tree(tree, tree, 1.0)
+    A = P.build_chebyshev(tree, st, pts, order)
+    t0 = time.perf_counter()
+    r = O.mmp(A, A, eps)
+    dt = time.perf_counter() - t0
+    return {"gflops": 2.0 * r.report.flops / dt / 1e9, "seconds": dt, "flops": r.report.flops, "n": n,
+            "wall_seconds_report": r.report.wall_seconds}
+
+
+def _cpu_worker(name, q):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    q.put(cpu_sample(name))
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    name = args.config
+    ctx = mp.get_context("spawn")
+    times = []
+    total_flops = 0
+    # warmup (untimed) then K steps, each step = `cores` independent single-thread oracle products
+    for step in range(args.warmup + args.steps):
+        q = ctx.Queue()
+        procs = [ctx.Process(target=_cpu_worker, args=(name, q)) for _ in range(cores)]
+        t0 = time.perf_counter()
+        for p in procs:
+            p.start()
+        res = [q.get() for _ in procs]
+        for p in procs:
+            p.join()
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            total_flops = sum(r["flops"] for r in res)
+    mean = sum(times) / len(times)
+    value = 2.0 * total_flops / mean / 1e9
+    sample = (f"{cores} concurrent single-thread oracle products of the {name} construction at "
+              f"N={CPU_SAMPLE[name]} (leaf {CONFIGS[name][1]}, order {CONFIGS[name][2]}, eps {CONFIGS[name][3]})")
+    line = {"metric": "H2-MMP FP64 GFLOP/s (2*MmpReport.flops / wall)", "value": value, "unit": "GFLOP/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": {"workload": name, "desc": CONFIGS[name][4]},
+            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_b200(args) -> None:
+    import torch
+    import paper_1908_05218_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", rank=rank, world_size=world)
+    else:
+        torch.cuda.set_device(local)
+
+    W = build_workload(args.config)
+    A, eps = W["A"], W["eps"]
+    ctx = P.Context(local)
+    dA = P.ResidentOperand(A, ctx)
+
+    # one product with report (counters, exec MACs) + warm-up
+    _, rep = P.mmp_resident(dA, dA, eps, want_report=True)
+    for _ in range(max(0, args.warmup - 1)):
+        P.mmp_resident(dA, dA, eps)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            P.mmp_resident(dA, dA, eps)
+            launches += ctx.kernel_launches()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops = 2.0 * rep.flops
+    value = world * flops / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel: one profiled (untimed) product
+    ctx.set_profile(True)
+    P.mmp_resident(dA, dA, eps)
+    prof = ctx.profile()
+    ctx.set_profile(False)
+    peak, peak_src = fp64_peak_tflops()
+    dom = max(prof, key=lambda e: e["ms"]) if prof else None
+    prof_ms = sum(e["ms"] for e in prof) if prof else 0.0
+    roofline = None
+    if dom:
+        ach = 2.0 * dom["macs"] / (dom["ms"] * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "kernel": dom["name"], "launches": dom["launches"],
+                    "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                    "traffic": None, "peak_source": peak_src,
+                    "share_of_step": round(dom["ms"] / prof_ms, 4) if prof_ms else None,
+                    "pipeline_exec_tflops": round(2.0 * rep.flops_exec / (ms * 1e-3) / 1e12, 3),
+                    "pipeline_frac": round(2.0 * rep.flops_exec / (ms * 1e-3) / 1e12 / peak, 4)}
+
+    # end-to-end through the drop-in C-ABI call with pinned host buffers
+    Ap, _pin = P.pin_matrix(A)
+    P.mmp(Ap, Ap, eps, ctx)  # warm (plan cached, pool warm)
+    e2e_times = []
+    h2d = d2h = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = P.mmp(Ap, Ap, eps, ctx)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        h2d, d2h = res.report.h2d_bytes, res.report.d2h_bytes
+        del res
+    e2e_s = sum(e2e_times) / len(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * flops / e2e_s / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        c = cpu_sample(args.config)
+        cpu = {"value": round(c["gflops"], 3), "unit": "GFLOP/s", "cores": 1, "kind": "port",
+               "sample": f"single-thread oracle (C++ restatement + OpenBLAS, 1 thread) on the {args.config} "
+                         f"construction at N={c['n']}: {c['seconds']:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "H2-MMP FP64 GFLOP/s (2*MmpReport.flops / wall)", "value": round(value, 3),
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "desc": W["desc"], "N": W["n"], "eps": eps,
+                       "flops_per_step": int(rep.flops), "flops_exec_per_step": int(rep.flops_exec),
+                       "max_rank": rep.max_rank(), "l2": "inputs (%.1f GB) >> 126 MB L2" % (A.values.nbytes / 1e9),
+                       "parallelism": f"replicas{world}"},
+            "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "seconds": round(e2e_s, 4)},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+        }
+        if args.profile:
+            line["profile"] = sorted(prof, key=lambda e: -e["ms"])[:25]
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

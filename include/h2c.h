@@ -34,6 +34,13 @@ const char* h2c_last_error(const h2c_context* ctx);
 h2c_context* h2c_create(int device);
 void h2c_destroy(h2c_context* ctx);
 int64_t h2c_kernel_launches(const h2c_context* ctx); /* launches of the last call */
+void* h2c_stream(const h2c_context* ctx);            /* the cudaStream_t all work runs on */
+/* per-launch CUDA-event profiling of the following calls (aggregated per
+ * pipeline phase and kernel); entries describe the last call */
+void h2c_set_profile(h2c_context* ctx, int on);
+int h2c_profile_count(const h2c_context* ctx);
+int h2c_profile_get(const h2c_context* ctx, int i, char* name, int cap, int64_t* launches, double* ms,
+                    int64_t* macs);
 
 /* ---- structure (host logic) ------------------------------------------
  * build_cluster_tree (cluster_tree.hpp:43, cluster_tree.cpp:66-93) followed by
@@ -47,7 +54,11 @@ void h2c_structure_free(h2c_structure* s);
  * 0 full_block, 1 admissible, 2 subdivided, 3 inside_admissible, <0 error */
 int h2c_target_status(const h2c_tree* tree, const h2c_blocks* blocks, int t, int s);
 
-/* ---- synthetic inputs (not in the reference: BASELINE.json configs) -----
+/* ---- synthetic inputs (not in the reference: BASELINE.json configs) ----- */
+/* make_random_cloud (geometry.cpp:39-52): n points uniform in [0,1)^3 from
+ * std::mt19937_64(seed), 53-bit mantissas, x,y,z per point. */
+int h2c_random_cloud(int n, uint64_t seed, double* xyz);
+/*
  * Nested tensor-Chebyshev H^2 matrix of order `order` (rank order^3) on the
  * cluster bounding boxes, orthonormalised bottom-up (QR; couplings
  * R_t S R_s^T) and, if eps_recompress > 0, recompressed to that accuracy.

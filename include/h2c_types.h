@@ -107,6 +107,8 @@ typedef struct h2c_report {
   int64_t flops_exec;       /* MACs the GPU schedule actually executed */
   double device_seconds;    /* CUDA-event time of the device pipeline  */
   double plan_seconds;      /* host time spent building the structure plan (0 if cached) */
+  int64_t h2d_bytes;        /* host->device bytes moved by the call */
+  int64_t d2h_bytes;        /* device->host bytes moved by the call */
 } h2c_report;
 
 #ifdef __cplusplus

@@ -39,6 +39,24 @@ class Context:
     def kernel_launches(self) -> int:
         return int(h2c.lib().h2c_kernel_launches(self._h))
 
+    def stream_ptr(self) -> int:
+        """cudaStream_t of the library (for torch.cuda.ExternalStream events)."""
+        return int(h2c.lib().h2c_stream(self._h) or 0)
+
+    def set_profile(self, on: bool) -> None:
+        h2c.lib().h2c_set_profile(self._h, int(on))
+
+    def profile(self) -> list[dict]:
+        """Per (phase/kernel) CUDA-event totals of the last call."""
+        L = h2c.lib()
+        out = []
+        for i in range(L.h2c_profile_count(self._h)):
+            name = C.create_string_buffer(128)
+            n, ms, macs = C.c_int64(), C.c_double(), C.c_int64()
+            L.h2c_profile_get(self._h, i, name, 128, C.byref(n), C.byref(ms), C.byref(macs))
+            out.append({"name": name.value.decode(), "launches": n.value, "ms": ms.value, "macs": macs.value})
+        return out
+
     def close(self):
         if self._h:
             h2c.lib().h2c_destroy(self._h)
@@ -118,6 +136,13 @@ def _take_h2(handle, tree: ClusterTree, structure: BlockTree) -> H2Matrix:
         return H2Matrix.from_desc(tree, structure, d)
     finally:
         L.h2c_h2_free(handle)
+
+
+def random_cloud(n: int, seed: int) -> np.ndarray:
+    """make_random_cloud (geometry.cpp:39-52): [n, 3] points uniform in the unit cube."""
+    out = np.zeros((int(n), 3))
+    raise_for(h2c.lib().h2c_random_cloud(int(n), int(seed), out.ctypes.data_as(h2c.P_f64)), h2c.last_error())
+    return out
 
 
 def build_chebyshev(tree: ClusterTree, structure: BlockTree, points: np.ndarray, order: int, kernel: str = "laplace",

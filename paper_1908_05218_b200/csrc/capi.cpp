@@ -7,6 +7,7 @@
 
 #include <cstring>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
 
@@ -81,6 +82,24 @@ h2c_context* h2c_create(int device) {
 void h2c_destroy(h2c_context* ctx) { delete ctx; }
 
 int64_t h2c_kernel_launches(const h2c_context* ctx) { return ctx ? ctx->ctx->last_kernel_launches() : 0; }
+void* h2c_stream(const h2c_context* ctx) { return ctx ? ctx->ctx->stream() : nullptr; }
+void h2c_set_profile(h2c_context* ctx, int on) {
+  if (ctx) ctx->ctx->profile = on != 0;
+}
+int h2c_profile_count(const h2c_context* ctx) { return ctx ? static_cast<int>(ctx->ctx->last_profile.size()) : 0; }
+int h2c_profile_get(const h2c_context* ctx, int i, char* name, int cap, int64_t* launches, double* ms,
+                    int64_t* macs) {
+  if (!ctx || i < 0 || i >= static_cast<int>(ctx->ctx->last_profile.size())) return H2C_ERR_CONFIG;
+  const ProfileEntry& e = ctx->ctx->last_profile[i];
+  if (name && cap > 0) {
+    std::strncpy(name, e.name.c_str(), cap - 1);
+    name[cap - 1] = 0;
+  }
+  if (launches) *launches = e.launches;
+  if (ms) *ms = e.ms;
+  if (macs) *macs = e.macs;
+  return H2C_OK;
+}
 
 h2c_structure* h2c_build_structure(const double* xyz, int n, int leafsize, double eta) {
   try {
@@ -103,6 +122,16 @@ int h2c_target_status(const h2c_tree* tree, const h2c_blocks* blocks, int t, int
     g_err = e.what();
     return -1;
   }
+}
+
+int h2c_random_cloud(int n, uint64_t seed, double* xyz) {
+  if (n < 1) {
+    g_err = "random_cloud: n must be positive";
+    return H2C_ERR_CONFIG;
+  }
+  std::mt19937_64 eng(seed);
+  for (int64_t i = 0; i < 3 * int64_t(n); ++i) xyz[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+  return H2C_OK;
 }
 
 h2c_h2* h2c_build_chebyshev(const h2c_tree* tree, const h2c_blocks* blocks, const double* xyz, int kernel,
@@ -190,6 +219,8 @@ void h2c_result_report(const h2c_result* r, h2c_report* d) {
   d->flops_exec = h.flops_exec;
   d->device_seconds = h.device_seconds;
   d->plan_seconds = h.plan_seconds;
+  d->h2d_bytes = h.h2d_bytes;
+  d->d2h_bytes = h.d2h_bytes;
 }
 
 void h2c_result_free(h2c_result* r) { delete r; }

@@ -429,6 +429,28 @@ struct EngineRun {
   int D, NL;
   int64_t exec_macs = 0;
   int64_t launches = 0;
+  // optional per-launch profiling (CUDA events on the engine stream)
+  struct ProfRec {
+    std::string phase;
+    const char* kernel;
+    int64_t macs;
+    cudaEvent_t a, b;
+  };
+  bool profiling = false;
+  std::string phase = "setup";
+  std::vector<ProfRec> prof;
+  void pre(const char* kernel, int64_t macs) {
+    if (!profiling) return;
+    ProfRec r{phase, kernel, macs, nullptr, nullptr};
+    CK(cudaEventCreate(&r.a));
+    CK(cudaEventCreate(&r.b));
+    CK(cudaEventRecord(r.a, s));
+    prof.push_back(r);
+  }
+  void post() {
+    if (!profiling) return;
+    CK(cudaEventRecord(prof.back().b, s));
+  }
 
   // C
   std::vector<int> KCr, KCc;
@@ -520,6 +542,9 @@ struct EngineRun {
     }
     sp.ngroups = ng;
     if (ng == 0 && acc) return;
+    int64_t macs = 0;
+    for (const Grp& g : gs) macs += (g.csr ? g.csr->entries : n_out) * int64_t(M) * N * g.K;
+    pre("seg_gemm", macs);
     const int TM = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
     const int TN = N <= 16 ? 16 : (N <= 32 ? 32 : 64);
     const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
@@ -532,6 +557,7 @@ struct EngineRun {
     else if (TM == 64 && TN == 16) launch_seg<64, 16>(sp, tiles);
     else if (TM == 64 && TN == 32) launch_seg<64, 32>(sp, tiles);
     else launch_seg<64, 64>(sp, tiles);
+    post();
   }
   // convenience: densely stored output [n_out][M x N]
   void segd(double* out, int M, int N, int n_out, std::initializer_list<Grp> gs) {
@@ -545,9 +571,11 @@ struct EngineRun {
   void seg_add(double* out, long long Os, const double* in, long long Is, const DevCsr& c, long long elems) {
     if (c.n_out <= 0) return;
     const int chunks = static_cast<int>(std::min<long long>(8, (elems / 2 + 255) / 256));
+    pre("seg_add", 0);
     seg_add_kernel<<<dim3(c.n_out, std::max(1, chunks)), 256, 0, s>>>(out, Os * W, in, Is * W, c.ptr, c.li,
                                                                       elems * W, 0);
     CK(cudaGetLastError());
+    post();
     launches++;
   }
 
@@ -562,11 +590,13 @@ struct EngineRun {
     Trunc t;
     DBuf G(sz(count, n, n), s);
     t.degen.alloc(count, s);
+    pre("gram_combine", 0);
     if (cplx)
       gram_combine_kernel<true><<<count, 256, 0, s>>>(g1, g2, g3, G, (long long)n * n, n * n, opdeg.p, nullptr, t.degen.p);
     else
       gram_combine_kernel<false><<<count, 256, 0, s>>>(g1, g2, g3, G, (long long)n * n, n * n, opdeg.p, nullptr, t.degen.p);
     CK(cudaGetLastError());
+    post();
     launches++;
     g1.release();
     g2.release();
@@ -585,6 +615,7 @@ struct EngineRun {
     jp.max_sweeps = 40;
     const size_t smem = size_t(2) * n * (n + 1) * W * sizeof(double);
     DBuf scratch;
+    pre("jacobi_eig", 0);
     if (smem <= 200 * 1024) {
       if (cplx) {
         CK(cudaFuncSetAttribute(jacobi_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -600,6 +631,7 @@ struct EngineRun {
       else jacobi_kernel<false, false><<<count, 256, 0, s>>>(jp);
     }
     CK(cudaGetLastError());
+    post();
     launches++;
     return t;
   }
@@ -617,8 +649,10 @@ struct EngineRun {
 
   void pack(const Trunc& t, int count, int n, DBuf& out, int rows, int kc) {
     out.alloc(sz(count, rows, kc), s);
+    pre("pack_basis", 0);
     pack_basis_kernel<<<count, 256, 0, s>>>(t.vec, n, out, rows, kc, t.rank.p, W);
     CK(cudaGetLastError());
+    post();
     launches++;
   }
 
@@ -632,8 +666,10 @@ struct EngineRun {
   void gather(DBuf& out, int count, const double* src, long long Ss, int R, int Cc, const int* idx) {
     out.alloc(sz(count, 2 * R, 2 * Cc), s);
     if (count <= 0) return;
+    pre("gather_quad", 0);
     gather_quad_kernel<<<count, 256, 0, s>>>(out, src, Ss, R, Cc, idx, nullptr, W);
     CK(cudaGetLastError());
+    post();
     launches++;
   }
 
@@ -644,6 +680,7 @@ struct EngineRun {
 
   // ---- basis products B_j = (V^A_col,j)^T V^B_row,j (mmp.cpp:106-124) --------
   void basis_products() {
+    phase = "basis_products";
     const LevelPlan& LL = P.lv[D];
     Bp[D].alloc(sz(LL.n, A.Kc[D], B.Kr[D]), s);
     segd(Bp[D], A.Kc[D], B.Kr[D], LL.n,
@@ -707,6 +744,7 @@ struct EngineRun {
     segd(VF, KAc, NL, nn, {Grp{ref(A.Vc, (long long)NL * KAc, NL, OP_T), BF, NL, nullptr, Q.near_row, nullptr}});
 
     if (adaptive) {
+      phase = "leaf.row_gram";
       // row Grams (mmp.cpp:164-200)
       DBuf g1(sz(n, NL, NL), s), g2(sz(n, NL, NL), s), g3(sz(n, NL, NL), s);
       {
@@ -726,6 +764,7 @@ struct EngineRun {
            {Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(A.Vr, (long long)NL * KAr, NL, OP_H), KAr, nullptr,
                 nullptr, nullptr}});
       Trunc tr = truncate(g1, g2, g3, n, NL, A.dgr_d[l]);
+      phase = "leaf.col_gram";
       // column Grams (mmp.cpp:202-238)
       DBuf c1(sz(n, NL, NL), s), c2(sz(n, NL, NL), s), c3(sz(n, NL, NL), s);
       {
@@ -745,6 +784,7 @@ struct EngineRun {
            {Grp{ref(B.Vc, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_H), KBc, nullptr,
                 nullptr, nullptr}});
       Trunc tc = truncate(c1, c2, c3, n, NL, B.dgc_d[l]);
+      phase = "leaf.bases";
       KCr[l] = fetch_ranks(tr.rank, n, rcr[l]);
       KCc[l] = fetch_ranks(tc.rank, n, rcc[l]);
       pack(tr, n, NL, Vr, NL, KCr[l]);
@@ -770,6 +810,7 @@ struct EngineRun {
     }
     const int Kr = KCr[l], Kc = KCc[l];
 
+    phase = "leaf.collect";
     // collected full blocks (mmp.cpp:287-298) and W factors of the F x F case
     LA[l].alloc(sz(nb, Kr, KBr), s);
     RB[l].alloc(sz(nb, KAc, Kc), s);
@@ -785,6 +826,7 @@ struct EngineRun {
     DBuf XA, YB;
     adm_factors(l, XA, YB);
 
+    phase = "leaf.coupling_targets";
     // coupling targets: admissible C blocks + pending pairs (mmp.cpp:319-334)
     const int nt = L.n_targets();
     Tg[l].alloc(sz(nt, Kr, Kc), s);
@@ -800,6 +842,7 @@ struct EngineRun {
     XA.release();
     YB.release();
 
+    phase = "leaf.full_targets";
     // full targets (mmp.cpp:310-317): C.full = FF + (sum FV S^B) V^B^T + V^A (sum S^A VF + (sum S^A B S^B) V^B^T)
     {
       DBuf SB(sz(na, KAr, KBr), s);
@@ -846,6 +889,7 @@ struct EngineRun {
     const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l];
     const long long MM = 4LL * Kn * Kq;
 
+    phase = "L" + std::to_string(l) + ".assemble";
     // merged children couplings and assembled collected blocks (mmp.cpp:344-404)
     DBuf Mg, Aa, Ab;
     gather(Mg, nm, Tg[l + 1].p + size_t(Lc.adm.size()) * Kn * Kq * W, (long long)Kn * Kq, Kn, Kq, Q.merged_quad);
@@ -866,6 +910,7 @@ struct EngineRun {
     Ab.release();
 
     if (adaptive) {
+      phase = "L" + std::to_string(l) + ".grams";
       // X3 = blkdiag(P^A_children) T^A_row ; X3c = blkdiag(P^B)^T conj(T^B_col) ; Y3 = blkdiag(P^B)^T T^B_col
       DBuf X3(sz(n, 2 * Kn, KAr), s), X3c(sz(n, 2 * Kq, KBc), s), Y3;
       for (int c = 0; c < 2; ++c) {
@@ -936,6 +981,7 @@ struct EngineRun {
     Bp[l + 1].release();
     const int Kr = KCr[l], Kc = KCc[l];
 
+    phase = "L" + std::to_string(l) + ".collect";
     // collects of subdivided blocks (mmp.cpp:544-552)
     LA[l].alloc(sz(nb, Kr, KBr), s);
     RB[l].alloc(sz(nb, KAc, Kc), s);
@@ -950,6 +996,7 @@ struct EngineRun {
     DBuf XA, YB;
     adm_factors(l, XA, YB);
 
+    phase = "L" + std::to_string(l) + ".targets";
     // targets: case 1 over merged (T^C^H M conj(T^C)), cases 2-4 (mmp.cpp:573-612)
     DBuf Z(sz(nm, Kr, 2 * Kq), s);
     segd(Z, Kr, 2 * Kq, nm,
@@ -969,6 +1016,7 @@ struct EngineRun {
 
   // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------
   void split() {
+    phase = "split";
     for (int l = 1; l < D; ++l) {
       const LevelPlan& L = P.lv[l];
       const LevelPlan& Lc = P.lv[l + 1];
@@ -1009,6 +1057,32 @@ struct EngineRun {
     leaf_phase();
     for (int l = D - 1; l >= 1; --l) upper_level(l);
     split();
+  }
+
+  // per (phase, kernel) totals of the profiled launches
+  void collect_profile(std::vector<ProfileEntry>& out) {
+    out.clear();
+    if (!profiling) return;
+    CK(cudaStreamSynchronize(s));
+    std::map<std::string, size_t> at;
+    for (ProfRec& r : prof) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      const std::string key = r.phase + "/" + r.kernel;
+      auto it = at.find(key);
+      if (it == at.end()) {
+        at[key] = out.size();
+        out.push_back({key, 0, 0.0, 0});
+        it = at.find(key);
+      }
+      ProfileEntry& e = out[it->second];
+      e.launches++;
+      e.ms += ms;
+      e.macs += r.macs;
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    prof.clear();
   }
 
   // ---- output in the flat layout (row bases, col bases by id, then blocks) ----
@@ -1219,6 +1293,7 @@ double Context::run_resident(const std::shared_ptr<DevOperand>& a, const std::sh
   const auto t0 = std::chrono::steady_clock::now();
   CK(cudaEventRecord(e0, s));
   EngineRun R(*this, *plan_, *dplan_, *a, *b, eps, adaptive != 0, s);
+  R.profiling = profile;
   R.run();
   CK(cudaEventRecord(e1, s));
   CK(cudaEventSynchronize(e1));
@@ -1227,6 +1302,7 @@ double Context::run_resident(const std::shared_ptr<DevOperand>& a, const std::sh
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   launches_ = R.launches;
+  R.collect_profile(last_profile);
   if (out) {
     h2c_blocks dummy{};
     (void)dummy;
@@ -1255,6 +1331,7 @@ void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adap
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, s));
   EngineRun R(*this, P, *dplan_, *A, *B, eps, adaptive != 0, s);
+  R.profiling = profile;
   R.run();
   CK(cudaEventRecord(e1, s));
   std::vector<double*> pool;
@@ -1264,6 +1341,9 @@ void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adap
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   launches_ = R.launches + up_launches;
+  R.collect_profile(last_profile);
+  out.h2d_bytes = int64_t(a.n_values) * R.W * 8 + (B.get() == A.get() ? 0 : int64_t(b.n_values) * R.W * 8);
+  out.d2h_bytes = out.n_values * R.W * 8;
   fill_report(P, *A, *B, R, adaptive != 0, eps, out);
   out.device_seconds = ms * 1e-3;
   out.plan_seconds = plan_s;

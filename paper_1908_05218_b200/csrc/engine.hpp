@@ -12,6 +12,13 @@ namespace h2b {
 
 struct DevPlan;  // device copies of the plan's index lists
 
+struct ProfileEntry {
+  std::string name;  // phase/kernel
+  int64_t launches = 0;
+  double ms = 0;
+  int64_t macs = 0;
+};
+
 // Host-side result of one product (flat layout of include/h2c_types.h).
 struct HostResult {
   int32_t scalar = 0;
@@ -26,6 +33,7 @@ struct HostResult {
   int64_t flops = 0, flops_exec = 0;
   std::array<int64_t, 4> case_flops{0, 0, 0, 0};
   double wall_seconds = 0, device_seconds = 0, plan_seconds = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
   std::vector<int64_t> max_row, max_col, case_products;
   std::vector<int32_t> t1, t2, t3;
   ~HostResult();
@@ -55,8 +63,8 @@ class Context {
                       double eps, int adaptive, HostResult* download_to);
   void* stream() const { return stream_; }
   int64_t last_kernel_launches() const { return launches_; }
-  // per-kernel-family timings of the last run (name, ms), filled when profiling is on
-  std::vector<std::pair<std::string, double>> last_timings;
+  // per (phase, kernel) timings of the last run, filled when profiling is on
+  std::vector<ProfileEntry> last_profile;
   bool profile = false;
 
  private:

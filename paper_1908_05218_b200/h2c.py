@@ -79,7 +79,7 @@ class h2c_report(C.Structure):
                 ("pending_after_split", C.c_int32), ("max_row_rank", P_i64), ("max_col_rank", P_i64),
                 ("case_products", P_i64), ("max_case1_terms", P_i32), ("max_case2_terms", P_i32),
                 ("max_case3_terms", P_i32), ("flops_exec", C.c_int64), ("device_seconds", C.c_double),
-                ("plan_seconds", C.c_double)]
+                ("plan_seconds", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 def _ptr(a: np.ndarray, t):
@@ -328,6 +328,8 @@ class MmpReport:
     flops_exec: int = 0
     device_seconds: float = 0.0
     plan_seconds: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
     def max_rank(self) -> int:
         return max([0] + [max(s.max_row_rank, s.max_col_rank) for s in self.levels])
@@ -341,7 +343,8 @@ class MmpReport:
                                  [int(r.case_products[4 * l + c]) for c in range(4)], int(r.max_case1_terms[l]),
                                  int(r.max_case2_terms[l]), int(r.max_case3_terms[l])))
         return MmpReport(r.eps_trunc, bool(r.adaptive), lv, int(r.flops), [int(x) for x in r.case_flops],
-                         r.wall_seconds, r.pending_after_split, int(r.flops_exec), r.device_seconds, r.plan_seconds)
+                         r.wall_seconds, r.pending_after_split, int(r.flops_exec), r.device_seconds, r.plan_seconds,
+                         int(r.h2d_bytes), int(r.d2h_bytes))
 
 
 @dataclass
@@ -370,6 +373,13 @@ def lib() -> C.CDLL:
         L.h2c_destroy.argtypes = [C.c_void_p]
         L.h2c_kernel_launches.restype = C.c_int64
         L.h2c_kernel_launches.argtypes = [C.c_void_p]
+        L.h2c_stream.restype = C.c_void_p
+        L.h2c_stream.argtypes = [C.c_void_p]
+        L.h2c_set_profile.argtypes = [C.c_void_p, C.c_int]
+        L.h2c_profile_count.restype = C.c_int
+        L.h2c_profile_count.argtypes = [C.c_void_p]
+        L.h2c_profile_get.restype = C.c_int
+        L.h2c_profile_get.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int, P_i64, C.POINTER(C.c_double), P_i64]
         L.h2c_build_structure.restype = C.c_void_p
         L.h2c_build_structure.argtypes = [P_f64, C.c_int, C.c_int, C.c_double]
         L.h2c_structure_tree.argtypes = [C.c_void_p, C.POINTER(h2c_tree)]
@@ -377,6 +387,8 @@ def lib() -> C.CDLL:
         L.h2c_structure_free.argtypes = [C.c_void_p]
         L.h2c_target_status.restype = C.c_int
         L.h2c_target_status.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), C.c_int, C.c_int]
+        L.h2c_random_cloud.restype = C.c_int
+        L.h2c_random_cloud.argtypes = [C.c_int, C.c_uint64, P_f64]
         L.h2c_build_chebyshev.restype = C.c_void_p
         L.h2c_build_chebyshev.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_int, C.c_double,
                                           C.c_double, C.c_int, C.c_double, C.c_int]
