@@ -1,0 +1,154 @@
+"""CPU-side tests of the B200 library: the C-ABI loads and exports what
+include/h2c.h declares, and the host logic (cluster/block trees, the
+structure plan, the reference's report counters, the input constructors)
+agrees with the oracle bit for bit.  No kernel is launched here."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_1908_05218_b200 as P
+from paper_1908_05218_b200 import h2c
+from oracle import pyoracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(h2c.LIBPATH))
+    declared = h2c.declared_symbols()
+    assert len(declared) >= 25
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_no_cpu_fallback_without_device():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    pts = P.random_cloud(64, 1)
+    t = P.build_cluster_tree(pts, 8)
+    s = P.build_block_tree(t, t, 1.0)
+    A = P.build_chebyshev(t, s, pts, 2)
+    with pytest.raises(P.DeviceError):
+        P.mmp(A, A, 1e-4, ctx=P.Context(0))
+
+
+GEOMS = [
+    dict(family="random_cloud", seed=1, n=1000),
+    dict(family="random_cloud", seed=7, n=777),
+    dict(family="bus", bus_count=4, samples_per_meter=2),
+    dict(family="slab", slab_width=20, slab_thickness=3),
+    dict(family="cube_array", array_edge=3, cube_points=3),
+]
+
+
+@pytest.mark.parametrize("g", GEOMS)
+@pytest.mark.parametrize("leaf,eta", [(16, 1.0), (30, 1.5), (8, 0.7)])
+def test_structure_matches_oracle(g, leaf, eta):
+    pts = O.geometry(**g)
+    to = O.build_cluster_tree(pts, leaf)
+    so = O.build_block_tree(to, eta)
+    tp = P.build_cluster_tree(pts, leaf)
+    sp = P.build_block_tree(tp, tp, eta)
+    assert tp.same_as(to)
+    assert sp.c_sp == so.c_sp
+    for f in ("level_ptr", "row", "col", "kind"):
+        assert np.array_equal(getattr(sp, f), getattr(so, f)), f
+
+
+def test_random_cloud_matches_reference_stream():
+    for seed in (0, 1, 23):
+        assert np.array_equal(P.random_cloud(513, seed), O.geometry("random_cloud", seed=seed, n=513))
+
+
+def test_target_status_matches_oracle():
+    pts = O.geometry("random_cloud", seed=5, n=600)
+    t = P.build_cluster_tree(pts, 12)
+    s = P.build_block_tree(t, t, 1.0)
+    rng = np.random.default_rng(0)
+    for l in range(1, t.depth + 1):
+        ids = t.levels[l]
+        for _ in range(20):
+            a, b = rng.choice(ids, 2)
+            assert P.target_status(s, int(a), int(b)) == O.target_status(s, int(a), int(b))
+
+
+def _cmp_reports(a, b):
+    assert a.flops == b.flops
+    assert a.case_flops == b.case_flops
+    assert len(a.levels) == len(b.levels)
+    for x, y in zip(a.levels, b.levels):
+        assert (x.max_row_rank, x.max_col_rank, x.case_products, x.max_case1_terms, x.max_case2_terms,
+                x.max_case3_terms) == (y.max_row_rank, y.max_col_rank, y.case_products, y.max_case1_terms,
+                                       y.max_case2_terms, y.max_case3_terms)
+
+
+@pytest.mark.parametrize("n,seed,leaf,eta,eps", [(256, 23, 25, 1.0, 1e-6), (256, 1, 8, 1.5, 1e-12),
+                                                  (512, 31, 30, 1.0, 1e-4), (400, 41, 20, 1.0, 1e-4),
+                                                  (600, 9, 10, 1.2, 1e-6)])
+def test_plan_and_counters_match_oracle_report(n, seed, leaf, eta, eps):
+    """The structure plan + counters reproduce the reference's MmpReport exactly."""
+    pts = O.geometry("random_cloud", seed=seed, n=n)
+    t = O.build_cluster_tree(pts, leaf)
+    s = O.build_block_tree(t, eta)
+    A = O.build_h2(O.assemble_dense(pts), s, 1e-6)
+    for adaptive in (True, False):
+        r = O.mmp(A, A, eps, adaptive=adaptive)
+        _cmp_reports(P.count_report(A, A, r.product, adaptive, eps), r.report)
+
+
+def test_counters_complex_asymmetric():
+    cp = O.geometry("cube_array", array_edge=2, cube_points=3)
+    t = O.build_cluster_tree(cp, 10)
+    s = O.build_block_tree(t, 1.5)
+    A = O.build_h2(O.assemble_dense(cp, "helmholtz", 6.283185307179586), s, 1e-6)
+    B = O.build_h2(O.assemble_dense(cp, "helmholtz", 2.5, diagonal=3.0), s, 1e-6)
+    r = O.mmp(A, B, 1e-8)
+    _cmp_reports(P.count_report(A, B, r.product, True, 1e-8), r.report)
+
+
+def test_chebyshev_operand_is_orthonormal_nested_and_accurate():
+    pts = P.random_cloud(2048, 1)
+    t = P.build_cluster_tree(pts, 32)
+    s = P.build_block_tree(t, t, 1.0)
+    A = P.build_chebyshev(t, s, pts, 3)
+    assert set(A.row_rank[t.parent >= 0].tolist()) == {27}
+    for c in range(t.n_clusters):
+        if t.parent[c] < 0:
+            continue
+        v = A.row_basis(c)
+        assert np.abs(v.T @ v - np.eye(v.shape[1])).max() < 1e-13
+    d = O.assemble_dense(pts) / (4 * np.pi)
+    np.fill_diagonal(d, 0.0)
+    assert np.linalg.norm(O.h2_to_dense(A) - d) / np.linalg.norm(d) < 2e-3
+
+
+def test_fd_laplacian_operand_is_the_stencil():
+    m = 8
+    h = 1.0 / (m + 1)
+    g = np.stack(np.meshgrid(*[np.arange(1, m + 1) * h] * 3, indexing="ij"), -1).reshape(-1, 3)
+    t = P.build_cluster_tree(g, 16)
+    s = P.build_block_tree(t, t, 1.0)
+    A = P.build_fd_laplacian(t, s, g, h)
+    dense = O.h2_to_dense(A)
+    ref = 6 * np.eye(m ** 3)
+    for i in range(m ** 3):
+        for j in range(m ** 3):
+            if abs(np.linalg.norm(g[i] - g[j]) - h) < 1e-9 * h:
+                ref[i, j] = -1
+    assert np.array_equal(dense, ref)
+    assert np.all(A.row_rank[t.parent >= 0] == 1) and np.all(A.row_degenerate[t.parent >= 0] == 1)
+
+
+def test_config_errors():
+    pts = P.random_cloud(32, 1)
+    with pytest.raises(P.ConfigError):
+        P.build_cluster_tree(pts, 0)
+    t = P.build_cluster_tree(pts, 8)
+    with pytest.raises(P.ConfigError):
+        P.build_block_tree(t, t, 0.0)
