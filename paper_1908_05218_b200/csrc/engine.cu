@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -448,9 +449,15 @@ struct EngineRun {
     prof.push_back(r);
   }
   void post() {
+    if (debug_sync) {  // H2B_DEBUG_SYNC=1: locate a faulting launch by phase
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess)
+        throw CudaError(std::string("CUDA error in phase ") + phase + ": " + cudaGetErrorString(e));
+    }
     if (!profiling) return;
     CK(cudaEventRecord(prof.back().b, s));
   }
+  const bool debug_sync = std::getenv("H2B_DEBUG_SYNC") != nullptr;
 
   // C
   std::vector<int> KCr, KCc;

@@ -1,0 +1,270 @@
+"""B200 parity: the CUDA product (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): identical block structure, equal per-cluster
+ranks (unless an eigenvalue sits within 1e-10 of the threshold), equal
+MmpReport counters, ||C_gpu - C_ref||_F / ||C_ref||_F <= 10 eps, and the dense
+check against D*D at the reference's own bounds (test_mmp.cpp, acceptance.cpp).
+"""
+import numpy as np
+import pytest
+
+import paper_1908_05218_b200 as P
+from paper_1908_05218_b200.h2c import ADMISSIBLE, INADMISSIBLE_LEAF
+from oracle import pyoracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return P.Context(0)
+
+
+def rel(x, ref):
+    return np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-300)
+
+
+def structure_preserved(h):
+    """test_support.hpp:133-159"""
+    s, t = h.structure, h.tree
+    for b in range(s.n_blocks):
+        if s.kind[b] == ADMISSIBLE:
+            if h.block_offset[b] < 0 or h.block(b).shape != (h.row_rank[s.row[b]], h.col_rank[s.col[b]]):
+                return False
+        elif s.kind[b] == INADMISSIBLE_LEAF:
+            if h.block_offset[b] < 0 or h.block(b).shape != (t.size(s.row[b]), t.size(s.col[b])):
+                return False
+        elif h.block_offset[b] >= 0:
+            return False
+    return True
+
+
+def check_against_oracle(A, B, eps, ctx, adaptive=True, tol=None):
+    got = P.mmp(A, B, eps, ctx) if adaptive else P.formatted_mmp(A, B, ctx)
+    ref, margin = O.mmp(A, B, eps, adaptive=adaptive, with_margin=True)
+    C = got.product
+    assert C.tree is A.tree and C.structure is A.structure  # C shares A's tree/structure (mmp.cpp:25-26)
+    assert structure_preserved(C)
+    if margin > 1e-10:
+        assert np.array_equal(C.row_rank, ref.product.row_rank)
+        assert np.array_equal(C.col_rank, ref.product.col_rank)
+        assert got.report.flops == ref.report.flops
+        assert got.report.case_flops == ref.report.case_flops
+        for x, y in zip(got.report.levels, ref.report.levels):
+            assert (x.max_row_rank, x.max_col_rank, x.case_products) == (y.max_row_rank, y.max_col_rank,
+                                                                        y.case_products)
+    assert np.array_equal(C.row_degenerate, ref.product.row_degenerate)
+    assert np.array_equal(C.col_degenerate, ref.product.col_degenerate)
+    cg, co = O.h2_to_dense(C), O.h2_to_dense(ref.product)
+    err = rel(cg, co)
+    assert err <= (tol if tol is not None else 10 * max(eps, 1e-14)), err
+    return got, ref, cg, co
+
+
+def laplace(n, seed, leaf, eta=1.0, eps_h2=1e-6):
+    pts = O.geometry("random_cloud", seed=seed, n=n)
+    t = O.build_cluster_tree(pts, leaf)
+    s = O.build_block_tree(t, eta)
+    return O.build_h2(O.assemble_dense(pts), s, eps_h2)
+
+
+CASES = [(256, 23, 25, 1.0, 1e-6), (256, 1, 8, 1.5, 1e-12), (512, 31, 30, 1.0, 1e-4), (400, 41, 20, 1.0, 1e-4),
+         (128, 43, 16, 1.0, 1e-8), (1024, 5, 16, 1.0, 1e-6), (1024, 9, 12, 1.3, 1e-10)]
+
+
+@pytest.mark.parametrize("n,seed,leaf,eta,eps", CASES)
+@pytest.mark.parametrize("adaptive", [True, False])
+def test_matches_oracle(ctx, n, seed, leaf, eta, eps, adaptive):
+    A = laplace(n, seed, leaf, eta)
+    got, ref, cg, co = check_against_oracle(A, A, eps, ctx, adaptive)
+    da = O.h2_to_dense(A)
+    dense = da @ da
+    assert rel(cg, dense) <= 1.1 * rel(co, dense) + 1e-13
+
+
+def test_dense_oracle_bound(ctx):
+    # test_mmp.cpp:50-59 / acceptance.cpp:50-64 (criterion 1)
+    for n in (256, 512, 1024):
+        A = laplace(n, 23, 25, 1.0, 1e-6)
+        da = O.h2_to_dense(A)
+        C = P.mmp(A, A, 1e-6, ctx).product
+        assert rel(O.h2_to_dense(C), da @ da) <= 1e-4
+
+
+def helmholtz(edge, leaf, eta, k=6.283185307179586, diag=None):
+    cp = O.geometry("cube_array", array_edge=edge, cube_points=3)
+    t = O.build_cluster_tree(cp, leaf)
+    s = O.build_block_tree(t, eta)
+    return cp, s, O.build_h2(O.assemble_dense(cp, "helmholtz", k, diag), s, 1e-6 if eta > 1 else 1e-4)
+
+
+def test_complex_kernel_bounds(ctx):
+    _, s, A = helmholtz(2, 20, 1.0)
+    da = O.h2_to_dense(A)
+    ref = da @ da
+    _, _, c6, _ = check_against_oracle(A, A, 1e-6, ctx)
+    assert rel(c6, ref) <= 2e-3
+    _, _, c8, _ = check_against_oracle(A, A, 1e-8, ctx)
+    assert rel(c8, ref) <= 5e-4
+
+
+def test_nonleaf_paths_exact(ctx):
+    A = laplace(256, 1, 8, 1.5)
+    d = O.h2_to_dense(A)
+    r = P.mmp(A, A, 1e-12, ctx)
+    assert sum(sum(lv.case_products) for lv in r.report.levels if lv.level < A.tree.depth) > 0
+    assert rel(O.h2_to_dense(r.product), d @ d) <= 1e-12
+    cp, s, Ac = helmholtz(2, 10, 1.5)
+    dc = O.h2_to_dense(Ac)
+    assert rel(O.h2_to_dense(P.mmp(Ac, Ac, 1e-12, ctx).product), dc @ dc) <= 1e-12
+
+
+def test_asymmetric_complex(ctx):
+    cp = O.geometry("cube_array", array_edge=2, cube_points=3)
+    t = O.build_cluster_tree(cp, 10)
+    s = O.build_block_tree(t, 1.5)
+    A = O.build_h2(O.assemble_dense(cp, "helmholtz", 6.283185307179586), s, 1e-6)
+    B = O.build_h2(O.assemble_dense(cp, "helmholtz", 2.5, diagonal=3.0), s, 1e-6)
+    got, _, cg, _ = check_against_oracle(A, B, 1e-12, ctx)
+    assert rel(cg, O.h2_to_dense(A) @ O.h2_to_dense(B)) <= 1e-12
+    C = got.product
+    for c in range(t.n_clusters):
+        for m in (C.row_basis(c), C.col_basis(c)):
+            if m.size:
+                assert np.abs(m.conj().T @ m - np.eye(m.shape[1])).max() <= 1e-12
+    ef = O.relative_error(A, B, P.formatted_mmp(A, B, ctx).product, 3)
+    assert O.relative_error(A, B, C, 3) <= ef
+
+
+def _zero(h, kind):
+    v = h.values.copy()
+    for b in range(h.structure.n_blocks):
+        if h.structure.kind[b] == kind:
+            o = h.block_offset[b]
+            r, c = h.block(b).shape
+            v[o:o + r * c] = 0
+    return h.copy_with(v)
+
+
+def test_single_case_isolation(ctx):
+    A = laplace(128, 43, 16, 1.0, 1e-8)
+    f, r = _zero(A, ADMISSIBLE), _zero(A, INADMISSIBLE_LEAF)
+    for a, b in ((f, f), (f, r), (r, f), (r, r)):
+        ref = O.h2_to_dense(a) @ O.h2_to_dense(b)
+        got = O.h2_to_dense(P.mmp(a, b, 1e-12, ctx).product)
+        assert np.linalg.norm(got - ref) <= 1e-10 * max(1.0, np.linalg.norm(ref))
+
+
+def test_zero_and_identity_operands(ctx):
+    pts = O.geometry("random_cloud", seed=3, n=128)
+    t = O.build_cluster_tree(pts, 16)
+    s = O.build_block_tree(t, 1.0)
+    A = O.build_h2(O.assemble_dense(pts), s, 1e-6)
+    Z = O.build_h2(np.zeros((128, 128)), s, 1e-6)
+    r = P.mmp(Z, A, 1e-6, ctx)
+    leaf = t.levels[t.depth][0]
+    assert np.linalg.norm(O.h2_to_dense(r.product)) <= 1e-14 and r.product.row_degenerate[leaf]
+    r2 = P.mmp(A, Z, 1e-6, ctx)
+    assert np.linalg.norm(O.h2_to_dense(r2.product)) <= 1e-14 and r2.product.col_degenerate[leaf]
+    B = laplace(256, 29, 25, 1.0, 1e-6)
+    eye = O.build_h2(np.eye(256), B.structure, 1e-8)
+    db = O.h2_to_dense(B)
+    assert rel(O.h2_to_dense(P.mmp(B, eye, 1e-10, ctx).product), db) <= 1e-7
+    assert rel(O.h2_to_dense(P.mmp(eye, B, 1e-10, ctx).product), db) <= 1e-7
+
+
+def test_formatted_collapse_and_dominance(ctx):
+    A = laplace(192, 47, 16, 1.0, 1e-8)
+    r = _zero(A, INADMISSIBLE_LEAF)
+    ref = O.h2_to_dense(r) @ O.h2_to_dense(r)
+    for res in (P.formatted_mmp(r, r, ctx), P.mmp(r, r, 1e-12, ctx)):
+        assert np.linalg.norm(O.h2_to_dense(res.product) - ref) <= 1e-10 * max(1.0, np.linalg.norm(ref))
+    _, _, H = helmholtz(2, 20, 1.0)
+    assert O.relative_error(H, H, P.formatted_mmp(H, H, ctx).product, 7) >= \
+        O.relative_error(H, H, P.mmp(H, H, 1e-2, ctx).product, 7)
+
+
+def test_config_errors(ctx):
+    pts = O.geometry("random_cloud", seed=71, n=64)
+    t1, t2 = O.build_cluster_tree(pts, 8), O.build_cluster_tree(pts, 8)
+    s1, s2 = O.build_block_tree(t1, 1.0), O.build_block_tree(t2, 1.0)
+    d = O.assemble_dense(pts)
+    A, B = O.build_h2(d, s1, 1e-4), O.build_h2(d, s2, 1e-4)
+    with pytest.raises(P.ConfigError):
+        P.mmp(A, B, 1e-4, ctx)
+    for bad in (0.0, 1.0, -1.0):
+        with pytest.raises(P.ConfigError):
+            P.mmp(A, A, bad, ctx)
+
+
+def test_exact_rows_in_span(ctx):
+    A = laplace(512, 73, 30, 1.0, 1e-6)
+    t, s = A.tree, A.structure
+    da = O.h2_to_dense(A)
+    ref = (da @ da)[np.ix_(t.perm, t.perm)]
+    C = P.mmp(A, A, 1e-12, ctx).product
+    for c in t.levels[t.depth]:
+        far = []
+        a = int(c)
+        while a >= 0:
+            for (i, k), kind in s.level_blocks(int(t.level[a])):
+                if kind == ADMISSIBLE and i == a:
+                    far.append((t.begin[k], t.size(k)))
+            a = int(t.parent[a])
+        if not far:
+            continue
+        rows = np.concatenate([ref[t.begin[c]:t.end[c], b:b + n] for b, n in far], axis=1)
+        v = C.row_basis(int(c))
+        assert np.linalg.norm(rows - v @ (v.conj().T @ rows)) / np.linalg.norm(rows) <= 1e-10
+
+
+def chebyshev(n, leaf, order, seed=1):
+    pts = P.random_cloud(n, seed)
+    t = P.build_cluster_tree(pts, leaf)
+    s = P.build_block_tree(t, t, 1.0)
+    return P.build_chebyshev(t, s, pts, order)
+
+
+def test_cfg1_parity_and_dense_check(ctx):
+    """BASELINE configs[0]: N=4096, leaf 32, Chebyshev order 3 (k=27), eps=1e-6, dense check."""
+    A = chebyshev(4096, 32, 3)
+    got, ref, cg, co = check_against_oracle(A, A, 1e-6, ctx)
+    da = O.h2_to_dense(A)
+    dense = da @ da
+    e_gpu, e_ref = rel(cg, dense), rel(co, dense)
+    assert e_gpu <= 1.1 * e_ref + 1e-14 and e_gpu <= 1e-4, (e_gpu, e_ref)
+
+
+def test_resident_path_matches_dropin(ctx):
+    A = chebyshev(2048, 32, 3)
+    r1 = P.mmp(A, A, 1e-6, ctx)
+    dA = P.ResidentOperand(A, ctx)
+    secs, rep = P.mmp_resident(dA, dA, 1e-6, want_report=True)
+    assert secs > 0 and rep.flops == r1.report.flops and rep.flops_exec == r1.report.flops_exec
+    assert ctx.kernel_launches() > 0
+
+
+def test_cfg2_construction_at_16k_matches_oracle(ctx):
+    """configs[1] construction (leaf 64, order 4 = k 64, eps 1e-8) at N=16384: full oracle parity."""
+    A = chebyshev(16384, 64, 4)
+    got, ref, cg, co = check_against_oracle(A, A, 1e-8, ctx)
+    assert got.report.max_rank() == ref.report.max_rank()
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_properties(ctx):
+    """configs[1] at N=65536: size-independent properties (MVP probe, orthonormality, counters)."""
+    A = chebyshev(65536, 64, 4)
+    r = P.mmp(A, A, 1e-8, ctx)
+    C = r.product
+    assert structure_preserved(C)
+    assert r.report.flops == P.count_report(A, A, C, True, 1e-8).flops
+    rng = np.random.default_rng(0)
+    for c in rng.choice(np.nonzero(A.tree.parent >= 0)[0], 64, replace=False):
+        for m in (C.row_basis(int(c)), C.col_basis(int(c))):
+            assert np.abs(m.T @ m - np.eye(m.shape[1])).max() <= 1e-12
+    X = rng.uniform(-1, 1, (65536, 4))
+    for j in range(X.shape[1]):
+        x = X[:, j]
+        ref = O.mvp(A, O.mvp(A, x))
+        assert np.linalg.norm(O.mvp(C, x) - ref) / np.linalg.norm(ref) <= 1e-6
