@@ -1,0 +1,16 @@
+"""Run one product of a Chebyshev workload with per-phase profiling (debug aid)."""
+import sys, time
+sys.path.insert(0, "/root/repo")
+import paper_1908_05218_b200 as P
+n = int(sys.argv[1]); leaf = int(sys.argv[2]); order = int(sys.argv[3]); eps = float(sys.argv[4])
+pts = P.random_cloud(n, 1)
+t = P.build_cluster_tree(pts, leaf); s = P.build_block_tree(t, t, 1.0)
+A = P.build_chebyshev(t, s, pts, order)
+ctx = P.Context(0)
+ctx.set_profile(True)
+t0 = time.time()
+r = P.mmp(A, A, eps, ctx)
+print("ok", n, time.time() - t0, "flops", r.report.flops, "maxrank", r.report.max_rank(), "dev", r.report.device_seconds,
+      "ranks", [(l.max_row_rank, l.max_col_rank) for l in r.report.levels], flush=True)
+for e in sorted(ctx.profile(), key=lambda e: -e["ms"])[:15]:
+    print(e)
