@@ -18,6 +18,7 @@
 //   sum_j WA_ij * WB_jk  (leaf full x full; WA = V^C^H F, WB = F conj(V^C))
 // and the leaf Gram G1 = sum_{j,k} (F F)(F F)^H as sum_j F_ij (sum_k F_jk F_jk^H) F_ij^H.
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -38,6 +39,8 @@ namespace h2b {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+constexpr int kJacobiMaxN = 64;
+
 struct ConfigErr : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
 };
@@ -621,9 +624,8 @@ struct EngineRun {
     jp.eps = adaptive ? eps : 0.5;
     jp.max_sweeps = 40;
     const size_t smem = size_t(2) * n * (n + 1) * W * sizeof(double);
-    DBuf scratch;
-    pre("jacobi_eig", 0);
-    if (smem <= 200 * 1024) {
+    if (n <= kJacobiMaxN) {
+      pre("jacobi_eig", 0);
       if (cplx) {
         CK(cudaFuncSetAttribute(jacobi_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         jacobi_kernel<true, true><<<count, 256, smem, s>>>(jp);
@@ -631,17 +633,51 @@ struct EngineRun {
         CK(cudaFuncSetAttribute(jacobi_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         jacobi_kernel<false, true><<<count, 256, smem, s>>>(jp);
       }
+      CK(cudaGetLastError());
+      post();
+      launches++;
     } else {
-      scratch.alloc(size_t(count) * 2 * n * (n + 1) * W, s);
-      jp.scratch = scratch;
-      if (cplx) jacobi_kernel<true, false><<<count, 256, 0, s>>>(jp);
-      else jacobi_kernel<false, false><<<count, 256, 0, s>>>(jp);
+      library_eig(G, count, n, t);
     }
+    return t;
+  }
+
+  // Gram dimensions beyond the shared-memory Jacobi (upper levels, where C's
+  // ranks grow): batched Hermitian eigensolver from cuSOLVER, then the same
+  // truncation rule on the device.
+  void library_eig(const DBuf& G, int count, int n, Trunc& t) {
+    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.solver());
+    DBuf V(sz(count, n, n), s), w(size_t(count) * n, s);
+    CK(cudaMemcpyAsync(V.p, G.p, sz(count, n, n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    const cudaDataType dt = cplx ? CUDA_C_64F : CUDA_R_64F;
+    size_t dev_bytes = 0, host_bytes = 0;
+    pre("syev_batched", 0);
+    auto chk = [](cusolverStatus_t st, const char* what) {
+      if (st != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string("cuSOLVER ") + what + " failed: " + std::to_string(int(st)));
+    };
+    chk(cusolverDnXsyevBatched_bufferSize(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p, n,
+                                          CUDA_R_64F, w.p, dt, &dev_bytes, &host_bytes, count),
+        "syevBatched_bufferSize");
+    DBuf work(dev_bytes / sizeof(double) + 2, s);
+    std::vector<char> hwork(host_bytes + 1);
+    DVec<int> info;
+    info.alloc(count, s);
+    chk(cusolverDnXsyevBatched(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p, n, CUDA_R_64F,
+                               w.p, dt, work.p, dev_bytes, hwork.data(), host_bytes, info.p, count),
+        "syevBatched");
+    post();
+    launches++;
+    pre("eig_finalize", 0);
+    if (cplx)
+      eig_finalize_kernel<true><<<count, 256, 0, s>>>(G, V, w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
+    else
+      eig_finalize_kernel<false><<<count, 256, 0, s>>>(G, V, w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
     CK(cudaGetLastError());
     post();
     launches++;
-    return t;
+    CK(cudaStreamSynchronize(s));  // host workspace lifetime
   }
+  double jp_eps() const { return adaptive ? eps : 0.5; }
 
   // ranks to host, padded width
   int fetch_ranks(const DVec<int32_t>& r, int count, std::vector<int64_t>& out) {
@@ -1219,7 +1255,18 @@ Context::Context(int device) : device_(device) {
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
 }
 
+void* Context::solver() {
+  if (!solver_) {
+    cusolverDnHandle_t h;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
+    cusolverDnSetStream(h, static_cast<cudaStream_t>(stream_));
+    solver_ = h;
+  }
+  return solver_;
+}
+
 Context::~Context() {
+  if (solver_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_));
   dplan_.reset();
   if (stream_) {
     cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));

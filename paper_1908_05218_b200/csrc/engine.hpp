@@ -62,6 +62,7 @@ class Context {
   double run_resident(const std::shared_ptr<DevOperand>& a, const std::shared_ptr<DevOperand>& b,
                       double eps, int adaptive, HostResult* download_to);
   void* stream() const { return stream_; }
+  void* solver();  // cusolverDn handle bound to the stream (lazy)
   int64_t last_kernel_launches() const { return launches_; }
   // per (phase, kernel) timings of the last run, filled when profiling is on
   std::vector<ProfileEntry> last_profile;
@@ -71,6 +72,7 @@ class Context {
   friend struct EngineRun;
   int device_;
   void* stream_ = nullptr;
+  void* solver_ = nullptr;
   std::string err_;
   uint64_t plan_key_ = 0;
   std::unique_ptr<Plan> plan_;

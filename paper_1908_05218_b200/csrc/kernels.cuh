@@ -560,6 +560,44 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Finalize a library eigendecomposition (ascending eigenvalues, eigenvectors
+// in columns) into the truncation output of jacobi_kernel: clamp at 0, sort
+// descending, strict threshold, >= 1 vector, e_1 for exactly-zero Grams
+// (truncation.cpp:23-45).
+template <bool CPLX>
+__global__ void eig_finalize_kernel(const double* G, const double* V, const double* w, int n, double eps,
+                                    double* vec_out, double* val_out, int* rank_out, uint8_t* degen_io) {
+  constexpr int W = CPLX ? 2 : 1;
+  const int b = blockIdx.x;
+  const double* g = G + (size_t)b * n * n * W;
+  const double* v = V + (size_t)b * n * n * W;
+  const double* wb = w + (size_t)b * n;
+  __shared__ int nz;
+  if (threadIdx.x == 0) nz = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int x = threadIdx.x; x < n * n * W; x += blockDim.x) mine |= g[x] != 0.0;
+  if (__syncthreads_or(mine) && threadIdx.x == 0) nz = 1;
+  __syncthreads();
+  const double top = fmax(wb[n - 1], 0.0);
+  const bool unit = !nz || !(top > 0.0);
+  double* vo = vec_out + (size_t)b * n * n * W;
+  // descending order = reversed ascending order (ties keep LAPACK's order reversed, as Eigen's reverse())
+  for (int x = threadIdx.x; x < n * n * W; x += blockDim.x) {
+    const int e = x / W, q = x % W;
+    const int r = e % n, c = e / n;
+    vo[x] = unit ? ((q == 0 && r == 0 && c == 0) ? 1.0 : 0.0) : v[(r + (size_t)(n - 1 - c) * n) * W + q];
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) val_out[(size_t)b * n + i] = fmax(wb[n - 1 - i], 0.0);
+  if (threadIdx.x == 0) {
+    int r = 0;
+    while (r < n && fmax(wb[n - 1 - r], 0.0) > eps * top) ++r;
+    rank_out[b] = unit ? 1 : (r < 1 ? 1 : r);
+    degen_io[b] = (unit ? 1 : 0) | degen_io[b];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // pack sorted eigenvectors (n x n) into a padded basis (rows x KC), zeroing
 // columns at and beyond the rank
 __global__ void pack_basis_kernel(const double* vec, int n, double* out, int rows, int kc,
