@@ -12,11 +12,15 @@
 // leak into results; ranks are tracked per cluster on the host.
 //
 // Reassociation (value-neutral up to rounding, counted separately as
-// flops_exec): the four product cases are evaluated as
-//   sum_j LA_ij * YB_jk  (B_jk admissible; LA = coll_a or P^A S^A B_j)
-//   sum_j XA_ij * RB_jk  (A_ij admissible, B_jk near; XA = P^A S^A, RB = coll_b)
-//   sum_j WA_ij * WB_jk  (leaf full x full; WA = V^C^H F, WB = F conj(V^C))
-// and the leaf Gram G1 = sum_{j,k} (F F)(F F)^H as sum_j F_ij (sum_k F_jk F_jk^H) F_ij^H.
+// flops_exec): the projections P^A_i, P^B_k of the four product cases depend
+// only on the target (i,k), so they are applied once per target after the sum
+// over the middle cluster j (see targets()):
+//   T_ik = P^A_i [ sum_RR (S^A B_j) S^B + sum_RF S^A coll_b ] + [ sum_FR coll_a S^B ] P^B_k ... * P^B_k
+// which costs k_A k_B k_B per R x R triple instead of the reference's
+// left-to-right chain (4 k^3, mmp.cpp:329-332) - 16x fewer MACs at the upper
+// levels where C's ranks grow to ~300.  Leaf full x full into couplings stays
+// sum_j (V^C^H F_ij)(F_jk conj(V^C)), and the leaf Gram
+// G1 = sum_{j,k} (F F)(F F)^H is evaluated as sum_j F_ij (sum_k F_jk F_jk^H) F_ij^H.
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
@@ -143,7 +147,8 @@ struct DevCsr {
 };
 
 struct DevLevel {
-  DevCsr ly, xr, ww, ff, fr, rf, rr, mg, hq, hqc, row_near, col_near, row_merged, col_merged;
+  DevCsr lyr, lyn, xr, ww, ff, fr, rf, rr, mg, hq, hqc, row_near, col_near, row_merged, col_merged;
+  const int *target_row = nullptr, *target_col = nullptr;
   const int *near_row = nullptr, *near_col = nullptr, *adm_row = nullptr, *adm_col = nullptr;
   const int *nearb = nullptr, *adm = nullptr, *merged_row = nullptr, *merged_quad = nullptr;
   const int *sub_child = nullptr, *nl_col = nullptr;
@@ -183,7 +188,10 @@ static std::unique_ptr<DevPlan> upload_plan(const Plan& P, cudaStream_t s) {
     const LevelPlan& L = P.lv[l];
     DevLevel& Q = D->lv[l];
     maxn = std::max(maxn, L.n);
-    put_csr(Q.ly, L.ly);
+    put_csr(Q.lyr, L.lyr);
+    put_csr(Q.lyn, L.lyn);
+    put(&Q.target_row, L.target_row);
+    put(&Q.target_col, L.target_col);
     put_csr(Q.xr, L.xr);
     put_csr(Q.ww, L.ww);
     put_csr(Q.ff, L.ff);
@@ -747,26 +755,67 @@ struct EngineRun {
   }
 
   // ---- admissible-block factors shared by leaf and upper levels --------------
-  // XA = P^A S^A, LA = XA B_j ; YB = S^B P^B, RB = B_j YB   (mmp.cpp:325-332,389-390)
-  void adm_factors(int l, DBuf& XA, DBuf& YB) {
+  // SB = S^A B_j, LA = P^A SB ; BS = B_i S^B, RB = BS P^B  (mmp.cpp:325-332,389-390)
+  void adm_factors(int l, DBuf& SB) {
     const LevelPlan& L = P.lv[l];
     const DevLevel& Q = DP.lv[l];
     const int na = static_cast<int>(L.adm.size());
     const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l], Kr = KCr[l], Kc = KCc[l];
-    XA.alloc(sz(na, Kr, KAc), s);
-    segd(XA, Kr, KAc, na,
-         {Grp{ref(PA[l], (long long)Kr * KAr, Kr, OP_N), ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), KAr, nullptr,
-              Q.adm_row, nullptr}});
-    seg(LA[l], (long long)Kr * KBr, 0, Kr, Q.adm, Kr, KBr, na, false,
-        {Grp{ref(XA, (long long)Kr * KAc, Kr, OP_N), ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), KAc, nullptr,
-             nullptr, Q.adm_col}});
-    YB.alloc(sz(na, KBr, Kc), s);
-    segd(YB, KBr, Kc, na,
-         {Grp{ref(B.S[l], (long long)KBr * KBc, KBr, OP_N), ref(PB[l], (long long)KBc * Kc, KBc, OP_N), KBc, nullptr,
+    SB.alloc(sz(na, KAr, KBr), s);
+    segd(SB, KAr, KBr, na,
+         {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), KAc, nullptr,
               nullptr, Q.adm_col}});
-    seg(RB[l], (long long)KAc * Kc, 0, KAc, Q.adm, KAc, Kc, na, false,
-        {Grp{ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), ref(YB, (long long)KBr * Kc, KBr, OP_N), KBr, nullptr,
+    seg(LA[l], (long long)Kr * KBr, 0, Kr, Q.adm, Kr, KBr, na, false,
+        {Grp{ref(PA[l], (long long)Kr * KAr, Kr, OP_N), ref(SB, (long long)KAr * KBr, KAr, OP_N), KAr, nullptr,
              Q.adm_row, nullptr}});
+    DBuf BS(sz(na, KAc, KBc), s);
+    segd(BS, KAc, KBc, na,
+         {Grp{ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), ref(B.S[l], (long long)KBr * KBc, KBr, OP_N), KBr, nullptr,
+              Q.adm_row, nullptr}});
+    seg(RB[l], (long long)KAc * Kc, 0, KAc, Q.adm, KAc, Kc, na, false,
+        {Grp{ref(BS, (long long)KAc * KBc, KAc, OP_N), ref(PB[l], (long long)KBc * Kc, KBc, OP_N), KBc, nullptr,
+             nullptr, Q.adm_col}});
+  }
+
+  // ---- coupling targets (mmp.cpp:319-334, 573-612) ----------------------------
+  // The projections depend only on the target, so they leave the sum over j:
+  //   T_ik = P^A_i (sum_RR S^A B_j S^B + ...) P^B_k
+  //        = P^A_i [V1 P^B_k + U2] + U1 P^B_k (+ merged + leaf F x F)
+  //   V1 = sum_{A,B adm} SB_ij S^B_jk,  U1 = sum_{A near} coll_a_ij S^B_jk,
+  //   U2 = sum_{A adm, B near} S^A_ij coll_b_jk
+  void targets(int l, const DBuf& SB, const DBuf* WA, const DBuf* WB, const DBuf* Z, int Kq) {
+    const LevelPlan& L = P.lv[l];
+    const DevLevel& Q = DP.lv[l];
+    const int nt = L.n_targets();
+    const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l], Kr = KCr[l], Kc = KCc[l];
+    const Ref BS_ = ref(B.S[l], (long long)KBr * KBc, KBr, OP_N);
+    DBuf V1(sz(nt, KAr, KBc), s), U1(sz(nt, Kr, KBc), s), U2(sz(nt, KAr, Kc), s);
+    segd(V1, KAr, KBc, nt, {Grp{ref(SB, (long long)KAr * KBr, KAr, OP_N), BS_, KBr, &Q.lyr, nullptr, nullptr}});
+    segd(U1, Kr, KBc, nt, {Grp{ref(LA[l], (long long)Kr * KBr, Kr, OP_N), BS_, KBr, &Q.lyn, nullptr, nullptr}});
+    segd(U2, KAr, Kc, nt,
+         {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(RB[l], (long long)KAc * Kc, KAc, OP_N), KAc, &Q.xr,
+              nullptr, nullptr}});
+    const Ref PBk = ref(PB[l], (long long)KBc * Kc, KBc, OP_N);
+    seg(U2, (long long)KAr * Kc, 0, KAr, nullptr, KAr, Kc, nt, true,
+        {Grp{ref(V1, (long long)KAr * KBc, KAr, OP_N), PBk, KBc, nullptr, nullptr, Q.target_col}});
+    V1.release();
+    Tg[l].alloc(sz(nt, Kr, Kc), s);
+    const Grp gA{ref(PA[l], (long long)Kr * KAr, Kr, OP_N), ref(U2, (long long)KAr * Kc, KAr, OP_N), KAr, nullptr,
+                 Q.target_row, nullptr};
+    const Grp gB{ref(U1, (long long)Kr * KBc, Kr, OP_N), PBk, KBc, nullptr, nullptr, Q.target_col};
+    if (Z) {
+      segd(Tg[l], Kr, Kc, nt,
+           {gA, gB,
+            Grp{ref(*Z, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, &Q.mg, nullptr,
+                nullptr}});
+    } else if (WA) {
+      segd(Tg[l], Kr, Kc, nt,
+           {gA, gB,
+            Grp{ref(*WA, (long long)Kr * NL, Kr, OP_N), ref(*WB, (long long)NL * Kc, NL, OP_N), NL, &Q.ww, nullptr,
+                nullptr}});
+    } else {
+      segd(Tg[l], Kr, Kc, nt, {gA, gB});
+    }
   }
 
   // ---- leaf level (mmp.cpp:245-340) ------------------------------------------
@@ -866,32 +915,17 @@ struct EngineRun {
     DBuf WA(sz(nn, Kr, NL), s), WB(sz(nn, NL, Kc), s);
     segd(WA, Kr, NL, nn, {Grp{ref(Vr, (long long)NL * Kr, NL, OP_H), AF, NL, nullptr, Q.near_row, nullptr}});
     segd(WB, NL, Kc, nn, {Grp{BF, ref(Vc, (long long)NL * Kc, NL, OP_C), NL, nullptr, nullptr, Q.near_col}});
-    DBuf XA, YB;
-    adm_factors(l, XA, YB);
+    DBuf SB;
+    adm_factors(l, SB);
 
     phase = "leaf.coupling_targets";
-    // coupling targets: admissible C blocks + pending pairs (mmp.cpp:319-334)
-    const int nt = L.n_targets();
-    Tg[l].alloc(sz(nt, Kr, Kc), s);
-    segd(Tg[l], Kr, Kc, nt,
-         {Grp{ref(LA[l], (long long)Kr * KBr, Kr, OP_N), ref(YB, (long long)KBr * Kc, KBr, OP_N), KBr, &Q.ly, nullptr,
-              nullptr},
-          Grp{ref(XA, (long long)Kr * KAc, Kr, OP_N), ref(RB[l], (long long)KAc * Kc, KAc, OP_N), KAc, &Q.xr,
-              nullptr, nullptr},
-          Grp{ref(WA, (long long)Kr * NL, Kr, OP_N), ref(WB, (long long)NL * Kc, NL, OP_N), NL, &Q.ww,
-              nullptr, nullptr}});
+    targets(l, SB, &WA, &WB, nullptr, 0);
     WA.release();
     WB.release();
-    XA.release();
-    YB.release();
 
     phase = "leaf.full_targets";
     // full targets (mmp.cpp:310-317): C.full = FF + (sum FV S^B) V^B^T + V^A (sum S^A VF + (sum S^A B S^B) V^B^T)
     {
-      DBuf SB(sz(na, KAr, KBr), s);
-      segd(SB, KAr, KBr, na,
-           {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), KAc,
-                nullptr, nullptr, Q.adm_col}});
       const Ref BS = ref(B.S[l], (long long)KBr * KBc, KBr, OP_N);
       DBuf T2(sz(nn, NL, KBc), s), T4(sz(nn, KAr, KBc), s), U(sz(nn, KAr, NL), s);
       segd(T2, NL, KBc, nn, {Grp{ref(FV, (long long)NL * KBr, NL, OP_N), BS, KBr, &Q.fr, nullptr, nullptr}});
@@ -1036,25 +1070,17 @@ struct EngineRun {
              nullptr, Q.near_col}});
     X.release();
     Xc.release();
-    DBuf XA, YB;
-    adm_factors(l, XA, YB);
+    DBuf SB;
+    adm_factors(l, SB);
 
     phase = "L" + std::to_string(l) + ".targets";
-    // targets: case 1 over merged (T^C^H M conj(T^C)), cases 2-4 (mmp.cpp:573-612)
+    // case 1 over merged children couplings: Z = T^C_row^H M (mmp.cpp:573-585)
     DBuf Z(sz(nm, Kr, 2 * Kq), s);
     segd(Z, Kr, 2 * Kq, nm,
          {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), ref(Mg, MM, 2 * Kn, OP_N), 2 * Kn, nullptr, Q.merged_row,
               nullptr}});
     Mg.release();
-    const int nt = L.n_targets();
-    Tg[l].alloc(sz(nt, Kr, Kc), s);
-    segd(Tg[l], Kr, Kc, nt,
-         {Grp{ref(Z, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, &Q.mg, nullptr,
-              nullptr},
-          Grp{ref(LA[l], (long long)Kr * KBr, Kr, OP_N), ref(YB, (long long)KBr * Kc, KBr, OP_N), KBr, &Q.ly, nullptr,
-              nullptr},
-          Grp{ref(XA, (long long)Kr * KAc, Kr, OP_N), ref(RB[l], (long long)KAc * Kc, KAc, OP_N), KAc, &Q.xr,
-              nullptr, nullptr}});
+    targets(l, SB, nullptr, nullptr, &Z, Kq);
   }
 
   // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------

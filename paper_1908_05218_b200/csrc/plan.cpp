@@ -326,7 +326,7 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
       if (s == kSubTarget) return na + np + L.nl_of_block[find_block(L, i, k)];
       return -1;
     };
-    Builder ly, xr, ww, ff, fr, rf, rr, hq, hqc;
+    Builder ly, lyr, lyn, xr, ww, ff, fr, rf, rr, hq, hqc;
     const int nnear = static_cast<int>(L.nearb.size());
     std::vector<std::vector<std::pair<int, int>>> hqc_rows;  // per B near: (i, A near)
     if (leaf) hqc_rows.resize(nnear);
@@ -353,7 +353,11 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
           for (size_t e = s0; e < s1; ++e) {
             const Triple& t = tr[e];
             const bool ra = L.bkind[t.a] == kAdm, rb = L.bkind[t.b] == kAdm;
-            if (rb) ly.add(o, t.a, L.kidx[t.b]);
+            if (rb) {
+              ly.add(o, t.a, L.kidx[t.b]);
+              if (ra) lyr.add(o, L.kidx[t.a], L.kidx[t.b]);
+              else lyn.add(o, t.a, L.kidx[t.b]);
+            }
             else if (ra) xr.add(o, L.kidx[t.a], t.b);
             else {  // full x full at the leaf level (NL x NL never reaches here)
               ww.add(o, L.kidx[t.a], L.kidx[t.b]);
@@ -368,6 +372,8 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
       }
     }
     L.ly = ly.done(nt);
+    L.lyr = lyr.done(nt);
+    L.lyn = lyn.done(nt);
     L.xr = xr.done(nt);
     L.ww = ww.done(nt);
     if (leaf) {

@@ -49,7 +49,9 @@ struct LevelPlan {
   std::vector<int32_t> target_row, target_col;  // positions of every coupling target
 
   // triple groups into coupling targets, entries in ascending middle cluster j
-  Csr ly;  // (A block idx, B adm idx) with B admissible, A any
+  Csr ly;  // (A block idx, B adm idx) with B admissible, A any (report counters)
+  Csr lyr;  // (A adm idx, B adm idx): R x R, summed as S^A B_j S^B (P^A, P^B factored out)
+  Csr lyn;  // (A block idx, B adm idx) with A near: coll_a S^B (P^B factored out)
   Csr xr;  // (A adm idx, B block idx) with A admissible, B near
   Csr ww;  // leaf only: (A near idx, B near idx) full x full into a coupling target
   // per-target case ids for the report: counts of case 0..3 contributions
