@@ -165,18 +165,41 @@ def build_fd_laplacian(tree: ClusterTree, structure: BlockTree, points: np.ndarr
 
 
 # ---------------------------------------------------------------------------
+class _ResultOwner:
+    """Keeps the library-owned result (pinned host values) alive while a view exists."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            if self.handle:
+                h2c.lib().h2c_result_free(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 def _result(handle, a: H2Matrix) -> MmpResult:
+    """Wraps an h2c_result: the value array is a zero-copy view of the library's pinned buffer."""
     L = h2c.lib()
-    try:
-        d = h2c_matrix()
-        L.h2c_result_matrix(handle, C.byref(d))
-        prod = H2Matrix.from_desc(a.tree, a.structure, d)
-        r = h2c_report()
-        L.h2c_result_report(handle, C.byref(r))
-        rep = MmpReport.from_desc(r)
-    finally:
-        L.h2c_result_free(handle)
-    return MmpResult(prod, rep)
+    owner = _ResultOwner(handle)
+    d = h2c_matrix()
+    L.h2c_result_matrix(handle, C.byref(d))
+    nc, nb = a.tree.n_clusters, a.structure.n_blocks
+    w = 2 if d.scalar == h2c.H2C_COMPLEX else 1
+    n = w * d.n_values
+    vals = np.ctypeslib.as_array(d.values, shape=(max(1, n),))[:n] if n else np.zeros(0)
+    if w == 2:
+        vals = vals.view(np.complex128)
+    prod = H2Matrix(a.tree, a.structure, d.scalar, h2c._copy(d.row_rank, nc, np.int32),
+                    h2c._copy(d.col_rank, nc, np.int32), h2c._copy(d.row_degenerate, nc, np.uint8),
+                    h2c._copy(d.col_degenerate, nc, np.uint8), h2c._copy(d.row_offset, nc, np.int64),
+                    h2c._copy(d.col_offset, nc, np.int64), h2c._copy(d.block_offset, nb, np.int64), vals)
+    prod._owner = owner
+    r = h2c_report()
+    L.h2c_result_report(handle, C.byref(r))
+    return MmpResult(prod, MmpReport.from_desc(r))
 
 
 def mmp(a: H2Matrix, b: H2Matrix, eps_trunc: float, ctx: Optional[Context] = None) -> MmpResult:

@@ -518,9 +518,10 @@ struct EngineRun {
   }
 
   void seg(double* out, long long Os, long long Ooff, int Old, const int* omap, int M, int N, int n_out,
-           bool acc, std::initializer_list<Grp> gs) {
+           bool acc, std::initializer_list<Grp> gs, bool sym = false) {
     if (n_out <= 0) return;
     SegParams sp{};
+    sp.sym = sym ? 1 : 0;
     sp.out = out;
     sp.Os = Os;
     sp.Ooff = Ooff;
@@ -556,16 +557,19 @@ struct EngineRun {
         G.li = g.li;
         G.ri = g.ri;
       }
-      exec_macs += entries * int64_t(M) * N * g.K;
+      exec_macs += entries * int64_t(M) * N * g.K / (sym ? 2 : 1);
     }
     sp.ngroups = ng;
     if (ng == 0 && acc) return;
     int64_t macs = 0;
     for (const Grp& g : gs) macs += (g.csr ? g.csr->entries : n_out) * int64_t(M) * N * g.K;
+    if (sym) macs = macs / 2 + macs / (2 * ((M + 63) / 64));
     pre("seg_gemm", macs);
     const int TM = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
     const int TN = N <= 16 ? 16 : (N <= 32 ? 32 : 64);
-    const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
+    const int tm_ = (M + TM - 1) / TM;
+    const int tiles = sym ? tm_ * (tm_ + 1) / 2 : tm_ * ((N + TN - 1) / TN);
+    if (sym && (M != N || acc)) throw std::logic_error("seg: symmetric launch needs a square, fresh output");
     if (TM == 16 && TN == 16) launch_seg<16, 16>(sp, tiles);
     else if (TM == 16 && TN == 32) launch_seg<16, 32>(sp, tiles);
     else if (TM == 16 && TN == 64) launch_seg<16, 64>(sp, tiles);
@@ -580,6 +584,10 @@ struct EngineRun {
   // convenience: densely stored output [n_out][M x N]
   void segd(double* out, int M, int N, int n_out, std::initializer_list<Grp> gs) {
     seg(out, (long long)M * N, 0, M, nullptr, M, N, n_out, false, gs);
+  }
+  // Hermitian outputs (Gram sums): lower tiles only, mirrored in the epilogue
+  void segh(double* out, int M, int n_out, std::initializer_list<Grp> gs) {
+    seg(out, (long long)M * M, 0, M, nullptr, M, M, n_out, false, gs, true);
   }
 
   static Ref ref(const double* p, long long stride, int ld, int op, long long off = 0) {
@@ -841,18 +849,18 @@ struct EngineRun {
       DBuf g1(sz(n, NL, NL), s), g2(sz(n, NL, NL), s), g3(sz(n, NL, NL), s);
       {
         DBuf O(sz(nn, NL, NL), s);
-        segd(O, NL, NL, nn, {Grp{BF, op(BF, OP_H), NL, nullptr, nullptr, nullptr}});
+        segh(O, NL, nn, {Grp{BF, op(BF, OP_H), NL, nullptr, nullptr, nullptr}});
         DBuf H(sz(nn, NL, NL), s);
         seg_add(H, NN, O, NN, Q.hq, NN);
         O.release();
         DBuf Y(sz(nn, NL, NL), s);
         segd(Y, NL, NL, nn, {Grp{AF, ref(H, NN, NL, OP_N), NL, nullptr, nullptr, nullptr}});
-        segd(g1, NL, NL, n, {Grp{ref(Y, NN, NL, OP_N), op(AF, OP_H), NL, &Q.row_near, nullptr, nullptr}});
+        segh(g1, NL, n, {Grp{ref(Y, NN, NL, OP_N), op(AF, OP_H), NL, &Q.row_near, nullptr, nullptr}});
       }
-      segd(g2, NL, NL, n,
+      segh(g2, NL, n,
            {Grp{ref(FV, (long long)NL * KBr, NL, OP_N), ref(FV, (long long)NL * KBr, NL, OP_H), KBr, &Q.row_near,
                 nullptr, nullptr}});
-      segd(g3, NL, NL, n,
+      segh(g3, NL, n,
            {Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(A.Vr, (long long)NL * KAr, NL, OP_H), KAr, nullptr,
                 nullptr, nullptr}});
       Trunc tr = truncate(g1, g2, g3, n, NL, A.dgr_d[l]);
@@ -861,18 +869,18 @@ struct EngineRun {
       DBuf c1(sz(n, NL, NL), s), c2(sz(n, NL, NL), s), c3(sz(n, NL, NL), s);
       {
         DBuf Kb(sz(nn, NL, NL), s);
-        segd(Kb, NL, NL, nn, {Grp{op(AF, OP_T), op(AF, OP_C), NL, nullptr, nullptr, nullptr}});
+        segh(Kb, NL, nn, {Grp{op(AF, OP_T), op(AF, OP_C), NL, nullptr, nullptr, nullptr}});
         DBuf H(sz(nn, NL, NL), s);
         seg_add(H, NN, Kb, NN, Q.hqc, NN);
         Kb.release();
         DBuf Y(sz(nn, NL, NL), s);
         segd(Y, NL, NL, nn, {Grp{op(BF, OP_T), ref(H, NN, NL, OP_N), NL, nullptr, nullptr, nullptr}});
-        segd(c1, NL, NL, n, {Grp{ref(Y, NN, NL, OP_N), op(BF, OP_C), NL, &Q.col_near, nullptr, nullptr}});
+        segh(c1, NL, n, {Grp{ref(Y, NN, NL, OP_N), op(BF, OP_C), NL, &Q.col_near, nullptr, nullptr}});
       }
-      segd(c2, NL, NL, n,
+      segh(c2, NL, n,
            {Grp{ref(VF, (long long)KAc * NL, KAc, OP_T), ref(VF, (long long)KAc * NL, KAc, OP_C), KAc, &Q.col_near,
                 nullptr, nullptr}});
-      segd(c3, NL, NL, n,
+      segh(c3, NL, n,
            {Grp{ref(B.Vc, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_H), KBc, nullptr,
                 nullptr, nullptr}});
       Trunc tc = truncate(c1, c2, c3, n, NL, B.dgc_d[l]);
@@ -1010,23 +1018,23 @@ struct EngineRun {
       }
       // row transfer Gram (mmp.cpp:406-457)
       DBuf g1(sz(n, 2 * Kn, 2 * Kn), s), g2(sz(n, 2 * Kn, 2 * Kn), s), g3(sz(n, 2 * Kn, 2 * Kn), s);
-      segd(g1, 2 * Kn, 2 * Kn, n,
+      segh(g1, 2 * Kn, n,
            {Grp{ref(Mg, MM, 2 * Kn, OP_N), ref(Mg, MM, 2 * Kn, OP_H), 2 * Kq, &Q.row_merged, nullptr, nullptr}});
-      segd(g2, 2 * Kn, 2 * Kn, n,
+      segh(g2, 2 * Kn, n,
            {Grp{ref(X, 2LL * Kn * KBr, 2 * Kn, OP_N), ref(X, 2LL * Kn * KBr, 2 * Kn, OP_H), KBr, &Q.row_near,
                 nullptr, nullptr}});
-      segd(g3, 2 * Kn, 2 * Kn, n,
+      segh(g3, 2 * Kn, n,
            {Grp{ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_N), ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_H), KAr, nullptr, nullptr,
                 nullptr}});
       Trunc tr = truncate(g1, g2, g3, n, 2 * Kn, A.dgr_d[l]);
       // column transfer Gram (mmp.cpp:459-512)
       DBuf c1(sz(n, 2 * Kq, 2 * Kq), s), c2(sz(n, 2 * Kq, 2 * Kq), s), c3(sz(n, 2 * Kq, 2 * Kq), s);
-      segd(c1, 2 * Kq, 2 * Kq, n,
+      segh(c1, 2 * Kq, n,
            {Grp{ref(Mg, MM, 2 * Kn, OP_T), ref(Mg, MM, 2 * Kn, OP_C), 2 * Kn, &Q.col_merged, nullptr, nullptr}});
-      segd(c2, 2 * Kq, 2 * Kq, n,
+      segh(c2, 2 * Kq, n,
            {Grp{ref(Xc, 2LL * Kq * KAc, 2 * Kq, OP_N), ref(Xc, 2LL * Kq * KAc, 2 * Kq, OP_H), KAc, &Q.col_near,
                 nullptr, nullptr}});
-      segd(c3, 2 * Kq, 2 * Kq, n,
+      segh(c3, 2 * Kq, n,
            {Grp{ref(X3c, 2LL * Kq * KBc, 2 * Kq, OP_N), ref(X3c, 2LL * Kq * KBc, 2 * Kq, OP_H), KBc, nullptr, nullptr,
                 nullptr}});
       Trunc tc = truncate(c1, c2, c3, n, 2 * Kq, B.dgc_d[l]);
@@ -1237,7 +1245,8 @@ struct EngineRun {
     for (const Job& j : jobs) cl.add(j.src, flat.p + j.dst * W, j.rows, j.cols, j.sld, j.dld);
     cl.run(s, W, &launches);
     out.n_values = total;
-    CK(cudaMallocHost(reinterpret_cast<void**>(&out.values), std::max<size_t>(1, size_t(total) * W * sizeof(double))));
+    out.pool = ctx.pinned;
+    out.values = out.pool->take(std::max<size_t>(1, size_t(total) * W * sizeof(double)), &out.values_bytes);
     if (total)
       CK(cudaMemcpyAsync(out.values, flat.p, size_t(total) * W * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1245,7 +1254,38 @@ struct EngineRun {
 };
 
 HostResult::~HostResult() {
-  if (values) cudaFreeHost(values);
+  if (values && pool) pool->give(values, values_bytes);
+}
+
+double* PinnedPool::take(size_t bytes, size_t* got) {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = free_.lower_bound(bytes);
+    if (it != free_.end() && it->first <= 2 * bytes) {
+      double* p = it->second;
+      *got = it->first;
+      free_.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  CK(cudaMallocHost(&p, bytes));
+  *got = bytes;
+  return static_cast<double*>(p);
+}
+
+void PinnedPool::give(double* p, size_t bytes) {
+  std::lock_guard<std::mutex> g(mu_);
+  free_.emplace(bytes, p);
+  while (free_.size() > 4) {  // keep the pool bounded
+    auto it = free_.begin();
+    cudaFreeHost(it->second);
+    free_.erase(it);
+  }
+}
+
+PinnedPool::~PinnedPool() {
+  for (auto& [b, p] : free_) cudaFreeHost(p);
 }
 
 // ---------------------------------------------------------------------------

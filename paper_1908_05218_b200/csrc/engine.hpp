@@ -2,7 +2,9 @@
 #pragma once
 
 #include <array>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -19,8 +21,24 @@ struct ProfileEntry {
   int64_t macs = 0;
 };
 
+// Reusable pinned host buffers for product downloads (pinning tens of GB per
+// call would dominate the end-to-end time).  Shared by the context and the
+// results it hands out, so either may outlive the other.
+class PinnedPool {
+ public:
+  double* take(size_t bytes, size_t* got);
+  void give(double* p, size_t bytes);
+  ~PinnedPool();
+
+ private:
+  std::mutex mu_;
+  std::multimap<size_t, double*> free_;
+};
+
 // Host-side result of one product (flat layout of include/h2c_types.h).
 struct HostResult {
+  std::shared_ptr<PinnedPool> pool;
+  size_t values_bytes = 0;
   int32_t scalar = 0;
   std::vector<int32_t> row_rank, col_rank;
   std::vector<uint8_t> row_dg, col_dg;
@@ -64,6 +82,7 @@ class Context {
   void* stream() const { return stream_; }
   void* solver();  // cusolverDn handle bound to the stream (lazy)
   int64_t last_kernel_launches() const { return launches_; }
+  std::shared_ptr<PinnedPool> pinned = std::make_shared<PinnedPool>();
   // per (phase, kernel) timings of the last run, filled when profiling is on
   std::vector<ProfileEntry> last_profile;
   bool profile = false;

@@ -40,6 +40,7 @@ struct SegParams {
   int M, N;            // output dims (padded)
   int n_out;
   int accumulate;      // out (+)= sum
+  int sym;             // Hermitian output (Gram): only tiles m0 >= n0 are computed, mirrored
   int ngroups;
   SegGroup g[kMaxGroups];
 };
@@ -95,8 +96,18 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(const SegParams p) {
 
   const int t = blockIdx.x;
   const int tilesM = (p.M + TM - 1) / TM;
-  const int m0 = (blockIdx.y % tilesM) * TM;
-  const int n0 = (blockIdx.y / tilesM) * TN;
+  int m0, n0;
+  if (p.sym) {  // lower-triangular tile enumeration
+    const int y = blockIdx.y;
+    int tm = (int)((sqrt(8.0 * y + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= y) ++tm;
+    while (tm * (tm + 1) / 2 > y) --tm;
+    m0 = tm * TM;
+    n0 = (y - tm * (tm + 1) / 2) * TN;
+  } else {
+    m0 = (blockIdx.y % tilesM) * TM;
+    n0 = (blockIdx.y / tilesM) * TN;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = (warp & 1) * (TM / 2), wn = (warp >> 1) * (TN / 2);
@@ -292,6 +303,8 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(const SegParams p) {
         const int n = n0 + wn + 8 * j + 2 * tq + q;
         if (m < p.M && n < p.N) {
           const long long off = m + (long long)n * p.Old;
+          const long long offt = n + (long long)m * p.Old;  // mirrored position
+          const bool mirror = p.sym && m0 != n0;
           if constexpr (CPLX) {
             double re = acc[i][j][q], im = acci[i][j][q];
             if (p.accumulate) {
@@ -300,10 +313,15 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(const SegParams p) {
             }
             Op[2 * off] = re;
             Op[2 * off + 1] = im;
+            if (mirror) {
+              Op[2 * offt] = re;
+              Op[2 * offt + 1] = -im;
+            }
           } else {
             double v = acc[i][j][q];
             if (p.accumulate) v += Op[off];
             Op[off] = v;
+            if (mirror) Op[offt] = v;
           }
         }
       }
