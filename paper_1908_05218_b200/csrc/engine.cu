@@ -505,9 +505,32 @@ struct EngineRun {
   size_t sz(size_t count, int r, int c) const { return count * size_t(r) * c * W; }
 
   // ---- launchers -----------------------------------------------------------
+  const bool seg_v1 = std::getenv("H2B_SEG_V1") != nullptr;
   template <int TM, int TN>
   void launch_seg(const SegParams& sp, int tiles) {
     dim3 grid(sp.n_out, tiles);
+    if (!seg_v1) {
+      if (cplx) {
+        constexpr int sm = Seg2Cfg<TM, TN, true>::SMEM;
+        static bool attr = false;
+        if (!attr) {
+          CK(cudaFuncSetAttribute(seg_gemm2_kernel<TM, TN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          attr = true;
+        }
+        seg_gemm2_kernel<TM, TN, true><<<grid, 128, sm, s>>>(sp);
+      } else {
+        constexpr int sm = Seg2Cfg<TM, TN, false>::SMEM;
+        static bool attr = false;
+        if (!attr) {
+          CK(cudaFuncSetAttribute(seg_gemm2_kernel<TM, TN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          attr = true;
+        }
+        seg_gemm2_kernel<TM, TN, false><<<grid, 128, sm, s>>>(sp);
+      }
+      CK(cudaGetLastError());
+      launches++;
+      return;
+    }
     if (cplx) {
       seg_gemm_kernel<TM, TN, true><<<grid, 128, SegCfg<TM, TN, true>::SMEM, s>>>(sp);
     } else {

@@ -328,6 +328,290 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(const SegParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// seg_gemm v2: STAGES-deep cp.async pipeline of raw (untransformed) tiles.
+// Each operand chunk is copied in its native layout ([k][m] for op N/C of a
+// column-major L, [m][k] for op T/H; mirrored for R), 16 B per cp.async with
+// zero fill past the padded bounds; the fragment loads pick the addressing of
+// the layout (both conflict-free with a +4 double pad).  No register staging:
+// fewer registers, more CTAs per SM, and STAGES-1 chunks in flight hide the
+// L2/HBM latency of the next entry's operands.
+template <int TM, int TN, bool CPLX>
+struct Seg2Cfg {
+  static constexpr int W = CPLX ? 2 : 1;
+  static constexpr int KC = CPLX ? 8 : 16;
+  static constexpr int STAGES = 3;
+  static constexpr int LKM = KC * (TM + 4), LMK = TM * (KC + 4);
+  static constexpr int RKN = KC * (TN + 4), RNK = TN * (KC + 4);
+  static constexpr int LSZ = (LKM > LMK ? LKM : LMK) * W;
+  static constexpr int RSZ = (RKN > RNK ? RKN : RNK) * W;
+  static constexpr int STAGE = LSZ + RSZ;  // doubles
+  static constexpr int SMEM = STAGES * STAGE * 8;
+  static constexpr int FM = TM / 16, FN = TN / 16;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = ok ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int TM, int TN, bool CPLX>
+__global__ void __launch_bounds__(128) seg_gemm2_kernel(const SegParams p) {
+  using C = Seg2Cfg<TM, TN, CPLX>;
+  constexpr int KC = C::KC, W = C::W, ST = C::STAGES;
+  extern __shared__ __align__(16) double smem[];
+
+  const int t = blockIdx.x;
+  const int tilesM = (p.M + TM - 1) / TM;
+  int m0, n0;
+  if (p.sym) {
+    const int y = blockIdx.y;
+    int tm = (int)((sqrt(8.0 * y + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= y) ++tm;
+    while (tm * (tm + 1) / 2 > y) --tm;
+    m0 = tm * TM;
+    n0 = (y - tm * (tm + 1) / 2) * TN;
+  } else {
+    m0 = (blockIdx.y % tilesM) * TM;
+    n0 = (blockIdx.y / tilesM) * TN;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = (warp & 1) * (TM / 2), wn = (warp >> 1) * (TN / 2);
+
+  double acc[C::FM][C::FN][2];
+  double acci[CPLX ? C::FM : 1][CPLX ? C::FN : 1][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if constexpr (CPLX) {
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) acci[i][j][0] = acci[i][j][1] = 0.0;
+  }
+
+  auto entry_range = [&](int g, int& e0, int& e1) {
+    const SegGroup& G = p.g[g];
+    if (G.ptr) {
+      e0 = G.ptr[t];
+      e1 = G.ptr[t + 1];
+    } else {
+      e0 = 0;
+      e1 = 1;
+    }
+  };
+  auto load_entry = [&](Cursor& c) {
+    const SegGroup& G = p.g[c.g];
+    if (G.ptr) {
+      c.l = G.li[c.e];
+      c.r = G.ri[c.e];
+    } else {
+      c.l = G.li ? G.li[t] : t;
+      c.r = G.ri ? G.ri[t] : t;
+    }
+  };
+  auto settle = [&](Cursor& c) -> bool {
+    while (c.g < p.ngroups) {
+      if (c.e < c.e1 && c.k0 < p.g[c.g].K) return true;
+      if (c.e < c.e1) {
+        c.e++;
+        c.k0 = 0;
+        if (c.e < c.e1) {
+          load_entry(c);
+          continue;
+        }
+      }
+      c.g++;
+      if (c.g < p.ngroups) {
+        entry_range(c.g, c.e, c.e1);
+        c.k0 = 0;
+        if (c.e < c.e1) load_entry(c);
+      }
+    }
+    return false;
+  };
+  auto init = [&](Cursor& c) -> bool {
+    c.g = 0;
+    c.k0 = 0;
+    if (p.ngroups == 0) return false;
+    entry_range(0, c.e, c.e1);
+    if (c.e < c.e1) load_entry(c);
+    return settle(c);
+  };
+
+  // issue the cp.async copies of one chunk into `stage`
+  auto issue = [&](const Cursor& c, int stage) {
+    const SegGroup& G = p.g[c.g];
+    double* Ls = smem + stage * C::STAGE;
+    double* Rs = Ls + C::LSZ;
+    const double* Lp = G.L + (G.Ls * c.l + G.Loff) * W;
+    const double* Rp = G.R + (G.Rs * c.r + G.Roff) * W;
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+    constexpr int EPS = CPLX ? 1 : 2;  // elements per 16-byte segment
+    // L chunk: TM x KC elements
+    constexpr int LSEG = TM * KC / EPS;
+    for (int sgi = tid; sgi < LSEG; sgi += 128) {
+      int m, k;
+      if (!lt) {  // [k][m], contiguous in m
+        k = sgi / (TM / EPS);
+        m = (sgi % (TM / EPS)) * EPS;
+      } else {  // [m][k], contiguous in k
+        m = sgi / (KC / EPS);
+        k = (sgi % (KC / EPS)) * EPS;
+      }
+      const int gm = m0 + m, gk = c.k0 + k;
+      const bool ok = gm < p.M && gk < G.K;
+      const long long off = lt ? (gk + (long long)gm * G.Lld) : (gm + (long long)gk * G.Lld);
+      double* dst = lt ? Ls + (m * (KC + 4) + k) * W : Ls + (k * (TM + 4) + m) * W;
+      cp_async16(dst, ok ? Lp + off * W : Lp, ok);
+    }
+    constexpr int RSEG = TN * KC / EPS;
+    for (int sgi = tid; sgi < RSEG; sgi += 128) {
+      int n, k;
+      if (rt) {  // [k][n], contiguous in n
+        k = sgi / (TN / EPS);
+        n = (sgi % (TN / EPS)) * EPS;
+      } else {  // [n][k], contiguous in k
+        n = sgi / (KC / EPS);
+        k = (sgi % (KC / EPS)) * EPS;
+      }
+      const int gn = n0 + n, gk = c.k0 + k;
+      const bool ok = gn < p.N && gk < G.K;
+      const long long off = rt ? (gn + (long long)gk * G.Rld) : (gk + (long long)gn * G.Rld);
+      double* dst = rt ? Rs + (k * (TN + 4) + n) * W : Rs + (n * (KC + 4) + k) * W;
+      cp_async16(dst, ok ? Rp + off * W : Rp, ok);
+    }
+  };
+
+  Cursor ci, cc;
+  bool vi = init(ci);
+  bool vc = init(cc);
+#pragma unroll 1
+  for (int s = 0; s < ST - 1; ++s) {
+    if (vi) {
+      issue(ci, s);
+      ci.k0 += KC;
+      vi = settle(ci);
+    }
+    cp_async_commit();
+  }
+  int stage = 0, istage = ST - 1;
+#pragma unroll 1
+  while (vc) {
+    cp_async_wait<ST - 2>();
+    __syncthreads();
+    if (vi) {
+      issue(ci, istage);
+      ci.k0 += KC;
+      vi = settle(ci);
+    }
+    cp_async_commit();
+    istage = istage + 1 == ST ? 0 : istage + 1;
+
+    const SegGroup& G = p.g[cc.g];
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+    const double* Ls = smem + stage * C::STAGE;
+    const double* Rs = Ls + C::LSZ;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      const int k = kk + tq;
+      if constexpr (CPLX) {
+        const double cl = (G.opL == OP_H || G.opL == OP_C) ? -1.0 : 1.0;
+        const double cr = (G.opR == OP_H || G.opR == OP_C) ? -1.0 : 1.0;
+        double a[C::FM], ai[C::FM], b[C::FN], bi[C::FN];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i) {
+          const int m = wm + 8 * i + gq;
+          const double2 v = *reinterpret_cast<const double2*>(Ls + 2 * (lt ? m * (KC + 4) + k : k * (TM + 4) + m));
+          a[i] = v.x;
+          ai[i] = cl * v.y;
+        }
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) {
+          const int n = wn + 8 * j + gq;
+          const double2 v = *reinterpret_cast<const double2*>(Rs + 2 * (rt ? k * (TN + 4) + n : n * (KC + 4) + k));
+          b[j] = v.x;
+          bi[j] = cr * v.y;
+        }
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) {
+            dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            dmma(acc[i][j][0], acc[i][j][1], -ai[i], bi[j]);
+            dmma(acci[i][j][0], acci[i][j][1], a[i], bi[j]);
+            dmma(acci[i][j][0], acci[i][j][1], ai[i], b[j]);
+          }
+      } else {
+        double a[C::FM], b[C::FN];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i) {
+          const int m = wm + 8 * i + gq;
+          a[i] = Ls[lt ? m * (KC + 4) + k : k * (TM + 4) + m];
+        }
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) {
+          const int n = wn + 8 * j + gq;
+          b[j] = Rs[rt ? k * (TN + 4) + n : n * (KC + 4) + k];
+        }
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    }
+    stage = stage + 1 == ST ? 0 : stage + 1;
+    cc.k0 += KC;
+    vc = settle(cc);
+  }
+  cp_async_wait<0>();
+
+  const int o = p.omap ? p.omap[t] : t;
+  double* Op = p.out + (p.Os * o + p.Ooff) * W;
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int m = m0 + wm + 8 * i + gq;
+        const int n = n0 + wn + 8 * j + 2 * tq + q;
+        if (m < p.M && n < p.N) {
+          const long long off = m + (long long)n * p.Old;
+          const long long offt = n + (long long)m * p.Old;
+          const bool mirror = p.sym && m0 != n0;
+          if constexpr (CPLX) {
+            double re = acc[i][j][q], im = acci[i][j][q];
+            if (p.accumulate) {
+              re += Op[2 * off];
+              im += Op[2 * off + 1];
+            }
+            Op[2 * off] = re;
+            Op[2 * off + 1] = im;
+            if (mirror) {
+              Op[2 * offt] = re;
+              Op[2 * offt + 1] = -im;
+            }
+          } else {
+            double v = acc[i][j][q];
+            if (p.accumulate) v += Op[off];
+            Op[off] = v;
+            if (mirror) Op[offt] = v;
+          }
+        }
+      }
+}
+
+// ---------------------------------------------------------------------------
 // seg_add: out_t = sum_{e in seg(t)} in[idx_e]   (elements = matrix size in doubles)
 __global__ void seg_add_kernel(double* out, long long Os, const double* in, long long Is,
                                const int* ptr, const int* idx, long long elems, int accumulate) {
