@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -469,6 +470,38 @@ struct EngineRun {
     CK(cudaEventRecord(prof.back().b, s));
   }
   const bool debug_sync = std::getenv("H2B_DEBUG_SYNC") != nullptr;
+  const bool debug_check = std::getenv("H2B_DEBUG_CHECK") != nullptr;
+  // H2B_DEBUG_CHECK=1: host check of the truncation output (orthonormal kept columns)
+  void check_trunc(const Trunc& t, int count, int n) {
+    std::vector<double> v(sz(count, n, n));
+    std::vector<int> r(count);
+    CK(cudaMemcpyAsync(v.data(), t.vec.p, v.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(r.data(), t.rank.p, count * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double worst = 0;
+    int rmin = 1 << 30, rmax = 0;
+    for (int b = 0; b < count; ++b) {
+      rmin = std::min(rmin, r[b]);
+      rmax = std::max(rmax, r[b]);
+      const double* V = v.data() + size_t(b) * n * n * W;
+      for (int i = 0; i < r[b]; ++i)
+        for (int j = 0; j <= i; ++j) {
+          double re = 0, im = 0;
+          for (int k = 0; k < n; ++k) {
+            if (W == 1) re += V[k + size_t(i) * n] * V[k + size_t(j) * n];
+            else {
+              const double ar = V[2 * (k + size_t(i) * n)], ai = V[2 * (k + size_t(i) * n) + 1];
+              const double br = V[2 * (k + size_t(j) * n)], bi = V[2 * (k + size_t(j) * n) + 1];
+              re += ar * br + ai * bi;
+              im += ar * bi - ai * br;
+            }
+          }
+          worst = std::max(worst, std::hypot(re - (i == j ? 1.0 : 0.0), im));
+        }
+    }
+    std::fprintf(stderr, "[check] %s n=%d count=%d rank[%d,%d] orth_defect=%.3e\n", phase.c_str(), n, count, rmin,
+                 rmax, worst);
+  }
 
   // C
   std::vector<int> KCr, KCc;
@@ -690,22 +723,52 @@ struct EngineRun {
     CK(cudaMemcpyAsync(V.p, G.p, sz(count, n, n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
     const cudaDataType dt = cplx ? CUDA_C_64F : CUDA_R_64F;
     size_t dev_bytes = 0, host_bytes = 0;
-    pre("syev_batched", 0);
     auto chk = [](cusolverStatus_t st, const char* what) {
       if (st != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string("cuSOLVER ") + what + " failed: " + std::to_string(int(st)));
     };
-    chk(cusolverDnXsyevBatched_bufferSize(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p, n,
-                                          CUDA_R_64F, w.p, dt, &dev_bytes, &host_bytes, count),
-        "syevBatched_bufferSize");
-    DBuf work(dev_bytes / sizeof(double) + 2, s);
-    std::vector<char> hwork(host_bytes + 1);
     DVec<int> info;
     info.alloc(count, s);
-    chk(cusolverDnXsyevBatched(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p, n, CUDA_R_64F,
-                               w.p, dt, work.p, dev_bytes, hwork.data(), host_bytes, info.p, count),
-        "syevBatched");
-    post();
-    launches++;
+    pre("syevd_streams", 0);
+    {
+      // per-matrix divide-and-conquer eigensolves spread over side streams
+      cusolverDnHandle_t h0 = static_cast<cusolverDnHandle_t>(ctx.side_solver(0));
+      chk(cusolverDnXsyevd_bufferSize(h0, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p, n,
+                                      CUDA_R_64F, w.p, dt, &dev_bytes, &host_bytes),
+          "syevd_bufferSize");
+      const int ns = std::min(count, Context::kSideStreams);
+      const size_t wdoubles = dev_bytes / sizeof(double) + 2;
+      DBuf work(wdoubles * ns, s);
+      std::vector<std::vector<char>> hwork(ns, std::vector<char>(host_bytes + 1));
+      cudaEvent_t ready;
+      CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      CK(cudaEventRecord(ready, s));
+      std::vector<cudaEvent_t> done(ns);
+      for (int k = 0; k < ns; ++k) {
+        CK(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+        CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(ctx.side_stream(k)), ready, 0));
+      }
+      for (int b = 0; b < count; ++b) {
+        const int k = b % ns;
+        cusolverDnHandle_t hk = static_cast<cusolverDnHandle_t>(ctx.side_solver(k));
+        chk(cusolverDnXsyevd(hk, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt,
+                             V.p + size_t(b) * n * n * W, n, CUDA_R_64F, w.p + size_t(b) * n, dt,
+                             work.p + wdoubles * k, dev_bytes, hwork[k].data(), host_bytes, info.p + b),
+            "syevd");
+      }
+      for (int k = 0; k < ns; ++k) {
+        CK(cudaEventRecord(done[k], static_cast<cudaStream_t>(ctx.side_stream(k))));
+        CK(cudaStreamWaitEvent(s, done[k], 0));
+      }
+      CK(cudaStreamSynchronize(s));  // host workspaces and `work` lifetime
+      std::vector<int> hinfo(count);
+      CK(cudaMemcpy(hinfo.data(), info.p, count * sizeof(int), cudaMemcpyDeviceToHost));
+      for (int b = 0; b < count; ++b)
+        if (hinfo[b] != 0) throw std::logic_error("svd_truncate_gram: eigendecomposition failed (syevd info " +
+                                                  std::to_string(hinfo[b]) + ")");
+      cudaEventDestroy(ready);
+      for (auto e : done) cudaEventDestroy(e);
+    }
+    post();  // library kernels are not counted in `launches`
     pre("eig_finalize", 0);
     if (cplx)
       eig_finalize_kernel<true><<<count, 256, 0, s>>>(G, V, w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
@@ -730,6 +793,7 @@ struct EngineRun {
   }
 
   void pack(const Trunc& t, int count, int n, DBuf& out, int rows, int kc) {
+    if (debug_check) check_trunc(t, count, n);
     out.alloc(sz(count, rows, kc), s);
     pre("pack_basis", 0);
     pack_basis_kernel<<<count, 256, 0, s>>>(t.vec, n, out, rows, kc, t.rank.p, W);
@@ -1354,7 +1418,29 @@ void* Context::solver() {
   return solver_;
 }
 
+void* Context::side_stream(int i) {
+  side_solver(i);
+  return side_streams_[i];
+}
+
+void* Context::side_solver(int i) {
+  if (side_solvers_.empty()) {
+    for (int k = 0; k < kSideStreams; ++k) {
+      cudaStream_t st;
+      CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      cusolverDnHandle_t h;
+      if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
+      cusolverDnSetStream(h, st);
+      side_streams_.push_back(st);
+      side_solvers_.push_back(h);
+    }
+  }
+  return side_solvers_[i];
+}
+
 Context::~Context() {
+  for (void* h : side_solvers_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(h));
+  for (void* st : side_streams_) cudaStreamDestroy(static_cast<cudaStream_t>(st));
   if (solver_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_));
   dplan_.reset();
   if (stream_) {

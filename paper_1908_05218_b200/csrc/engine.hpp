@@ -81,6 +81,11 @@ class Context {
                       double eps, int adaptive, HostResult* download_to);
   void* stream() const { return stream_; }
   void* solver();  // cusolverDn handle bound to the stream (lazy)
+  // side streams with their own cusolverDn handles: independent per-matrix
+  // eigensolves of one level run concurrently instead of back to back
+  static constexpr int kSideStreams = 16;
+  void* side_stream(int i);
+  void* side_solver(int i);
   int64_t last_kernel_launches() const { return launches_; }
   std::shared_ptr<PinnedPool> pinned = std::make_shared<PinnedPool>();
   // per (phase, kernel) timings of the last run, filled when profiling is on
@@ -92,6 +97,7 @@ class Context {
   int device_;
   void* stream_ = nullptr;
   void* solver_ = nullptr;
+  std::vector<void*> side_streams_, side_solvers_;
   std::string err_;
   uint64_t plan_key_ = 0;
   std::unique_ptr<Plan> plan_;
