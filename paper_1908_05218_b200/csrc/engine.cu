@@ -471,37 +471,6 @@ struct EngineRun {
   }
   const bool debug_sync = std::getenv("H2B_DEBUG_SYNC") != nullptr;
   const bool debug_check = std::getenv("H2B_DEBUG_CHECK") != nullptr;
-  // H2B_DEBUG_CHECK=1: host check of the truncation output (orthonormal kept columns)
-  void check_trunc(const Trunc& t, int count, int n) {
-    std::vector<double> v(sz(count, n, n));
-    std::vector<int> r(count);
-    CK(cudaMemcpyAsync(v.data(), t.vec.p, v.size() * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(r.data(), t.rank.p, count * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    double worst = 0;
-    int rmin = 1 << 30, rmax = 0;
-    for (int b = 0; b < count; ++b) {
-      rmin = std::min(rmin, r[b]);
-      rmax = std::max(rmax, r[b]);
-      const double* V = v.data() + size_t(b) * n * n * W;
-      for (int i = 0; i < r[b]; ++i)
-        for (int j = 0; j <= i; ++j) {
-          double re = 0, im = 0;
-          for (int k = 0; k < n; ++k) {
-            if (W == 1) re += V[k + size_t(i) * n] * V[k + size_t(j) * n];
-            else {
-              const double ar = V[2 * (k + size_t(i) * n)], ai = V[2 * (k + size_t(i) * n) + 1];
-              const double br = V[2 * (k + size_t(j) * n)], bi = V[2 * (k + size_t(j) * n) + 1];
-              re += ar * br + ai * bi;
-              im += ar * bi - ai * br;
-            }
-          }
-          worst = std::max(worst, std::hypot(re - (i == j ? 1.0 : 0.0), im));
-        }
-    }
-    std::fprintf(stderr, "[check] %s n=%d count=%d rank[%d,%d] orth_defect=%.3e\n", phase.c_str(), n, count, rmin,
-                 rmax, worst);
-  }
 
   // C
   std::vector<int> KCr, KCc;
@@ -780,6 +749,49 @@ struct EngineRun {
     CK(cudaStreamSynchronize(s));  // host workspace lifetime
   }
   double jp_eps() const { return adaptive ? eps : 0.5; }
+
+  // H2B_DEBUG_CHECK=1: host check of the truncation output (orthonormal kept columns)
+  void check_trunc(const Trunc& t, int count, int n) {
+    std::vector<double> v(sz(count, n, n));
+    std::vector<int> r(count);
+    std::vector<double> ev(size_t(count) * n);
+    CK(cudaMemcpyAsync(ev.data(), t.val.p, ev.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(v.data(), t.vec.p, v.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(r.data(), t.rank.p, count * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double worst = 0;
+    int rmin = 1 << 30, rmax = 0;
+    for (int b = 0; b < count; ++b) {
+      rmin = std::min(rmin, r[b]);
+      rmax = std::max(rmax, r[b]);
+      const double* V = v.data() + size_t(b) * n * n * W;
+      for (int i = 0; i < r[b]; ++i)
+        for (int j = 0; j <= i; ++j) {
+          double re = 0, im = 0;
+          for (int k = 0; k < n; ++k) {
+            if (W == 1) re += V[k + size_t(i) * n] * V[k + size_t(j) * n];
+            else {
+              const double ar = V[2 * (k + size_t(i) * n)], ai = V[2 * (k + size_t(i) * n) + 1];
+              const double br = V[2 * (k + size_t(j) * n)], bi = V[2 * (k + size_t(j) * n) + 1];
+              re += ar * br + ai * bi;
+              im += ar * bi - ai * br;
+            }
+          }
+          worst = std::max(worst, std::hypot(re - (i == j ? 1.0 : 0.0), im));
+        }
+    }
+    double margin = 1e300;
+    const double e_ = jp_eps();
+    for (int b = 0; b < count; ++b) {
+      const double top = ev[size_t(b) * n];
+      for (int i = 0; i < n; ++i) {
+        const double l = ev[size_t(b) * n + i];
+        if (l > 0 && top > 0) margin = std::min(margin, std::abs(l - e_ * top) / (e_ * top));
+      }
+    }
+    std::fprintf(stderr, "[check] %s n=%d count=%d rank[%d,%d] orth_defect=%.3e min_margin=%.3e\n", phase.c_str(), n,
+                 count, rmin, rmax, worst, margin);
+  }
 
   // ranks to host, padded width
   int fetch_ranks(const DVec<int32_t>& r, int count, std::vector<int64_t>& out) {

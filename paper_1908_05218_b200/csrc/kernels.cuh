@@ -732,9 +732,17 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
     ss += __shfl_xor_sync(0xffffffffu, ss, o);
     nz |= __shfl_xor_sync(0xffffffffu, nz, o);
   }
+  // deterministic block reduction (fixed order) of the Frobenius norm
+  __shared__ double warp_ss[32];
   if ((tid & 31) == 0) {
-    atomicAdd(&fro, ss);
+    warp_ss[tid >> 5] = ss;
     if (nz) nonzero = 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double f = 0.0;
+    for (int w = 0; w < nt / 32; ++w) f += warp_ss[w];
+    fro = f;
   }
   __syncthreads();
   const double tol_abs = 1e-22 * sqrt(fro);

@@ -29,3 +29,9 @@ if run_oracle:
     x = O.random_vector(n, 9)
     d = O.mvp(r1.product, x) - O.mvp(ro.product, x)
     print("gpu-vs-oracle mvp rel", np.linalg.norm(d) / np.linalg.norm(O.mvp(ro.product, x)))
+# where do the two GPU runs differ?
+t_ = A.tree
+for l, ids in enumerate(t_.levels):
+    a, b = r1.product.row_rank[ids], r2.product.row_rank[ids]
+    if not np.array_equal(a, b):
+        print("level", l, "rank differences at", int(np.sum(a != b)), "clusters", flush=True)
