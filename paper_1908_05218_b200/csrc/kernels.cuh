@@ -749,6 +749,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
   const int half = n / 2;
   if (nonzero) {
     for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
+      __syncthreads();  // every thread has read the previous sweep's flag
       if (tid == 0) any_rot = 0;
       __syncthreads();
       for (int step = 0; step < n - 1; ++step) {
@@ -827,7 +828,8 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
         }
         __syncthreads();
       }
-      if (!any_rot) break;
+      const int rotated = any_rot;
+      if (!rotated) break;
     }
   }
   __syncthreads();
