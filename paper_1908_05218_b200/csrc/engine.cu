@@ -697,45 +697,23 @@ struct EngineRun {
     };
     DVec<int> info;
     info.alloc(count, s);
-    pre("syevd_streams", 0);
+    pre("syev_batched", 0);
     {
-      // per-matrix divide-and-conquer eigensolves spread over side streams
-      cusolverDnHandle_t h0 = static_cast<cusolverDnHandle_t>(ctx.side_solver(0));
-      chk(cusolverDnXsyevd_bufferSize(h0, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p, n,
-                                      CUDA_R_64F, w.p, dt, &dev_bytes, &host_bytes),
-          "syevd_bufferSize");
-      const int ns = std::min(count, Context::kSideStreams);
-      const size_t wdoubles = dev_bytes / sizeof(double) + 2;
-      DBuf work(wdoubles * ns, s);
-      std::vector<std::vector<char>> hwork(ns, std::vector<char>(host_bytes + 1));
-      cudaEvent_t ready;
-      CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-      CK(cudaEventRecord(ready, s));
-      std::vector<cudaEvent_t> done(ns);
-      for (int k = 0; k < ns; ++k) {
-        CK(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
-        CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(ctx.side_stream(k)), ready, 0));
-      }
-      for (int b = 0; b < count; ++b) {
-        const int k = b % ns;
-        cusolverDnHandle_t hk = static_cast<cusolverDnHandle_t>(ctx.side_solver(k));
-        chk(cusolverDnXsyevd(hk, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt,
-                             V.p + size_t(b) * n * n * W, n, CUDA_R_64F, w.p + size_t(b) * n, dt,
-                             work.p + wdoubles * k, dev_bytes, hwork[k].data(), host_bytes, info.p + b),
-            "syevd");
-      }
-      for (int k = 0; k < ns; ++k) {
-        CK(cudaEventRecord(done[k], static_cast<cudaStream_t>(ctx.side_stream(k))));
-        CK(cudaStreamWaitEvent(s, done[k], 0));
-      }
-      CK(cudaStreamSynchronize(s));  // host workspaces and `work` lifetime
+      cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.solver());
+      chk(cusolverDnXsyevBatched_bufferSize(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p,
+                                            n, CUDA_R_64F, w.p, dt, &dev_bytes, &host_bytes, count),
+          "syevBatched_bufferSize");
+      DBuf work(dev_bytes / sizeof(double) + 2, s);
+      std::vector<char> hwork(host_bytes + 1);
+      chk(cusolverDnXsyevBatched(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p, n,
+                                 CUDA_R_64F, w.p, dt, work.p, dev_bytes, hwork.data(), host_bytes, info.p, count),
+          "syevBatched");
+      CK(cudaStreamSynchronize(s));  // host workspace lifetime
       std::vector<int> hinfo(count);
       CK(cudaMemcpy(hinfo.data(), info.p, count * sizeof(int), cudaMemcpyDeviceToHost));
       for (int b = 0; b < count; ++b)
-        if (hinfo[b] != 0) throw std::logic_error("svd_truncate_gram: eigendecomposition failed (syevd info " +
-                                                  std::to_string(hinfo[b]) + ")");
-      cudaEventDestroy(ready);
-      for (auto e : done) cudaEventDestroy(e);
+        if (hinfo[b] != 0)
+          throw std::logic_error("svd_truncate_gram: eigendecomposition failed (syev info " + std::to_string(hinfo[b]) + ")");
     }
     post();  // library kernels are not counted in `launches`
     pre("eig_finalize", 0);
