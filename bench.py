@@ -288,6 +288,7 @@ def run_b200(args) -> None:
         }
         if args.profile:
             line["profile"] = sorted(prof, key=lambda e: -e["ms"])[:25]
+            line["profile_sum_ms"] = round(prof_ms, 3)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

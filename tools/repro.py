@@ -12,5 +12,13 @@ t0 = time.time()
 r = P.mmp(A, A, eps, ctx)
 print("ok", n, time.time() - t0, "flops", r.report.flops, "maxrank", r.report.max_rank(), "dev", r.report.device_seconds,
       "ranks", [(l.max_row_rank, l.max_col_rank) for l in r.report.levels], flush=True)
-for e in sorted(ctx.profile(), key=lambda e: -e["ms"])[:15]:
+r = P.mmp(A, A, eps, ctx)  # warm second run
+prof = ctx.profile()
+print("second run dev", r.report.device_seconds, "profile sum ms", sum(e["ms"] for e in prof), "entries", len(prof))
+agg = {}
+for e in prof:
+    k = e["name"].split("/")[1]
+    agg[k] = agg.get(k, 0) + e["ms"]
+print({k: round(v, 1) for k, v in sorted(agg.items(), key=lambda x: -x[1])})
+for e in sorted(prof, key=lambda e: -e["ms"])[:40]:
     print(e)
