@@ -480,6 +480,21 @@ struct EngineRun {
   std::vector<DBuf> Tr, Tc, Tg;
   // per-level intermediates
   std::vector<DBuf> Bp, PA, PB, LA, RB;
+  // auxiliary stream for the C-independent leaf full targets
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_full = nullptr;
+  bool joined = false;
+  std::vector<DBuf> hold;
+  void join() {
+    if (joined) return;
+    CK(cudaStreamWaitEvent(s, ev_full, 0));
+    hold.clear();  // frees on the main stream, ordered after the join
+    joined = true;
+  }
+  ~EngineRun() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_full) cudaEventDestroy(ev_full);
+  }
 
   EngineRun(Context& c, const Plan& p, const DevPlan& dp, const DevOperand& a, const DevOperand& b,
             double e, bool ad, cudaStream_t st)
@@ -502,6 +517,9 @@ struct EngineRun {
     PB.resize(D + 1);
     LA.resize(D + 2);
     RB.resize(D + 2);
+    s_aux = static_cast<cudaStream_t>(c.side_stream(0));
+    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_full, cudaEventDisableTiming));
   }
 
   size_t sz(size_t count, int r, int c) const { return count * size_t(r) * c * W; }
@@ -841,15 +859,24 @@ struct EngineRun {
 
   // ---- admissible-block factors shared by leaf and upper levels --------------
   // SB = S^A B_j, LA = P^A SB ; BS = B_i S^B, RB = BS P^B  (mmp.cpp:325-332,389-390)
+  // SB = S^A B_j per admissible block (independent of C)
+  void make_sb(int l, DBuf& SB) {
+    const LevelPlan& L = P.lv[l];
+    const DevLevel& Q = DP.lv[l];
+    const int na = static_cast<int>(L.adm.size());
+    const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l];
+    SB.alloc(sz(na, KAr, KBr), s);
+    segd(SB, KAr, KBr, na,
+         {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), KAc, nullptr,
+              nullptr, Q.adm_col}});
+  }
+
   void adm_factors(int l, DBuf& SB) {
     const LevelPlan& L = P.lv[l];
     const DevLevel& Q = DP.lv[l];
     const int na = static_cast<int>(L.adm.size());
     const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l], Kr = KCr[l], Kc = KCc[l];
-    SB.alloc(sz(na, KAr, KBr), s);
-    segd(SB, KAr, KBr, na,
-         {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(Bp[l], (long long)KAc * KBr, KAc, OP_N), KAc, nullptr,
-              nullptr, Q.adm_col}});
+    if (!SB.p) make_sb(l, SB);
     seg(LA[l], (long long)Kr * KBr, 0, Kr, Q.adm, Kr, KBr, na, false,
         {Grp{ref(PA[l], (long long)Kr * KAr, Kr, OP_N), ref(SB, (long long)KAr * KBr, KAr, OP_N), KAr, nullptr,
              Q.adm_row, nullptr}});
@@ -919,6 +946,19 @@ struct EngineRun {
     DBuf FV(sz(nn, NL, KBr), s), VF(sz(nn, KAc, NL), s);
     segd(FV, NL, KBr, nn, {Grp{AF, ref(B.Vr, (long long)NL * KBr, NL, OP_N), NL, nullptr, nullptr, Q.near_col}});
     segd(VF, KAc, NL, nn, {Grp{ref(A.Vc, (long long)NL * KAc, NL, OP_T), BF, NL, nullptr, Q.near_row, nullptr}});
+    DBuf SB;
+    make_sb(l, SB);
+    {  // full targets on the auxiliary stream, overlapping everything until split()
+      CK(cudaEventRecord(ev_fork, s));
+      CK(cudaStreamWaitEvent(s_aux, ev_fork, 0));
+      cudaStream_t keep = s;
+      const std::string ph = phase;
+      s = s_aux;
+      leaf_full_targets(FV, VF, SB);
+      s = keep;
+      phase = ph;
+      CK(cudaEventRecord(ev_full, s_aux));
+    }
 
     if (adaptive) {
       phase = "leaf.row_gram";
@@ -1000,34 +1040,48 @@ struct EngineRun {
     DBuf WA(sz(nn, Kr, NL), s), WB(sz(nn, NL, Kc), s);
     segd(WA, Kr, NL, nn, {Grp{ref(Vr, (long long)NL * Kr, NL, OP_H), AF, NL, nullptr, Q.near_row, nullptr}});
     segd(WB, NL, Kc, nn, {Grp{BF, ref(Vc, (long long)NL * Kc, NL, OP_C), NL, nullptr, nullptr, Q.near_col}});
-    DBuf SB;
     adm_factors(l, SB);
 
     phase = "leaf.coupling_targets";
     targets(l, SB, &WA, &WB, nullptr, 0);
     WA.release();
     WB.release();
+    // the auxiliary stream still reads these: release after the join
+    hold.push_back(std::move(FV));
+    hold.push_back(std::move(VF));
+    hold.push_back(std::move(SB));
 
+  }
+
+  // ---- leaf full targets (mmp.cpp:310-317) on the auxiliary stream ------------
+  // C.full = FF + (sum FV S^B) V^B^T + V^A (sum S^A VF + (sum S^A B S^B) V^B^T).
+  // Independent of C's bases, so it overlaps the Gram / eigensolver / upper
+  // level pipeline of the main stream; split() joins it.
+  void leaf_full_targets(const DBuf& FV, const DBuf& VF, const DBuf& SB) {
+    const int l = D;
+    const LevelPlan& L = P.lv[l];
+    const DevLevel& Q = DP.lv[l];
+    const int nn = static_cast<int>(L.nearb.size());
+    const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l];
+    const long long NN = (long long)NL * NL;
+    const Ref AF = ref(A.F, NN, NL, OP_N), BF = ref(B.F, NN, NL, OP_N);
     phase = "leaf.full_targets";
-    // full targets (mmp.cpp:310-317): C.full = FF + (sum FV S^B) V^B^T + V^A (sum S^A VF + (sum S^A B S^B) V^B^T)
-    {
-      const Ref BS = ref(B.S[l], (long long)KBr * KBc, KBr, OP_N);
-      DBuf T2(sz(nn, NL, KBc), s), T4(sz(nn, KAr, KBc), s), U(sz(nn, KAr, NL), s);
-      segd(T2, NL, KBc, nn, {Grp{ref(FV, (long long)NL * KBr, NL, OP_N), BS, KBr, &Q.fr, nullptr, nullptr}});
-      segd(T4, KAr, KBc, nn, {Grp{ref(SB, (long long)KAr * KBr, KAr, OP_N), BS, KBr, &Q.rr, nullptr, nullptr}});
-      segd(U, KAr, NL, nn,
-           {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(VF, (long long)KAc * NL, KAc, OP_N), KAc, &Q.rf,
-                nullptr, nullptr},
-            Grp{ref(T4, (long long)KAr * KBc, KAr, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
-                nullptr, Q.near_col}});
-      F.alloc(sz(nn, NL, NL), s);
-      segd(F, NL, NL, nn,
-           {Grp{AF, BF, NL, &Q.ff, nullptr, nullptr},
-            Grp{ref(T2, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
-                nullptr, Q.near_col},
-            Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(U, (long long)KAr * NL, KAr, OP_N), KAr, nullptr,
-                Q.near_row, nullptr}});
-    }
+    const Ref BS = ref(B.S[l], (long long)KBr * KBc, KBr, OP_N);
+    DBuf T2(sz(nn, NL, KBc), s), T4(sz(nn, KAr, KBc), s), U(sz(nn, KAr, NL), s);
+    segd(T2, NL, KBc, nn, {Grp{ref(FV, (long long)NL * KBr, NL, OP_N), BS, KBr, &Q.fr, nullptr, nullptr}});
+    segd(T4, KAr, KBc, nn, {Grp{ref(SB, (long long)KAr * KBr, KAr, OP_N), BS, KBr, &Q.rr, nullptr, nullptr}});
+    segd(U, KAr, NL, nn,
+         {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(VF, (long long)KAc * NL, KAc, OP_N), KAc, &Q.rf,
+              nullptr, nullptr},
+          Grp{ref(T4, (long long)KAr * KBc, KAr, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
+              nullptr, Q.near_col}});
+    F.alloc(sz(nn, NL, NL), s);
+    segd(F, NL, NL, nn,
+         {Grp{AF, BF, NL, &Q.ff, nullptr, nullptr},
+          Grp{ref(T2, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
+              nullptr, Q.near_col},
+          Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(U, (long long)KAr * NL, KAr, OP_N), KAr, nullptr,
+              Q.near_row, nullptr}});
   }
 
   void formatted_bases(int l) {
@@ -1170,6 +1224,7 @@ struct EngineRun {
 
   // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------
   void split() {
+    join();
     phase = "split";
     for (int l = 1; l < D; ++l) {
       const LevelPlan& L = P.lv[l];
@@ -1211,6 +1266,7 @@ struct EngineRun {
     leaf_phase();
     for (int l = D - 1; l >= 1; --l) upper_level(l);
     split();
+    join();
   }
 
   // per (phase, kernel) totals of the profiled launches
