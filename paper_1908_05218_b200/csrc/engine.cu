@@ -25,6 +25,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -32,6 +33,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <exception>
 #include <thread>
 #include <tuple>
 
@@ -441,7 +443,7 @@ struct EngineRun {
   cudaStream_t s;
   int D, NL;
   int64_t exec_macs = 0;
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};
   // optional per-launch profiling (CUDA events on the engine stream)
   struct ProfRec {
     std::string phase;
@@ -459,6 +461,17 @@ struct EngineRun {
     CK(cudaEventCreate(&r.b));
     CK(cudaEventRecord(r.a, s));
     prof.push_back(r);
+  }
+  // phase boundary on the main stream: in profiling mode an event pair per
+  // phase measures its wall time on the device, gaps included
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  void mark(const std::string& name) {
+    phase = name;
+    if (!profiling) return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, s));
+    marks.push_back({name, e});
   }
   void post() {
     if (debug_sync) {  // H2B_DEBUG_SYNC=1: locate a faulting launch by phase
@@ -654,8 +667,10 @@ struct EngineRun {
     DBuf vec, val;
     DVec<int32_t> rank;
     DVec<uint8_t> degen;
+    DBuf G;  // deferred library eigensolve input
+    int n = 0, count = 0;
   };
-  Trunc truncate(DBuf& g1, DBuf& g2, DBuf& g3, int count, int n, const DVec<uint8_t>& opdeg) {
+  Trunc truncate(DBuf& g1, DBuf& g2, DBuf& g3, int count, int n, const DVec<uint8_t>& opdeg, bool defer = false) {
     Trunc t;
     DBuf G(sz(count, n, n), s);
     t.degen.alloc(count, s);
@@ -695,17 +710,49 @@ struct EngineRun {
       CK(cudaGetLastError());
       post();
       launches++;
+    } else if (defer) {
+      t.G = std::move(G);  // solved later by solve_deferred (possibly concurrently)
+      t.n = n;
+      t.count = count;
     } else {
       library_eig(G, count, n, t);
     }
     return t;
   }
 
+  // Runs a deferred library eigensolve on side stream 1 in a host thread, so
+  // the row and column eigensolves of a level overlap (cuSOLVER's batched
+  // solver is launch-latency bound).
+  std::thread solve_async(Trunc& t, std::exception_ptr& err) {
+    if (!t.G.p) return std::thread();
+    cudaStream_t st = static_cast<cudaStream_t>(ctx.side_stream(1));
+    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.side_solver(1));
+    CK(cudaEventRecord(ev_fork, s));
+    CK(cudaStreamWaitEvent(st, ev_fork, 0));
+    CK(cudaSetDevice(ctx.device()));
+    return std::thread([this, &t, &err, st, h] {
+      try {
+        CK(cudaSetDevice(ctx.device()));
+        library_eig_on(t.G, t.count, t.n, t, st, h);
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+  }
+  void finish_async(std::thread& th, std::exception_ptr& err, Trunc& t) {
+    if (th.joinable()) th.join();
+    if (err) std::rethrow_exception(err);
+    t.G.release();
+  }
+
   // Gram dimensions beyond the shared-memory Jacobi (upper levels, where C's
   // ranks grow): batched Hermitian eigensolver from cuSOLVER, then the same
   // truncation rule on the device.
   void library_eig(const DBuf& G, int count, int n, Trunc& t) {
-    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.solver());
+    library_eig_on(G, count, n, t, s, static_cast<cusolverDnHandle_t>(ctx.solver()));
+  }
+  void library_eig_on(const DBuf& G, int count, int n, Trunc& t, cudaStream_t s, cusolverDnHandle_t h) {
+    const bool main_thread = s == this->s;
     DBuf V(sz(count, n, n), s), w(size_t(count) * n, s);
     CK(cudaMemcpyAsync(V.p, G.p, sz(count, n, n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
     const cudaDataType dt = cplx ? CUDA_C_64F : CUDA_R_64F;
@@ -715,9 +762,8 @@ struct EngineRun {
     };
     DVec<int> info;
     info.alloc(count, s);
-    pre("syev_batched", 0);
+    if (main_thread) pre("syev_batched", 0);
     {
-      cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.solver());
       chk(cusolverDnXsyevBatched_bufferSize(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p,
                                             n, CUDA_R_64F, w.p, dt, &dev_bytes, &host_bytes, count),
           "syevBatched_bufferSize");
@@ -733,14 +779,14 @@ struct EngineRun {
         if (hinfo[b] != 0)
           throw std::logic_error("svd_truncate_gram: eigendecomposition failed (syev info " + std::to_string(hinfo[b]) + ")");
     }
-    post();  // library kernels are not counted in `launches`
-    pre("eig_finalize", 0);
+    if (main_thread) post();  // library kernels are not counted in `launches`
+    if (main_thread) pre("eig_finalize", 0);
     if (cplx)
       eig_finalize_kernel<true><<<count, 256, 0, s>>>(G, V, w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
     else
       eig_finalize_kernel<false><<<count, 256, 0, s>>>(G, V, w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
     CK(cudaGetLastError());
-    post();
+    if (main_thread) post();
     launches++;
     CK(cudaStreamSynchronize(s));  // host workspace lifetime
   }
@@ -834,7 +880,7 @@ struct EngineRun {
 
   // ---- basis products B_j = (V^A_col,j)^T V^B_row,j (mmp.cpp:106-124) --------
   void basis_products() {
-    phase = "basis_products";
+    mark("basis_products");
     const LevelPlan& LL = P.lv[D];
     Bp[D].alloc(sz(LL.n, A.Kc[D], B.Kr[D]), s);
     segd(Bp[D], A.Kc[D], B.Kr[D], LL.n,
@@ -961,7 +1007,7 @@ struct EngineRun {
     }
 
     if (adaptive) {
-      phase = "leaf.row_gram";
+      mark("leaf.row_gram");
       // row Grams (mmp.cpp:164-200)
       DBuf g1(sz(n, NL, NL), s), g2(sz(n, NL, NL), s), g3(sz(n, NL, NL), s);
       {
@@ -981,7 +1027,7 @@ struct EngineRun {
            {Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(A.Vr, (long long)NL * KAr, NL, OP_H), KAr, nullptr,
                 nullptr, nullptr}});
       Trunc tr = truncate(g1, g2, g3, n, NL, A.dgr_d[l]);
-      phase = "leaf.col_gram";
+      mark("leaf.col_gram");
       // column Grams (mmp.cpp:202-238)
       DBuf c1(sz(n, NL, NL), s), c2(sz(n, NL, NL), s), c3(sz(n, NL, NL), s);
       {
@@ -1001,7 +1047,7 @@ struct EngineRun {
            {Grp{ref(B.Vc, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_H), KBc, nullptr,
                 nullptr, nullptr}});
       Trunc tc = truncate(c1, c2, c3, n, NL, B.dgc_d[l]);
-      phase = "leaf.bases";
+      mark("leaf.bases");
       KCr[l] = fetch_ranks(tr.rank, n, rcr[l]);
       KCc[l] = fetch_ranks(tc.rank, n, rcc[l]);
       pack(tr, n, NL, Vr, NL, KCr[l]);
@@ -1027,7 +1073,7 @@ struct EngineRun {
     }
     const int Kr = KCr[l], Kc = KCc[l];
 
-    phase = "leaf.collect";
+    mark("leaf.collect");
     // collected full blocks (mmp.cpp:287-298) and W factors of the F x F case
     LA[l].alloc(sz(nb, Kr, KBr), s);
     RB[l].alloc(sz(nb, KAc, Kc), s);
@@ -1042,7 +1088,7 @@ struct EngineRun {
     segd(WB, NL, Kc, nn, {Grp{BF, ref(Vc, (long long)NL * Kc, NL, OP_C), NL, nullptr, nullptr, Q.near_col}});
     adm_factors(l, SB);
 
-    phase = "leaf.coupling_targets";
+    mark("leaf.coupling_targets");
     targets(l, SB, &WA, &WB, nullptr, 0);
     WA.release();
     WB.release();
@@ -1105,7 +1151,7 @@ struct EngineRun {
     const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l];
     const long long MM = 4LL * Kn * Kq;
 
-    phase = "L" + std::to_string(l) + ".assemble";
+    mark("L" + std::to_string(l) + ".assemble");
     // merged children couplings and assembled collected blocks (mmp.cpp:344-404)
     DBuf Mg, Aa, Ab;
     gather(Mg, nm, Tg[l + 1].p + size_t(Lc.adm.size()) * Kn * Kq * W, (long long)Kn * Kq, Kn, Kq, Q.merged_quad);
@@ -1126,7 +1172,7 @@ struct EngineRun {
     Ab.release();
 
     if (adaptive) {
-      phase = "L" + std::to_string(l) + ".grams";
+      mark("L" + std::to_string(l) + ".grams");
       // X3 = blkdiag(P^A_children) T^A_row ; X3c = blkdiag(P^B)^T conj(T^B_col) ; Y3 = blkdiag(P^B)^T T^B_col
       DBuf X3(sz(n, 2 * Kn, KAr), s), X3c(sz(n, 2 * Kq, KBc), s), Y3;
       for (int c = 0; c < 2; ++c) {
@@ -1157,7 +1203,9 @@ struct EngineRun {
       segh(g3, 2 * Kn, n,
            {Grp{ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_N), ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_H), KAr, nullptr, nullptr,
                 nullptr}});
-      Trunc tr = truncate(g1, g2, g3, n, 2 * Kn, A.dgr_d[l]);
+      Trunc tr = truncate(g1, g2, g3, n, 2 * Kn, A.dgr_d[l], /*defer=*/true);
+      std::exception_ptr row_err;
+      std::thread row_th = solve_async(tr, row_err);
       // column transfer Gram (mmp.cpp:459-512)
       DBuf c1(sz(n, 2 * Kq, 2 * Kq), s), c2(sz(n, 2 * Kq, 2 * Kq), s), c3(sz(n, 2 * Kq, 2 * Kq), s);
       segh(c1, 2 * Kq, n,
@@ -1168,7 +1216,14 @@ struct EngineRun {
       segh(c3, 2 * Kq, n,
            {Grp{ref(X3c, 2LL * Kq * KBc, 2 * Kq, OP_N), ref(X3c, 2LL * Kq * KBc, 2 * Kq, OP_H), KBc, nullptr, nullptr,
                 nullptr}});
-      Trunc tc = truncate(c1, c2, c3, n, 2 * Kq, B.dgc_d[l]);
+      Trunc tc;
+      try {
+        tc = truncate(c1, c2, c3, n, 2 * Kq, B.dgc_d[l]);
+      } catch (...) {
+        if (row_th.joinable()) row_th.join();
+        throw;
+      }
+      finish_async(row_th, row_err, tr);
       KCr[l] = fetch_ranks(tr.rank, n, rcr[l]);
       KCc[l] = fetch_ranks(tc.rank, n, rcc[l]);
       pack(tr, n, 2 * Kn, Tr[l], 2 * Kn, KCr[l]);
@@ -1197,7 +1252,7 @@ struct EngineRun {
     Bp[l + 1].release();
     const int Kr = KCr[l], Kc = KCc[l];
 
-    phase = "L" + std::to_string(l) + ".collect";
+    mark("L" + std::to_string(l) + ".collect");
     // collects of subdivided blocks (mmp.cpp:544-552)
     LA[l].alloc(sz(nb, Kr, KBr), s);
     RB[l].alloc(sz(nb, KAc, Kc), s);
@@ -1212,7 +1267,7 @@ struct EngineRun {
     DBuf SB;
     adm_factors(l, SB);
 
-    phase = "L" + std::to_string(l) + ".targets";
+    mark("L" + std::to_string(l) + ".targets");
     // case 1 over merged children couplings: Z = T^C_row^H M (mmp.cpp:573-585)
     DBuf Z(sz(nm, Kr, 2 * Kq), s);
     segd(Z, Kr, 2 * Kq, nm,
@@ -1225,7 +1280,7 @@ struct EngineRun {
   // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------
   void split() {
     join();
-    phase = "split";
+    mark("split");
     for (int l = 1; l < D; ++l) {
       const LevelPlan& L = P.lv[l];
       const LevelPlan& Lc = P.lv[l + 1];
@@ -1293,6 +1348,21 @@ struct EngineRun {
       cudaEventDestroy(r.b);
     }
     prof.clear();
+    // phase wall times (main stream, gaps included)
+    if (!marks.empty()) {
+      cudaEvent_t end;
+      CK(cudaEventCreate(&end));
+      CK(cudaEventRecord(end, s));
+      CK(cudaEventSynchronize(end));
+      for (size_t i = 0; i < marks.size(); ++i) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, marks[i].second, i + 1 < marks.size() ? marks[i + 1].second : end));
+        out.push_back({"wall:" + marks[i].first, 1, ms, 0});
+      }
+      for (auto& m : marks) cudaEventDestroy(m.second);
+      cudaEventDestroy(end);
+      marks.clear();
+    }
   }
 
   // ---- output in the flat layout (row bases, col bases by id, then blocks) ----
@@ -1376,7 +1446,9 @@ struct EngineRun {
     }
     DBuf flat(size_t(total) * W, s);
     for (const Job& j : jobs) cl.add(j.src, flat.p + j.dst * W, j.rows, j.cols, j.sld, j.dld);
-    cl.run(s, W, &launches);
+    int64_t dl = 0;
+    cl.run(s, W, &dl);
+    launches += dl;
     out.n_values = total;
     out.pool = ctx.pinned;
     out.values = out.pool->take(std::max<size_t>(1, size_t(total) * W * sizeof(double)), &out.values_bytes);

@@ -80,6 +80,7 @@ class Context {
   double run_resident(const std::shared_ptr<DevOperand>& a, const std::shared_ptr<DevOperand>& b,
                       double eps, int adaptive, HostResult* download_to);
   void* stream() const { return stream_; }
+  int device() const { return device_; }
   void* solver();  // cusolverDn handle bound to the stream (lazy)
   // side streams with their own cusolverDn handles: independent per-matrix
   // eigensolves of one level run concurrently instead of back to back
