@@ -465,8 +465,12 @@ struct EngineRun {
   // phase boundary on the main stream: in profiling mode an event pair per
   // phase measures its wall time on the device, gaps included
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  std::chrono::steady_clock::time_point host_t0 = std::chrono::steady_clock::now();
+  std::vector<std::pair<std::string, double>> host_marks;
   void mark(const std::string& name) {
     phase = name;
+    if (profiling)
+      host_marks.push_back({name, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count()});
     if (!profiling) return;
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
@@ -1359,6 +1363,9 @@ struct EngineRun {
         CK(cudaEventElapsedTime(&ms, marks[i].second, i + 1 < marks.size() ? marks[i + 1].second : end));
         out.push_back({"wall:" + marks[i].first, 1, ms, 0});
       }
+      for (size_t i = 0; i + 1 < host_marks.size(); ++i)
+        out.push_back({"host:" + host_marks[i].first, 1, host_marks[i + 1].second - host_marks[i].second, 0});
+      host_marks.clear();
       for (auto& m : marks) cudaEventDestroy(m.second);
       cudaEventDestroy(end);
       marks.clear();

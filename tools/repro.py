@@ -13,7 +13,9 @@ r = P.mmp(A, A, eps, ctx)
 print("ok", n, time.time() - t0, "flops", r.report.flops, "maxrank", r.report.max_rank(), "dev", r.report.device_seconds,
       "ranks", [(l.max_row_rank, l.max_col_rank) for l in r.report.levels], flush=True)
 r = P.mmp(A, A, eps, ctx)  # warm second run
-prof = [e for e in ctx.profile() if not e["name"].startswith("wall:")]
+prof = [e for e in ctx.profile() if not e["name"].startswith(("wall:", "host:"))]
+hosts = [e for e in ctx.profile() if e["name"].startswith("host:")]
+print("host phase times (ms):", [(e["name"][5:], round(e["ms"], 1)) for e in hosts])
 walls = [e for e in ctx.profile() if e["name"].startswith("wall:")]
 print("phase walls (ms):", [(e["name"][5:], round(e["ms"], 1)) for e in walls])
 print("second run dev", r.report.device_seconds, "profile sum ms", sum(e["ms"] for e in prof), "entries", len(prof))
