@@ -106,6 +106,12 @@ int h2c_mmp_resident(h2c_context* ctx, const h2c_operand* a, const h2c_operand* 
 int h2c_count_report(const h2c_matrix* a, const h2c_matrix* b, const h2c_matrix* c, int adaptive,
                      double eps_trunc, h2c_result** out);
 
+/* Structure-plan statistics per level (host logic): for level l the 10
+ * values out[10*l + 0..9] = clusters, admissible blocks, near blocks, pending
+ * pairs, non-leaf couplings, merged pairs, R x R triples, R/F x R triples,
+ * R x F triples, F x F coupling-target triples.  Returns depth+1 (levels). */
+int h2c_plan_stats(const h2c_tree* tree, const h2c_blocks* blocks, int64_t* out, int cap_levels);
+
 /* ---- pinned host memory for zero-copy-speed transfers ------------------- */
 void* h2c_host_alloc(size_t bytes);
 void h2c_host_free(void* p);

@@ -165,6 +165,18 @@ def build_fd_laplacian(tree: ClusterTree, structure: BlockTree, points: np.ndarr
 
 
 # ---------------------------------------------------------------------------
+def plan_stats(structure: BlockTree) -> list[dict]:
+    """Per-level sizes of the structure plan (blocks, targets, triples)."""
+    cap = structure.depth + 1
+    out = np.zeros(10 * cap, dtype=np.int64)
+    n = h2c.lib().h2c_plan_stats(C.byref(structure.tree.desc()), C.byref(structure.desc()),
+                                 out.ctypes.data_as(h2c.P_i64), cap)
+    if n < 0:
+        raise h2c.InvariantError(h2c.last_error())
+    keys = ["clusters", "admissible", "near", "pending", "nonleaf", "merged", "RxR", "FRxR", "RxF", "FxF"]
+    return [dict(level=l, **{k: int(out[10 * l + i]) for i, k in enumerate(keys)}) for l in range(n)]
+
+
 class _ResultOwner:
     """Keeps the library-owned result (pinned host values) alive while a view exists."""
 

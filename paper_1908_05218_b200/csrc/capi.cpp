@@ -303,3 +303,27 @@ int h2c_count_report(const h2c_matrix* a, const h2c_matrix* b, const h2c_matrix*
   if (rc == H2C_OK) *out = res.release();
   return rc;
 }
+
+int h2c_plan_stats(const h2c_tree* tree, const h2c_blocks* blocks, int64_t* out, int cap) {
+  try {
+    const Plan P = build_plan(*tree, *blocks, 8);
+    for (int l = 0; l <= P.depth && l < cap; ++l) {
+      const LevelPlan& L = P.lv[l];
+      int64_t* o = out + 10 * l;
+      o[0] = L.n;
+      o[1] = static_cast<int64_t>(L.adm.size());
+      o[2] = static_cast<int64_t>(L.nearb.size());
+      o[3] = static_cast<int64_t>(L.pend_row.size());
+      o[4] = static_cast<int64_t>(L.nl_block.size());
+      o[5] = static_cast<int64_t>(L.merged_row.size());
+      o[6] = L.lyr.entries();
+      o[7] = L.lyn.entries();
+      o[8] = L.xr.entries();
+      o[9] = L.ww.entries();
+    }
+    return P.depth + 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}

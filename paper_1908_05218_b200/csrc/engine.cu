@@ -230,7 +230,7 @@ static std::unique_ptr<DevPlan> upload_plan(const Plan& P, cudaStream_t s) {
     put(&Q.nl_col, nlc);
     if (l < P.depth) {
       const LevelPlan& C = P.lv[l + 1];
-      const int cna = static_cast<int>(C.adm.size()), cnp = static_cast<int>(C.pend_row.size());
+      const int cna = static_cast<int>(C.adm.size());
       for (int q = 0; q < 4; ++q) {
         std::vector<int32_t> src, prow, omap, fsrc, fprow, fnear, fcrow, fccol;
         for (size_t e = 0; e < L.split_src[q].size(); ++e) {
@@ -246,7 +246,8 @@ static std::unique_ptr<DevPlan> upload_plan(const Plan& P, cudaStream_t s) {
           } else {
             src.push_back(nl);
             prow.push_back(pr);
-            omap.push_back(C.bkind[cb] == kAdm ? C.kidx[cb] : cna + cnp + C.nl_of_block[cb]);
+            // compacted target store of level+1: [admissible | non-leaf] (pending dropped)
+            omap.push_back(C.bkind[cb] == kAdm ? C.kidx[cb] : cna + C.nl_of_block[cb]);
           }
         }
         Q.sp_n[q] = static_cast<int>(src.size());
@@ -1159,6 +1160,7 @@ struct EngineRun {
     // merged children couplings and assembled collected blocks (mmp.cpp:344-404)
     DBuf Mg, Aa, Ab;
     gather(Mg, nm, Tg[l + 1].p + size_t(Lc.adm.size()) * Kn * Kq * W, (long long)Kn * Kq, Kn, Kq, Q.merged_quad);
+    compact_targets(l + 1);
     gather(Aa, ns, LA[l + 1], (long long)Kn * KBr1, Kn, KBr1, Q.sub_child);
     gather(Ab, ns, RB[l + 1], (long long)KAc1 * Kq, KAc1, Kq, Q.sub_child);
     LA[l + 1].release();
@@ -1281,6 +1283,26 @@ struct EngineRun {
     targets(l, SB, nullptr, nullptr, &Z, Kq);
   }
 
+  // Drop the pending part of a level's target store once the parent level has
+  // gathered it (mmp.cpp:344-365): keeps [admissible couplings | non-leaf
+  // couplings] and frees the (largest) pending slots early.
+  std::vector<char> compacted;
+  void compact_targets(int l) {
+    if (compacted.empty()) compacted.assign(D + 1, 0);
+    if (compacted[l]) return;
+    compacted[l] = 1;
+    const LevelPlan& L = P.lv[l];
+    const size_t one = size_t(KCr[l]) * KCc[l] * W;
+    const size_t na = L.adm.size(), np = L.pend_row.size(), nl = L.nl_block.size();
+    if (np == 0) return;
+    DBuf T(one * (na + nl), s);
+    if (na) CK(cudaMemcpyAsync(T.p, Tg[l].p, na * one * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (nl)
+      CK(cudaMemcpyAsync(T.p + na * one, Tg[l].p + (na + np) * one, nl * one * sizeof(double), cudaMemcpyDeviceToDevice,
+                         s));
+    Tg[l] = std::move(T);
+  }
+
   // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------
   void split() {
     join();
@@ -1292,7 +1314,7 @@ struct EngineRun {
       const int nnl = static_cast<int>(L.nl_block.size());
       if (nnl == 0) continue;
       const int Kr = KCr[l], Kc = KCc[l], Kn = KCr[l + 1], Kq = KCc[l + 1];
-      const long long first = (long long)(L.adm.size() + L.pend_row.size()) * Kr * Kc;
+      const long long first = (long long)L.adm.size() * Kr * Kc;  // compacted store: [adm | NL]
       DBuf Qb(sz(nnl, Kr, 2 * Kq), s);  // NL * T^C_col^T
       segd(Qb, Kr, 2 * Kq, nnl,
            {Grp{ref(Tg[l], (long long)Kr * Kc, Kr, OP_N, first), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_T), Kc, nullptr,
@@ -1324,6 +1346,8 @@ struct EngineRun {
     basis_products();
     leaf_phase();
     for (int l = D - 1; l >= 1; --l) upper_level(l);
+    for (int l = std::max(1, D == 0 ? 0 : 1); l <= D; ++l) compact_targets(l);
+    if (D == 0) compact_targets(0);
     split();
     join();
   }

@@ -414,6 +414,8 @@ def lib() -> C.CDLL:
                                        C.POINTER(C.c_double), C.POINTER(C.c_void_p)]
         L.h2c_count_report.restype = C.c_int
         L.h2c_count_report.argtypes = [C.POINTER(h2c_matrix)] * 3 + [C.c_int, C.c_double, C.POINTER(C.c_void_p)]
+        L.h2c_plan_stats.restype = C.c_int
+        L.h2c_plan_stats.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_i64, C.c_int]
         L.h2c_host_alloc.restype = C.c_void_p
         L.h2c_host_alloc.argtypes = [C.c_size_t]
         L.h2c_host_free.argtypes = [C.c_void_p]
