@@ -63,11 +63,84 @@ struct ConfigErr : std::invalid_argument {
 static inline int pad8(int64_t r) { return static_cast<int>(std::max<int64_t>(8, (r + 7) / 8 * 8)); }
 
 // ---------------------------------------------------------------------------
-// stream-ordered device buffers
+// Device memory.  Large buffers of the main stream come from a per-context
+// arena (one cudaMalloc, best-fit free list with coalescing, host-side
+// immediate free: every user of such a buffer is ordered on the main stream,
+// or joined to it before the free).  This avoids the pool growth / physical
+// re-mapping that fragmented cudaMallocAsync pools pay for multi-GB,
+// differently-sized per-level buffers on every product.  Everything else is
+// stream-ordered cudaMallocAsync.
+class Arena {
+ public:
+  bool init(size_t bytes) {
+    if (cudaMalloc(&base_, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      base_ = nullptr;
+      return false;
+    }
+    cap_ = bytes;
+    free_.clear();
+    free_[0] = bytes;
+    return true;
+  }
+  ~Arena() {
+    if (base_) cudaFree(base_);
+  }
+  void* alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    std::lock_guard<std::mutex> g(mu_);
+    auto best = free_.end();
+    for (auto it = free_.begin(); it != free_.end(); ++it)
+      if (it->second >= bytes && (best == free_.end() || it->second < best->second)) best = it;
+    if (best == free_.end()) return nullptr;
+    const size_t off = best->first, sz = best->second;
+    free_.erase(best);
+    if (sz > bytes) free_[off + bytes] = sz - bytes;
+    used_[off] = bytes;
+    return static_cast<char*>(base_) + off;
+  }
+  bool owns(const void* p) const {
+    return base_ && p >= base_ && p < static_cast<const char*>(base_) + cap_;
+  }
+  void free(void* p) {
+    std::lock_guard<std::mutex> g(mu_);
+    size_t off = static_cast<char*>(p) - static_cast<char*>(base_);
+    auto u = used_.find(off);
+    if (u == used_.end()) return;
+    size_t sz = u->second;
+    used_.erase(u);
+    auto next = free_.lower_bound(off);
+    if (next != free_.end() && next->first == off + sz) {  // merge right
+      sz += next->second;
+      next = free_.erase(next);
+    }
+    if (next != free_.begin()) {  // merge left
+      auto prev = std::prev(next);
+      if (prev->first + prev->second == off) {
+        prev->second += sz;
+        return;
+      }
+    }
+    free_[off] = sz;
+  }
+
+ private:
+  void* base_ = nullptr;
+  size_t cap_ = 0;
+  std::map<size_t, size_t> free_, used_;
+  std::mutex mu_;
+};
+
+// the arena of the context running on this thread, and its main stream
+thread_local Arena* t_arena = nullptr;
+thread_local cudaStream_t t_arena_stream = nullptr;
+constexpr size_t kArenaMin = size_t(8) << 20;
+
 struct DBuf {
   double* p = nullptr;
   size_t n = 0;  // doubles
   cudaStream_t s = nullptr;
+  Arena* arena = nullptr;
   DBuf() = default;
   DBuf(size_t doubles, cudaStream_t st, bool zero = false) { alloc(doubles, st, zero); }
   DBuf(const DBuf&) = delete;
@@ -79,8 +152,10 @@ struct DBuf {
       p = o.p;
       n = o.n;
       s = o.s;
+      arena = o.arena;
       o.p = nullptr;
       o.n = 0;
+      o.arena = nullptr;
     }
     return *this;
   }
@@ -88,13 +163,21 @@ struct DBuf {
     release();
     s = st;
     n = std::max<size_t>(doubles, 2);
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(double), s));
+    if (t_arena && st == t_arena_stream && n * sizeof(double) >= kArenaMin) {
+      p = static_cast<double*>(t_arena->alloc(n * sizeof(double)));
+      if (p) arena = t_arena;
+    }
+    if (!p) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(double), s));
     if (zero) CK(cudaMemsetAsync(p, 0, n * sizeof(double), s));
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      if (arena) arena->free(p);
+      else cudaFreeAsync(p, s);
+    }
     p = nullptr;
     n = 0;
+    arena = nullptr;
   }
   ~DBuf() { release(); }
   operator double*() const { return p; }
@@ -1588,6 +1671,8 @@ void* Context::side_solver(int i) {
 }
 
 Context::~Context() {
+  if (stream_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
+  delete static_cast<Arena*>(arena_);
   for (void* h : side_solvers_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(h));
   for (void* st : side_streams_) cudaStreamDestroy(static_cast<cudaStream_t>(st));
   if (solver_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_));
@@ -1658,8 +1743,38 @@ static void fill_report(const Plan& P, const DevOperand& A, const DevOperand& B,
   }
 }
 
+// binds the context's arena to this thread for the duration of a call
+struct ArenaScope {
+  Arena* prev_a;
+  cudaStream_t prev_s;
+  ArenaScope(Arena* a, cudaStream_t s) : prev_a(t_arena), prev_s(t_arena_stream) {
+    t_arena = a;
+    t_arena_stream = s;
+  }
+  ~ArenaScope() {
+    t_arena = prev_a;
+    t_arena_stream = prev_s;
+  }
+};
+
+Arena* Context::arena() {
+  if (!arena_tried_) {
+    arena_tried_ = true;
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t reserve = size_t(28) << 30;  // pool (aux stream, solver) + operands headroom
+    if (fr > reserve + (size_t(4) << 30)) {
+      auto* a = new Arena;
+      if (a->init(fr - reserve)) arena_ = a;
+      else delete a;
+    }
+  }
+  return static_cast<Arena*>(arena_);
+}
+
 double Context::run_resident(const std::shared_ptr<DevOperand>& a, const std::shared_ptr<DevOperand>& b,
                              double eps, int adaptive, HostResult* out) {
+  ArenaScope scope(arena(), static_cast<cudaStream_t>(stream_));
   if (!plan_ || a->key != plan_key_ || b->key != plan_key_)
     throw ConfigErr("mmp: operands were uploaded for another structure");
   if (a->scalar != b->scalar) throw ConfigErr("mmp: operands must share the scalar type");
@@ -1693,6 +1808,7 @@ double Context::run_resident(const std::shared_ptr<DevOperand>& a, const std::sh
 
 void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adaptive, HostResult& out) {
   const auto t0 = std::chrono::steady_clock::now();
+  ArenaScope scope(arena(), static_cast<cudaStream_t>(stream_));
   if (a.tree != b.tree || a.blocks != b.blocks)  // mmp.cpp:58-63
     throw ConfigErr("mmp: operands must share cluster trees and block structure");
   if (a.scalar != b.scalar) throw ConfigErr("mmp: operands must share the scalar type");

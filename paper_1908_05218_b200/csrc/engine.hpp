@@ -82,6 +82,7 @@ class Context {
   void* stream() const { return stream_; }
   int device() const { return device_; }
   void* solver();  // cusolverDn handle bound to the stream (lazy)
+  struct Arena* arena();  // large-buffer arena of the main stream (lazy)
   // side streams with their own cusolverDn handles: independent per-matrix
   // eigensolves of one level run concurrently instead of back to back
   static constexpr int kSideStreams = 16;
@@ -98,6 +99,8 @@ class Context {
   int device_;
   void* stream_ = nullptr;
   void* solver_ = nullptr;
+  void* arena_ = nullptr;
+  bool arena_tried_ = false;
   std::vector<void*> side_streams_, side_solvers_;
   std::string err_;
   uint64_t plan_key_ = 0;

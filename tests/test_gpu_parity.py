@@ -295,3 +295,58 @@ def test_cfg2_full_size_properties(ctx):
         x = O.random_vector(65536, seed)
         ref = O.mvp(A, O.mvp(A, x))
         assert np.linalg.norm(O.mvp(C, x) - ref) / np.linalg.norm(ref) <= 1e-4
+
+
+# ---- the other BASELINE configurations at oracle-checkable sizes ------------------
+def test_cfg4_like_fd_times_laplace(ctx):
+    """configs[3] shape at 16^3: FD Laplacian (rank-1 degenerate far field) x Laplace H^2 (order 4)."""
+    m = 16
+    h = 1.0 / (m + 1)
+    g = np.stack(np.meshgrid(*[np.arange(1, m + 1) * h] * 3, indexing="ij"), -1).reshape(-1, 3)
+    t = P.build_cluster_tree(g, 64)
+    s = P.build_block_tree(t, t, 1.0)
+    A = P.build_fd_laplacian(t, s, g, h)
+    B = P.build_chebyshev(t, s, g, 4)
+    got, ref, cg, co = check_against_oracle(A, B, 1e-6, ctx)
+    dense = O.h2_to_dense(A) @ O.h2_to_dense(B)
+    assert rel(cg, dense) <= 1.1 * rel(co, dense) + 1e-13
+
+
+def test_cfg3_like_plates_times_jittered(ctx):
+    """configs[2] shape, small: parallel plates with centroid panels, A x B with B on jittered
+    centroids built over A's tree/structure (self term 2 ln(1+sqrt2)/(pi h))."""
+    nplates, m = 4, 24
+    hh = 1.0 / m
+    pts = []
+    for p_ in range(nplates):
+        for i in range(m):
+            for j in range(m):
+                pts.append(((i + 0.5) * hh, (j + 0.5) * hh, 0.1 * p_))
+    pts = np.array(pts)
+    t = P.build_cluster_tree(pts, 32)
+    s = P.build_block_tree(t, t, 1.0)
+    diag = 2.0 * np.log(1.0 + np.sqrt(2.0)) / (np.pi * hh)
+    A = P.build_chebyshev(t, s, pts, 3, diagonal=diag)
+    rng = np.random.default_rng(2)
+    jit = pts + 0.05 * hh * rng.uniform(-1, 1, pts.shape)
+    B = P.build_chebyshev(t, s, jit, 3, diagonal=diag)
+    got, ref, cg, co = check_against_oracle(A, B, 1e-6, ctx)
+    dense = O.h2_to_dense(A) @ O.h2_to_dense(B)
+    assert rel(cg, dense) <= 1.1 * rel(co, dense) + 1e-13
+
+
+def test_cfg5_like_helmholtz_chebyshev(ctx):
+    """configs[4] shape, small: complex128 Helmholtz exp(-i k r)/(4 pi r) on a Fibonacci sphere."""
+    n = 2048
+    i = np.arange(n) + 0.5
+    phi = np.arccos(1 - 2 * i / n)
+    theta = np.pi * (1 + 5 ** 0.5) * i
+    sph = 2.0 * np.stack([np.cos(theta) * np.sin(phi), np.sin(theta) * np.sin(phi), np.cos(phi)], 1)
+    t = P.build_cluster_tree(sph, 64)
+    s = P.build_block_tree(t, t, 1.0)
+    A = P.build_chebyshev(t, s, sph, 4, kernel="helmholtz", kappa=2 * np.pi)
+    assert A.scalar == P.H2C_COMPLEX
+    got, ref, cg, co = check_against_oracle(A, A, 1e-4, ctx)
+    da = O.h2_to_dense(A)
+    dense = da @ da
+    assert rel(cg, dense) <= 1.1 * rel(co, dense) + 1e-13
