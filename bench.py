@@ -175,6 +175,21 @@ def run_reference(args) -> None:
 
 
 # ---------------------------------------------------------------------------
+def max_over_ranks(x: float, dist, device: str) -> float:
+    """Max of a per-rank scalar (times are taken as the slowest rank)."""
+    if dist is None:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(flops_per_rank: float, world: int, seconds: float) -> float:
+    """Whole-job GFLOP/s: every rank runs one product (replicas, weak scaling)."""
+    return world * flops_per_rank / seconds / 1e9
+
+
 def run_b200(args) -> None:
     import torch
     import paper_1908_05218_b200 as P
@@ -216,20 +231,16 @@ def run_b200(args) -> None:
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, "cuda")
     flops = 2.0 * rep.flops
-    value = world * flops / (ms * 1e-3) / 1e9
+    value = job_throughput(flops, world, ms * 1e-3)
 
     # roofline of the dominant kernel: one profiled (untimed) product
     ctx.set_profile(True)
     P.mmp_resident(dA, dA, eps)
     prof_all = ctx.profile()
     ctx.set_profile(False)
-    prof = [e for e in prof_all if not e["name"].startswith("wall:")]
+    prof = [e for e in prof_all if not e["name"].startswith(("wall:", "host:"))]
     walls = [e for e in prof_all if e["name"].startswith("wall:")]
     peak, peak_src = fp64_peak_tflops()
     dom = max(prof, key=lambda e: e["ms"]) if prof else None
@@ -257,12 +268,8 @@ def run_b200(args) -> None:
         e2e_times.append(time.perf_counter() - t0)
         h2d, d2h = res.report.h2d_bytes, res.report.d2h_bytes
         del res
-    e2e_s = sum(e2e_times) / len(e2e_times)
-    if dist:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * flops / e2e_s / 1e9
+    e2e_s = max_over_ranks(sum(e2e_times) / len(e2e_times), dist, "cuda")
+    e2e_value = job_throughput(flops, world, e2e_s)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
