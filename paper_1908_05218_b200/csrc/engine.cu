@@ -627,27 +627,38 @@ struct EngineRun {
 
   // ---- launchers -----------------------------------------------------------
   const bool seg_v1 = std::getenv("H2B_SEG_V1") != nullptr;
+  // pipeline shape of seg_gemm v2 (k-chunk x stages); H2B_SEG_CFG=16x3 (default), 32x2, 16x4, 8x4
+  const int seg_cfg = [] {
+    const char* e = std::getenv("H2B_SEG_CFG");
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "32x2" ? 1 : v == "16x4" ? 2 : v == "8x4" ? 3 : 0;
+  }();
+  template <int TM, int TN, bool CX, int KC, int ST>
+  void launch_v2_cfg(const SegParams& sp, dim3 grid) {
+    constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST>::SMEM;
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(seg_gemm2_kernel<TM, TN, CX, KC, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      attr = true;
+    }
+    seg_gemm2_kernel<TM, TN, CX, KC, ST><<<grid, 128, sm, s>>>(sp);
+  }
+  template <int TM, int TN, bool CX>
+  void launch_v2(const SegParams& sp, dim3 grid) {
+    switch (seg_cfg) {
+      case 1: launch_v2_cfg<TM, TN, CX, 32, 2>(sp, grid); break;
+      case 2: launch_v2_cfg<TM, TN, CX, 16, 4>(sp, grid); break;
+      case 3: launch_v2_cfg<TM, TN, CX, 8, 4>(sp, grid); break;
+      default: launch_v2_cfg<TM, TN, CX, 16, 3>(sp, grid); break;
+    }
+  }
   template <int TM, int TN>
   void launch_seg(const SegParams& sp, int tiles) {
     dim3 grid(sp.n_out, tiles);
     if (!seg_v1) {
-      if (cplx) {
-        constexpr int sm = Seg2Cfg<TM, TN, true>::SMEM;
-        static bool attr = false;
-        if (!attr) {
-          CK(cudaFuncSetAttribute(seg_gemm2_kernel<TM, TN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-          attr = true;
-        }
-        seg_gemm2_kernel<TM, TN, true><<<grid, 128, sm, s>>>(sp);
-      } else {
-        constexpr int sm = Seg2Cfg<TM, TN, false>::SMEM;
-        static bool attr = false;
-        if (!attr) {
-          CK(cudaFuncSetAttribute(seg_gemm2_kernel<TM, TN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-          attr = true;
-        }
-        seg_gemm2_kernel<TM, TN, false><<<grid, 128, sm, s>>>(sp);
-      }
+      if (cplx) launch_v2<TM, TN, true>(sp, grid);
+      else launch_v2<TM, TN, false>(sp, grid);
       CK(cudaGetLastError());
       launches++;
       return;

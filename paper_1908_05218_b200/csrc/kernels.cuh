@@ -335,11 +335,11 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(const SegParams p) {
 // the layout (both conflict-free with a +4 double pad).  No register staging:
 // fewer registers, more CTAs per SM, and STAGES-1 chunks in flight hide the
 // L2/HBM latency of the next entry's operands.
-template <int TM, int TN, bool CPLX>
+template <int TM, int TN, bool CPLX, int KC_ = 16, int ST_ = 3>
 struct Seg2Cfg {
   static constexpr int W = CPLX ? 2 : 1;
-  static constexpr int KC = CPLX ? 8 : 16;
-  static constexpr int STAGES = 3;
+  static constexpr int KC = CPLX ? KC_ / 2 : KC_;
+  static constexpr int STAGES = ST_;
   static constexpr int LKM = KC * (TM + 4), LMK = TM * (KC + 4);
   static constexpr int RKN = KC * (TN + 4), RNK = TN * (KC + 4);
   static constexpr int LSZ = (LKM > LMK ? LKM : LMK) * W;
@@ -360,9 +360,9 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int TM, int TN, bool CPLX>
+template <int TM, int TN, bool CPLX, int KC_ = 16, int ST_ = 3>
 __global__ void __launch_bounds__(128) seg_gemm2_kernel(const SegParams p) {
-  using C = Seg2Cfg<TM, TN, CPLX>;
+  using C = Seg2Cfg<TM, TN, CPLX, KC_, ST_>;
   constexpr int KC = C::KC, W = C::W, ST = C::STAGES;
   extern __shared__ __align__(16) double smem[];
 
