@@ -627,12 +627,12 @@ struct EngineRun {
 
   // ---- launchers -----------------------------------------------------------
   const bool seg_v1 = std::getenv("H2B_SEG_V1") != nullptr;
-  // pipeline shape of seg_gemm v2 (k-chunk x stages); H2B_SEG_CFG=16x3 (default), 32x2, 16x4, 8x4
+  // pipeline shape of seg_gemm v2 (k-chunk x stages); H2B_SEG_CFG=8x4 (default), 16x3, 32x2, 16x4
   const int seg_cfg = [] {
     const char* e = std::getenv("H2B_SEG_CFG");
-    if (!e) return 0;
+    if (!e) return 3;  // 8x4: measured best on cfg2 (profiles/r01/seg_cfg_ab.txt)
     const std::string v(e);
-    return v == "32x2" ? 1 : v == "16x4" ? 2 : v == "8x4" ? 3 : 0;
+    return v == "32x2" ? 1 : v == "16x4" ? 2 : v == "16x3" ? 0 : 3;
   }();
   template <int TM, int TN, bool CX, int KC, int ST>
   void launch_v2_cfg(const SegParams& sp, dim3 grid) {
