@@ -98,6 +98,16 @@ void h2c_operand_free(h2c_operand* op);
 int h2c_mmp_resident(h2c_context* ctx, const h2c_operand* a, const h2c_operand* b,
                      double eps_trunc, int adaptive, double* device_seconds, h2c_result** out);
 
+/* ---- exact H^2 matrix-vector product on the device (h2_matrix.cpp:213-278) ----
+ * Y = A X for nv vectors; X, Y column-major N x nv in the ORIGINAL point
+ * ordering (complex interleaved).  Used for the paper's eps_rel metric
+ * (metrics.cpp:37-55) at sizes where a dense check is impossible. */
+int h2c_mvp(h2c_context* ctx, const h2c_matrix* a, const double* x, int nv, double* y);
+int h2c_mvp_resident(h2c_context* ctx, const h2c_operand* a, const double* x, int nv, double* y);
+/* random_vector (metrics.cpp:11-35): U[-1,1] from std::mt19937_64(seed), 53-bit
+ * mantissas; complex draws re then im. */
+int h2c_random_vector(int n, uint64_t seed, int scalar, double* out);
+
 /* ---- host-side accounting (no device needed) ----------------------------
  * The reference's MmpReport counters (mmp.cpp:67-80 and LevelStats) for the
  * product C = A*B, computed from the structure plan and the ranks of A, B

@@ -165,6 +165,37 @@ def build_fd_laplacian(tree: ClusterTree, structure: BlockTree, points: np.ndarr
 
 
 # ---------------------------------------------------------------------------
+def random_vector(n: int, seed: int, complex_: bool = False) -> np.ndarray:
+    """random_vector (metrics.cpp:11-35)."""
+    out = np.zeros(n, dtype=np.complex128 if complex_ else np.float64)
+    raise_for(h2c.lib().h2c_random_vector(int(n), int(seed), int(complex_), out.ctypes.data_as(h2c.P_f64)),
+              h2c.last_error())
+    return out
+
+
+def mvp(a: H2Matrix, x: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
+    """Exact H^2 MVP on the B200 (h2_matrix.cpp:213-278); x is [N] or [N, nv]."""
+    ctx = ctx or default_context()
+    xx = np.asfortranarray(x, dtype=a.dtype)
+    nv = 1 if xx.ndim == 1 else xx.shape[1]
+    y = np.zeros_like(xx, order="F")
+    rc = h2c.lib().h2c_mvp(ctx.handle, C.byref(a.desc()), xx.ctypes.data_as(h2c.P_f64), nv,
+                           y.ctypes.data_as(h2c.P_f64))
+    raise_for(rc, h2c.last_error(ctx.handle))
+    return y
+
+
+def relative_error(a: H2Matrix, b: H2Matrix, c: H2Matrix, seed: int, ctx: Optional[Context] = None) -> float:
+    """||C x - A (B x)|| / ||A (B x)|| with x = random_vector(seed) (metrics.cpp:37-55), on the B200."""
+    if not (a.tree is b.tree is c.tree):
+        raise ConfigError("relative_error: operands must share the cluster tree")
+    x = random_vector(a.size(), seed, a.scalar == h2c.H2C_COMPLEX)
+    ref = mvp(a, mvp(b, x, ctx), ctx)
+    cx = mvp(c, x, ctx)
+    rn = np.linalg.norm(ref)
+    return float(np.linalg.norm(cx)) if rn == 0 else float(np.linalg.norm(cx - ref) / rn)
+
+
 def plan_stats(structure: BlockTree) -> list[dict]:
     """Per-level sizes of the structure plan (blocks, targets, triples)."""
     cap = structure.depth + 1

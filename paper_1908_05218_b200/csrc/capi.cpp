@@ -327,3 +327,27 @@ int h2c_plan_stats(const h2c_tree* tree, const h2c_blocks* blocks, int64_t* out,
     return -1;
   }
 }
+
+int h2c_mvp_resident(h2c_context* ctx, const h2c_operand* a, const double* x, int nv, double* y) {
+  if (!ctx) return H2C_ERR_CUDA;
+  return guarded(ctx, [&] { ctx->ctx->mvp(a->op, x, nv, y); });
+}
+
+int h2c_mvp(h2c_context* ctx, const h2c_matrix* a, const double* x, int nv, double* y) {
+  if (!ctx) return H2C_ERR_CUDA;
+  return guarded(ctx, [&] {
+    auto op = ctx->ctx->upload(*a);
+    ctx->ctx->mvp(op, x, nv, y);
+  });
+}
+
+int h2c_random_vector(int n, uint64_t seed, int scalar, double* out) {
+  if (n < 0) {
+    g_err = "random_vector: negative length";
+    return H2C_ERR_CONFIG;
+  }
+  std::mt19937_64 eng(seed);
+  auto u = [&eng] { return 2.0 * (static_cast<double>(eng() >> 11) * 0x1.0p-53) - 1.0; };
+  for (int64_t i = 0; i < int64_t(n) * (scalar == H2C_COMPLEX ? 2 : 1); ++i) out[i] = u();
+  return H2C_OK;
+}

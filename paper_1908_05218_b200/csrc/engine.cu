@@ -235,6 +235,8 @@ struct DevCsr {
 struct DevLevel {
   DevCsr lyr, lyn, xr, ww, ff, fr, rf, rr, mg, hq, hqc, row_near, col_near, row_merged, col_merged;
   const int *target_row = nullptr, *target_col = nullptr;
+  DevCsr adm_by_row;   // per row position: (adm idx, col position)   (MVP coupling products)
+  DevCsr near_by_row;  // per row position: (near idx, col position)  (MVP near field)
   const int *near_row = nullptr, *near_col = nullptr, *adm_row = nullptr, *adm_col = nullptr;
   const int *nearb = nullptr, *adm = nullptr, *merged_row = nullptr, *merged_quad = nullptr;
   const int *sub_child = nullptr, *nl_col = nullptr;
@@ -311,6 +313,26 @@ static std::unique_ptr<DevPlan> upload_plan(const Plan& P, cudaStream_t s) {
     put(&Q.merged_quad, L.merged_quad);
     put(&Q.sub_child, L.sub_child);
     put(&Q.nl_col, nlc);
+    {
+      Csr ar, nr;
+      ar.ptr.assign(L.n + 1, 0);
+      nr.ptr.assign(L.n + 1, 0);
+      for (int p = 0; p < L.n; ++p) {
+        for (int b = L.row_ptr[p]; b < L.row_ptr[p + 1]; ++b) {
+          if (L.bkind[b] == kAdm) {
+            ar.li.push_back(L.kidx[b]);
+            ar.ri.push_back(L.bcol[b]);
+          } else if (L.bkind[b] == kFull) {
+            nr.li.push_back(L.kidx[b]);
+            nr.ri.push_back(L.bcol[b]);
+          }
+        }
+        ar.ptr[p + 1] = static_cast<int32_t>(ar.li.size());
+        nr.ptr[p + 1] = static_cast<int32_t>(nr.li.size());
+      }
+      put_csr(Q.adm_by_row, ar);
+      put_csr(Q.near_by_row, nr);
+    }
     if (l < P.depth) {
       const LevelPlan& C = P.lv[l + 1];
       const int cna = static_cast<int>(C.adm.size());
@@ -1446,6 +1468,76 @@ struct EngineRun {
     join();
   }
 
+  // ---- exact H^2 matrix-vector product Y = A X (h2_matrix.cpp:213-278) -----
+  // X, Y: device [N x nv] column-major in the ORIGINAL ordering.  Forward
+  // transform up the column tree, coupling products, backward transform down
+  // the row tree, near field - each level one segmented batched launch.
+  void mvp(const double* X, int nv, double* Y, const int* perm) {
+    const LevelPlan& LL = P.lv[D];
+    const int nL = LL.n;
+    const int NV = pad8(nv);
+    const int N = P.n_points;
+    // leaf-blocked copies of x (tree order, padded NL x NV per leaf)
+    DBuf XL(sz(nL, NL, NV), s, true), YL(sz(nL, NL, NV), s, true);
+    DVec<int32_t> beg, sizes;
+    {
+      std::vector<int32_t> b(nL), z(nL);
+      int at = 0;
+      for (int p = 0; p < nL; ++p) {
+        b[p] = at;
+        z[p] = LL.size[p];
+        at += LL.size[p];
+      }
+      beg.upload(b, s);
+      sizes.upload(z, s);
+    }
+    mvp_gather_kernel<<<nL, 256, 0, s>>>(X, N, nv, perm, beg.p, sizes.p, XL, NL, NV, W);
+    CK(cudaGetLastError());
+    launches++;
+    // forward: xhat_L = V_col^T x ; xhat_l = sum_s T_col[s]^T xhat_{l+1}[child s]
+    std::vector<DBuf> xh(D + 1), yh(D + 1);
+    xh[D].alloc(sz(nL, A.Kc[D], NV), s);
+    segd(xh[D], A.Kc[D], NV, nL,
+         {Grp{ref(A.Vc, (long long)NL * A.Kc[D], NL, OP_T), ref(XL, (long long)NL * NV, NL, OP_N), NL, nullptr,
+              nullptr, nullptr}});
+    for (int l = D - 1; l >= 1; --l) {
+      const int n = P.lv[l].n, K = A.Kc[l], K1 = A.Kc[l + 1];
+      xh[l].alloc(sz(n, K, NV), s);
+      segd(xh[l], K, NV, n,
+           {Grp{ref(A.Tc[l], 2LL * K1 * K, 2 * K1, OP_T), ref(xh[l + 1], (long long)K1 * NV, K1, OP_N), K1, nullptr,
+                nullptr, DP.even},
+            Grp{ref(A.Tc[l], 2LL * K1 * K, 2 * K1, OP_T, K1), ref(xh[l + 1], (long long)K1 * NV, K1, OP_N), K1,
+                nullptr, nullptr, DP.odd}});
+    }
+    // couplings: yhat_l[i] = sum_{(i,j) adm} S_ij xhat_l[j]
+    const int l0 = D == 0 ? 0 : 1;
+    for (int l = l0; l <= D; ++l) {
+      const int n = P.lv[l].n, Kr = A.Kr[l], Kc = A.Kc[l];
+      yh[l].alloc(sz(n, Kr, NV), s);
+      if (!xh[l].p) xh[l].alloc(sz(n, Kc, NV), s, true);
+      segd(yh[l], Kr, NV, n,
+           {Grp{ref(A.S[l], (long long)Kr * Kc, Kr, OP_N), ref(xh[l], (long long)Kc * NV, Kc, OP_N), Kc,
+                &DP.lv[l].adm_by_row, nullptr, nullptr}});
+    }
+    // backward: yhat_{l+1}[child s] += T_row[s] yhat_l
+    for (int l = l0; l < D; ++l) {
+      const int n = P.lv[l].n, K = A.Kr[l], K1 = A.Kr[l + 1];
+      for (int c = 0; c < 2; ++c)
+        seg(yh[l + 1], (long long)K1 * NV, 0, K1, c ? DP.odd : DP.even, K1, NV, n, true,
+            {Grp{ref(A.Tr[l], 2LL * K1 * K, 2 * K1, OP_N, (long long)c * K1), ref(yh[l], (long long)K * NV, K, OP_N),
+                 K, nullptr, nullptr, nullptr}});
+    }
+    // leaves: y = V_row yhat + sum_full F x
+    segd(YL, NL, NV, nL,
+         {Grp{ref(A.Vr, (long long)NL * A.Kr[D], NL, OP_N), ref(yh[D], (long long)A.Kr[D] * NV, A.Kr[D], OP_N), A.Kr[D],
+              nullptr, nullptr, nullptr},
+          Grp{ref(A.F, (long long)NL * NL, NL, OP_N), ref(XL, (long long)NL * NV, NL, OP_N), NL,
+              &DP.lv[D].near_by_row, nullptr, nullptr}});
+    mvp_scatter_kernel<<<nL, 256, 0, s>>>(YL, NL, NV, perm, beg.p, sizes.p, Y, N, nv, W);
+    CK(cudaGetLastError());
+    launches++;
+  }
+
   // per (phase, kernel) totals of the profiled launches
   void collect_profile(std::vector<ProfileEntry>& out) {
     out.clear();
@@ -1703,6 +1795,7 @@ const Plan& Context::plan_for(const h2c_tree& t, const h2c_blocks& b, double* bu
   CK(cudaSetDevice(device_));
   dplan_.reset();
   plan_ = std::make_unique<Plan>(build_plan(t, b, std::max(1u, std::thread::hardware_concurrency())));
+  perm_.assign(t.perm, t.perm + t.n_points);
   dplan_ = upload_plan(*plan_, static_cast<cudaStream_t>(stream_));
   plan_key_ = key;
   if (build_seconds) *build_seconds = plan_->build_seconds;
@@ -1815,6 +1908,25 @@ double Context::run_resident(const std::shared_ptr<DevOperand>& a, const std::sh
     out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   return ms * 1e-3;
+}
+
+void Context::mvp(const std::shared_ptr<DevOperand>& a, const double* x_host, int nv, double* y_host) {
+  if (!plan_ || a->key != plan_key_) throw ConfigErr("mvp: operand was uploaded for another structure");
+  if (nv < 1) throw ConfigErr("mvp: need at least one vector");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  CK(cudaSetDevice(device_));
+  ArenaScope scope(arena(), s);
+  const int W = a->scalar == H2C_COMPLEX ? 2 : 1;
+  const size_t bytes = size_t(plan_->n_points) * nv * W * sizeof(double);
+  DBuf X(bytes / 8, s), Y(bytes / 8, s);
+  CK(cudaMemcpyAsync(X.p, x_host, bytes, cudaMemcpyHostToDevice, s));
+  DVec<int32_t> perm;
+  perm.upload(perm_, s);
+  EngineRun R(*this, *plan_, *dplan_, *a, *a, 0.5, true, s);
+  R.mvp(X.p, nv, Y.p, perm.p);
+  CK(cudaMemcpyAsync(y_host, Y.p, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  launches_ = R.launches;
 }
 
 void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adaptive, HostResult& out) {

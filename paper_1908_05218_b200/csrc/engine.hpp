@@ -79,6 +79,8 @@ class Context {
   // runs the pipeline on resident operands; returns device seconds (CUDA events)
   double run_resident(const std::shared_ptr<DevOperand>& a, const std::shared_ptr<DevOperand>& b,
                       double eps, int adaptive, HostResult* download_to);
+  // exact H^2 MVP Y = A X on a resident operand (host X, Y: N x nv, original ordering)
+  void mvp(const std::shared_ptr<DevOperand>& a, const double* x, int nv, double* y);
   void* stream() const { return stream_; }
   int device() const { return device_; }
   void* solver();  // cusolverDn handle bound to the stream (lazy)
@@ -105,6 +107,7 @@ class Context {
   std::string err_;
   uint64_t plan_key_ = 0;
   std::unique_ptr<Plan> plan_;
+  std::vector<int32_t> perm_;
   std::unique_ptr<DevPlan> dplan_;
   int64_t launches_ = 0;
 };

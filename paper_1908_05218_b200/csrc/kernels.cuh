@@ -960,6 +960,28 @@ __global__ void copy_jobs_kernel(const CopyJob* jobs, int W) {
   }
 }
 
+// MVP: original-order vectors <-> leaf blocks in tree order (padded)
+__global__ void mvp_gather_kernel(const double* X, int N, int nv, const int* perm, const int* beg, const int* size,
+                                  double* XL, int NL, int NV, int W) {
+  const int p = blockIdx.x;
+  double* o = XL + (size_t)p * NL * NV * W;
+  for (int x = threadIdx.x; x < size[p] * nv * W; x += blockDim.x) {
+    const int e = x / W, w = x % W;
+    const int r = e % size[p], v = e / size[p];
+    o[(r + (size_t)v * NL) * W + w] = X[(perm[beg[p] + r] + (size_t)v * N) * W + w];
+  }
+}
+__global__ void mvp_scatter_kernel(const double* YL, int NL, int NV, const int* perm, const int* beg, const int* size,
+                                   double* Y, int N, int nv, int W) {
+  const int p = blockIdx.x;
+  const double* i_ = YL + (size_t)p * NL * NV * W;
+  for (int x = threadIdx.x; x < size[p] * nv * W; x += blockDim.x) {
+    const int e = x / W, w = x % W;
+    const int r = e % size[p], v = e / size[p];
+    Y[(perm[beg[p] + r] + (size_t)v * N) * W + w] = i_[(r + (size_t)v * NL) * W + w];
+  }
+}
+
 // identity matrices (formatted product: P = I, mmp.cpp:280-283)
 __global__ void set_identity_kernel(double* out, int n, int ld, const int* rank, int W) {
   const int b = blockIdx.x;

@@ -350,3 +350,28 @@ def test_cfg5_like_helmholtz_chebyshev(ctx):
     da = O.h2_to_dense(A)
     dense = da @ da
     assert rel(cg, dense) <= 1.1 * rel(co, dense) + 1e-13
+
+
+# ---- exact H^2 MVP on the device (h2_matrix.cpp:213-278) and eps_rel (metrics.cpp:37-55)
+@pytest.mark.parametrize("kind", ["real", "complex"])
+def test_mvp_matches_oracle(ctx, kind):
+    if kind == "real":
+        A = laplace(1024, 5, 16, 1.2)
+    else:
+        _, _, A = helmholtz(3, 20, 1.5)
+    n = A.size()
+    X = np.stack([P.random_vector(n, s_, kind == "complex") for s_ in range(3)], 1)
+    Y = P.mvp(A, X, ctx)
+    for j in range(3):
+        ref = O.mvp(A, X[:, j])
+        assert np.linalg.norm(Y[:, j] - ref) <= 1e-13 * np.linalg.norm(ref)
+    y1 = P.mvp(A, X[:, 0], ctx)
+    assert np.linalg.norm(y1 - O.mvp(A, X[:, 0])) <= 1e-13 * np.linalg.norm(y1)
+
+
+def test_relative_error_matches_oracle(ctx):
+    A = chebyshev(4096, 32, 3)
+    C = P.mmp(A, A, 1e-6, ctx).product
+    e_gpu = P.relative_error(A, A, C, 99, ctx)
+    e_ora = O.relative_error(A, A, C, 99)
+    assert abs(e_gpu - e_ora) <= 1e-9 * max(e_ora, 1e-30) + 1e-15

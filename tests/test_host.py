@@ -152,3 +152,8 @@ def test_config_errors():
     t = P.build_cluster_tree(pts, 8)
     with pytest.raises(P.ConfigError):
         P.build_block_tree(t, t, 0.0)
+
+
+def test_random_vector_matches_reference_stream():
+    for seed, cplx in ((5, False), (99, False), (3, True)):
+        assert np.array_equal(P.random_vector(257, seed, cplx), O.random_vector(257, seed, cplx))
