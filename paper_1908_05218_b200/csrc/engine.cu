@@ -656,15 +656,16 @@ struct EngineRun {
     const std::string v(e);
     return v == "32x2" ? 1 : v == "16x4" ? 2 : v == "16x3" ? 0 : 3;
   }();
-  template <int TM, int TN, bool CX, int KC, int ST>
+  template <int TM, int TN, bool CX, int KC, int ST, int WM = 2, int WN = 2>
   void launch_v2_cfg(const SegParams& sp, dim3 grid) {
-    constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST>::SMEM;
+    constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST, WM, WN>::SMEM;
     static bool attr = false;
     if (!attr) {
-      CK(cudaFuncSetAttribute(seg_gemm2_kernel<TM, TN, CX, KC, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(seg_gemm2_kernel<TM, TN, CX, KC, ST, WM, WN>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       attr = true;
     }
-    seg_gemm2_kernel<TM, TN, CX, KC, ST><<<grid, 128, sm, s>>>(sp);
+    seg_gemm2_kernel<TM, TN, CX, KC, ST, WM, WN><<<grid, 32 * WM * WN, sm, s>>>(sp);
   }
   template <int TM, int TN, bool CX>
   void launch_v2(const SegParams& sp, dim3 grid) {
@@ -675,6 +676,15 @@ struct EngineRun {
       default: launch_v2_cfg<TM, TN, CX, 16, 3>(sp, grid); break;
     }
   }
+  // wide CTA tiles (8 or 16 warps of 32x32) for outputs larger than 64 in a dimension
+  const bool seg_wide = !std::getenv("H2B_SEG_NARROW");
+  template <bool CX>
+  void launch_wide(const SegParams& sp, int tm, int tn, dim3 grid) {
+    if (tm == 128 && tn == 128) launch_v2_cfg<128, 128, CX, 8, 4, 4, 4>(sp, grid);
+    else if (tm == 128) launch_v2_cfg<128, 64, CX, 8, 4, 4, 2>(sp, grid);
+    else launch_v2_cfg<64, 128, CX, 8, 4, 2, 4>(sp, grid);
+  }
+
   template <int TM, int TN>
   void launch_seg(const SegParams& sp, int tiles) {
     dim3 grid(sp.n_out, tiles);
@@ -742,6 +752,17 @@ struct EngineRun {
     for (const Grp& g : gs) macs += (g.csr ? g.csr->entries : n_out) * int64_t(M) * N * g.K;
     if (sym) macs = macs / 2 + macs / (2 * ((M + 63) / 64));
     pre("seg_gemm", macs);
+    if (seg_wide && !seg_v1 && !sym && (M > 64 || N > 64)) {
+      const int tm = M > 64 ? 128 : 64, tn = N > 64 ? 128 : 64;
+      const int tiles = ((M + tm - 1) / tm) * ((N + tn - 1) / tn);
+      dim3 grid(sp.n_out, tiles);
+      if (cplx) launch_wide<true>(sp, tm, tn, grid);
+      else launch_wide<false>(sp, tm, tn, grid);
+      CK(cudaGetLastError());
+      launches++;
+      post();
+      return;
+    }
     const int TM = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
     const int TN = N <= 16 ? 16 : (N <= 32 ? 32 : 64);
     const int tm_ = (M + TM - 1) / TM;

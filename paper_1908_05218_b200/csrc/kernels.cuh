@@ -335,8 +335,9 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(const SegParams p) {
 // the layout (both conflict-free with a +4 double pad).  No register staging:
 // fewer registers, more CTAs per SM, and STAGES-1 chunks in flight hide the
 // L2/HBM latency of the next entry's operands.
-template <int TM, int TN, bool CPLX, int KC_ = 16, int ST_ = 3>
+template <int TM, int TN, bool CPLX, int KC_ = 16, int ST_ = 3, int WM_ = 2, int WN_ = 2>
 struct Seg2Cfg {
+  static constexpr int WM = WM_, WN = WN_, NT = 32 * WM_ * WN_;
   static constexpr int W = CPLX ? 2 : 1;
   static constexpr int KC = CPLX ? KC_ / 2 : KC_;
   static constexpr int STAGES = ST_;
@@ -346,7 +347,7 @@ struct Seg2Cfg {
   static constexpr int RSZ = (RKN > RNK ? RKN : RNK) * W;
   static constexpr int STAGE = LSZ + RSZ;  // doubles
   static constexpr int SMEM = STAGES * STAGE * 8;
-  static constexpr int FM = TM / 16, FN = TN / 16;
+  static constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
@@ -360,9 +361,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int TM, int TN, bool CPLX, int KC_ = 16, int ST_ = 3>
-__global__ void __launch_bounds__(128) seg_gemm2_kernel(const SegParams p) {
-  using C = Seg2Cfg<TM, TN, CPLX, KC_, ST_>;
+template <int TM, int TN, bool CPLX, int KC_ = 16, int ST_ = 3, int WM_ = 2, int WN_ = 2>
+__global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm2_kernel(const SegParams p) {
+  using C = Seg2Cfg<TM, TN, CPLX, KC_, ST_, WM_, WN_>;
+  constexpr int NT = C::NT;
   constexpr int KC = C::KC, W = C::W, ST = C::STAGES;
   extern __shared__ __align__(16) double smem[];
 
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(128) seg_gemm2_kernel(const SegParams p) {
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
-  const int wm = (warp & 1) * (TM / 2), wn = (warp >> 1) * (TN / 2);
+  const int wm = (warp % C::WM) * (TM / C::WM), wn = (warp / C::WM) * (TN / C::WN);
 
   double acc[C::FM][C::FN][2];
   double acci[CPLX ? C::FM : 1][CPLX ? C::FN : 1][2];
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(128) seg_gemm2_kernel(const SegParams p) {
     constexpr int EPS = CPLX ? 1 : 2;  // elements per 16-byte segment
     // L chunk: TM x KC elements
     constexpr int LSEG = TM * KC / EPS;
-    for (int sgi = tid; sgi < LSEG; sgi += 128) {
+    for (int sgi = tid; sgi < LSEG; sgi += NT) {
       int m, k;
       if (!lt) {  // [k][m], contiguous in m
         k = sgi / (TM / EPS);
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(128) seg_gemm2_kernel(const SegParams p) {
       cp_async16(dst, ok ? Lp + off * W : Lp, ok);
     }
     constexpr int RSEG = TN * KC / EPS;
-    for (int sgi = tid; sgi < RSEG; sgi += 128) {
+    for (int sgi = tid; sgi < RSEG; sgi += NT) {
       int n, k;
       if (rt) {  // [k][n], contiguous in n
         k = sgi / (TN / EPS);
