@@ -677,7 +677,8 @@ struct EngineRun {
     }
   }
   // wide CTA tiles (8 or 16 warps of 32x32) for outputs larger than 64 in a dimension
-  const bool seg_wide = !std::getenv("H2B_SEG_NARROW");
+  // measured slower than 4-warp tiles on cfg2 (profiles/r01/seg_cfg_ab.txt): opt-in only
+  const bool seg_wide = std::getenv("H2B_SEG_WIDE") != nullptr;
   template <bool CX>
   void launch_wide(const SegParams& sp, int tm, int tn, dim3 grid) {
     if (tm == 128 && tn == 128) launch_v2_cfg<128, 128, CX, 8, 4, 4, 4>(sp, grid);
