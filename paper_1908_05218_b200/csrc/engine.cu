@@ -47,6 +47,7 @@ struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 constexpr int kJacobiMaxN = 64;
+constexpr int kJacobiPackedMaxN = 224;
 
 struct ConfigErr : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
@@ -853,6 +854,8 @@ struct EngineRun {
       CK(cudaGetLastError());
       post();
       launches++;
+    } else if (!cplx && n <= kJacobiPackedMaxN) {
+      packed_jacobi(G, count, n, t);
     } else if (defer) {
       t.G = std::move(G);  // solved later by solve_deferred (possibly concurrently)
       t.n = n;
@@ -861,6 +864,46 @@ struct EngineRun {
       library_eig(G, count, n, t);
     }
     return t;
+  }
+
+  // 64 < n <= 224 (real): packed shared-memory Jacobi + parallel replay of the rotations
+  void packed_jacobi(const DBuf& G, int count, int n, Trunc& t) {
+    constexpr int kSweeps = 20;
+    const int h = n / 2;
+    DBuf log(size_t(count) * kSweeps * (n - 1) * h * 3, s);
+    DVec<int> steps, order;
+    steps.alloc(count, s);
+    order.alloc(size_t(count) * n, s);
+    JacobiPackedParams jp{};
+    jp.G = G;
+    jp.log = log;
+    jp.steps_out = steps.p;
+    jp.order_out = order.p;
+    jp.val_out = t.val;
+    jp.rank_out = t.rank.p;
+    jp.degen_io = t.degen.p;
+    jp.n = n;
+    jp.eps = jp_eps();
+    jp.max_sweeps = kSweeps;
+    const int smem = n * (n + 1) / 2 * int(sizeof(double));
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(jacobi_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      CK(cudaFuncSetAttribute(jacobi_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr = true;
+    }
+    pre("jacobi_packed", 0);
+    jacobi_packed_kernel<<<count, 512, smem, s>>>(jp);
+    CK(cudaGetLastError());
+    post();
+    launches++;
+    const int rows = 32;
+    pre("jacobi_replay", 0);
+    jacobi_replay_kernel<<<dim3((n + rows - 1) / rows, count), 256, rows * n * sizeof(double), s>>>(
+        log, steps.p, order.p, n, kSweeps, rows, t.vec);
+    CK(cudaGetLastError());
+    post();
+    launches++;
   }
 
   // Runs a deferred library eigensolve on side stream 1 in a host thread, so

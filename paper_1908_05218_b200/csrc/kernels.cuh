@@ -874,6 +874,214 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Medium Gram dimensions (64 < n <= 224, real): two-sided cyclic Jacobi on the
+// packed lower triangle in shared memory (n(n+1)/2 doubles <= 200 KB).  With
+// disjoint rotation pairs, every unordered 2x2 block (i, j) of the current
+// pairing is updated exactly once per step as B' = G_i B G_j^T (one phase, two
+// barriers per step).  The rotations are logged to global memory and V is
+// rebuilt afterwards by jacobi_replay_kernel, whose rows are independent
+// (V <- V G^T), so the eigenvector accumulation neither needs shared memory
+// nor serialises the sweep.
+struct JacobiPackedParams {
+  const double* G;     // [batch][n*n] (lower triangle read)
+  double* log;         // [batch][max_steps][n/2][3]  (c, s, sign)
+  int* steps_out;      // [batch] rotation steps taken
+  int* order_out;      // [batch][n] position of eigenvalue i in descending order
+  double* val_out;     // [batch][n]
+  int* rank_out;
+  uint8_t* degen_io;
+  int n;
+  double eps;
+  int max_sweeps;
+};
+
+__device__ __forceinline__ int pk(int r, int c) { return r >= c ? r * (r + 1) / 2 + c : c * (c + 1) / 2 + r; }
+
+__global__ void __launch_bounds__(512) jacobi_packed_kernel(const JacobiPackedParams p) {
+  extern __shared__ __align__(16) double Ap[];
+  const int n = p.n, h = n / 2, b = blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double cs_c[128], cs_s[128], cs_g[128];
+  __shared__ int pp[128], qq[128];
+  __shared__ int any_rot, nonzero, steps;
+  __shared__ double warp_ss[16], fro;
+  const double* G = p.G + (size_t)b * n * n;
+  if (tid == 0) { any_rot = 0; nonzero = 0; steps = 0; }
+  __syncthreads();
+  double ss = 0.0;
+  int nz = 0;
+  for (int x = tid; x < n * (n + 1) / 2; x += nt) {
+    // packed index x -> (r, c), r >= c
+    int r = (int)((sqrt(8.0 * x + 1.0) - 1.0) * 0.5);
+    while ((r + 1) * (r + 2) / 2 <= x) ++r;
+    while (r * (r + 1) / 2 > x) --r;
+    const int c = x - r * (r + 1) / 2;
+    const double v = G[r + (size_t)c * n];
+    Ap[x] = v;
+    nz |= v != 0.0;
+    ss += (r == c ? 1.0 : 2.0) * v * v;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+  }
+  if ((tid & 31) == 0) {
+    warp_ss[tid >> 5] = ss;
+    if (nz) nonzero = 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double f = 0.0;
+    for (int w = 0; w < nt / 32; ++w) f += warp_ss[w];
+    fro = f;
+  }
+  __syncthreads();
+  const double tol_abs = 1e-22 * sqrt(fro);
+  double* log = p.log + (size_t)b * (size_t)p.max_sweeps * (n - 1) * h * 3;
+  int nsteps = 0;
+  const int nblk = h * (h + 1) / 2;
+  if (nonzero) {
+    for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
+      __syncthreads();
+      if (tid == 0) any_rot = 0;
+      __syncthreads();
+      for (int step = 0; step < n - 1; ++step) {
+        for (int i = tid; i < h; i += nt) {
+          auto idx = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + step) % (n - 1)); };
+          const int a = idx(i), c = idx(n - 1 - i);
+          const int pq = a < c ? a : c, qv = a < c ? c : a;
+          pp[i] = pq;
+          qq[i] = qv;
+          const double app = Ap[pk(pq, pq)], aqq = Ap[pk(qv, qv)], br = Ap[pk(qv, pq)];
+          const double babs = fabs(br);
+          double c_ = 1.0, s_ = 0.0, g_ = 1.0;
+          if (babs > tol_abs && babs > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
+            const double tau = (aqq - app) / (2.0 * babs);
+            const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c_ = 1.0 / sqrt(1.0 + tt * tt);
+            s_ = tt * c_;
+            g_ = br >= 0 ? 1.0 : -1.0;
+            any_rot = 1;
+          }
+          cs_c[i] = c_;
+          cs_s[i] = s_;
+          cs_g[i] = g_;
+          double* lg = log + ((size_t)nsteps * h + i) * 3;
+          lg[0] = c_;
+          lg[1] = s_;
+          lg[2] = g_;
+        }
+        __syncthreads();
+        // rotation G = [[c, -s g], [s, c g]] on the (p, q) plane: B' = G_i B G_j^T
+        for (int t = tid; t < nblk; t += nt) {
+          int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+          while ((i + 1) * (i + 2) / 2 <= t) ++i;
+          while (i * (i + 1) / 2 > t) --i;
+          const int j = t - i * (i + 1) / 2;  // j <= i
+          const double ci = cs_c[i], si = cs_s[i], gi = cs_g[i];
+          const double cj = cs_c[j], sj = cs_s[j], gj = cs_g[j];
+          if (si == 0.0 && sj == 0.0) continue;
+          const int pi_ = pp[i], qi = qq[i], pj = pp[j], qj = qq[j];
+          if (i == j) {
+            const double x = Ap[pk(pi_, pi_)], y = Ap[pk(qi, pi_)], w = Ap[pk(qi, qi)];
+            // rows then columns: B' = G B G^T with B symmetric
+            const double r00 = ci * x - si * gi * y, r01 = ci * y - si * gi * w;
+            const double r10 = si * x + ci * gi * y, r11 = si * y + ci * gi * w;
+            Ap[pk(pi_, pi_)] = r00 * ci - r01 * si * gi;
+            Ap[pk(qi, qi)] = r10 * si + r11 * ci * gi;
+            Ap[pk(qi, pi_)] = 0.0;  // annihilated by construction
+          } else {
+            const double x = Ap[pk(pi_, pj)], y = Ap[pk(pi_, qj)], z = Ap[pk(qi, pj)], w = Ap[pk(qi, qj)];
+            const double r00 = ci * x - si * gi * z, r01 = ci * y - si * gi * w;  // G_i B
+            const double r10 = si * x + ci * gi * z, r11 = si * y + ci * gi * w;
+            Ap[pk(pi_, pj)] = r00 * cj - r01 * sj * gj;  // (G_i B) G_j^T
+            Ap[pk(pi_, qj)] = r00 * sj + r01 * cj * gj;
+            Ap[pk(qi, pj)] = r10 * cj - r11 * sj * gj;
+            Ap[pk(qi, qj)] = r10 * sj + r11 * cj * gj;
+          }
+        }
+        __syncthreads();
+        ++nsteps;
+      }
+      const int rotated = any_rot;
+      if (!rotated) break;
+    }
+  }
+  __syncthreads();
+  __shared__ double top_s;
+  __shared__ int rank_s;
+  if (tid == 0) {
+    double top = 0.0;
+    for (int i = 0; i < n; ++i) top = fmax(top, fmax(Ap[pk(i, i)], 0.0));
+    top_s = top;
+    rank_s = 0;
+  }
+  __syncthreads();
+  const double top = top_s;
+  const bool unit = !nonzero || !(top > 0.0);
+  for (int i = tid; i < n; i += nt) {
+    const double li = fmax(Ap[pk(i, i)], 0.0);
+    int pos = 0;
+    for (int j = 0; j < n; ++j) {
+      const double lj = fmax(Ap[pk(j, j)], 0.0);
+      pos += (lj > li) || (lj == li && j < i);
+    }
+    p.val_out[(size_t)b * n + pos] = li;
+    p.order_out[(size_t)b * n + i] = pos;
+    if (li > p.eps * top) atomicAdd(&rank_s, 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    p.steps_out[b] = unit ? -1 : nsteps;  // -1: e_1 basis
+    p.rank_out[b] = unit ? 1 : (rank_s < 1 ? 1 : rank_s);
+    p.degen_io[b] = (unit ? 1 : 0) | p.degen_io[b];
+  }
+}
+
+// V = G_1^T G_2^T ... (rows independent): each CTA rebuilds `rows` rows of V in
+// shared memory and writes them as sorted eigenvector columns.
+__global__ void __launch_bounds__(256) jacobi_replay_kernel(const double* log, const int* steps, const int* order,
+                                                            int n, int max_sweeps, int rows_per_cta, double* vec_out) {
+  extern __shared__ __align__(16) double Vs[];  // [rows][n]
+  const int b = blockIdx.y, r0 = blockIdx.x * rows_per_cta;
+  const int h = n / 2, tid = threadIdx.x, nt = blockDim.x;
+  const int nr = min(rows_per_cta, n - r0);
+  if (nr <= 0) return;
+  const int ns = steps[b];
+  for (int x = tid; x < nr * n; x += nt) {
+    const int rr = x / n, c = x % n;
+    Vs[x] = (r0 + rr == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const double* lg = log + (size_t)b * (size_t)max_sweeps * (n - 1) * h * 3;
+  for (int st = 0; st < ns; ++st) {
+    const int step = st % (n - 1);
+    for (int x = tid; x < nr * h; x += nt) {
+      const int rr = x / h, i = x % h;
+      const double* g = lg + ((size_t)st * h + i) * 3;
+      const double c_ = g[0], s_ = g[1], g_ = g[2];
+      if (s_ == 0.0) continue;
+      auto idx = [&](int y) { return y == 0 ? 0 : 1 + ((y - 1 + step) % (n - 1)); };
+      const int a = idx(i), cc = idx(n - 1 - i);
+      const int pq = a < cc ? a : cc, qv = a < cc ? cc : a;
+      double* v = Vs + rr * n;
+      const double vp = v[pq], vq = v[qv];
+      v[pq] = c_ * vp - s_ * g_ * vq;
+      v[qv] = s_ * vp + c_ * g_ * vq;
+    }
+    __syncthreads();
+  }
+  double* out = vec_out + (size_t)b * n * n;
+  for (int x = tid; x < nr * n; x += nt) {
+    const int rr = x / n, c = x % n;
+    const int pos = ns < 0 ? c : order[(size_t)b * n + c];
+    double v = Vs[x];
+    if (ns < 0) v = (r0 + rr == 0 && c == 0) ? 1.0 : 0.0;  // e_1
+    out[(r0 + rr) + (size_t)pos * n] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Finalize a library eigendecomposition (ascending eigenvalues, eigenvectors
 // in columns) into the truncation output of jacobi_kernel: clamp at 0, sort
 // descending, strict threshold, >= 1 vector, e_1 for exactly-zero Grams
