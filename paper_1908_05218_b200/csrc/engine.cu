@@ -886,12 +886,9 @@ struct EngineRun {
     jp.eps = jp_eps();
     jp.max_sweeps = kSweeps;
     const int smem = n * (n + 1) / 2 * int(sizeof(double));
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(jacobi_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      CK(cudaFuncSetAttribute(jacobi_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr = true;
-    }
+    CK(cudaFuncSetAttribute(jacobi_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(jacobi_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(32 * n * sizeof(double))));
     pre("jacobi_packed", 0);
     jacobi_packed_kernel<<<count, 512, smem, s>>>(jp);
     CK(cudaGetLastError());
