@@ -98,6 +98,13 @@ void h2c_operand_free(h2c_operand* op);
 int h2c_mmp_resident(h2c_context* ctx, const h2c_operand* a, const h2c_operand* b,
                      double eps_trunc, int adaptive, double* device_seconds, h2c_result** out);
 
+/* ---- svd_truncate_gram on the device (truncation.hpp:18-19, truncation.cpp:9-47) ----
+ * Orthonormal eigenvectors of a Hermitian PSD Gram with lambda_i > eps*lambda_max
+ * (strict, >= 1 kept, zero Gram -> e_1 + degenerate), through the same device
+ * solvers the product uses.  basis_out: n x n scalars (first *rank columns set). */
+int h2c_truncate_gram(h2c_context* ctx, int scalar, const double* gram, int n, double eps,
+                      double* basis_out, int* rank, int* degenerate);
+
 /* ---- exact H^2 matrix-vector product on the device (h2_matrix.cpp:213-278) ----
  * Y = A X for nv vectors; X, Y column-major N x nv in the ORIGINAL point
  * ordering (complex interleaved).  Used for the paper's eps_rel metric

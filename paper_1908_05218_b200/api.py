@@ -165,6 +165,23 @@ def build_fd_laplacian(tree: ClusterTree, structure: BlockTree, points: np.ndarr
 
 
 # ---------------------------------------------------------------------------
+def svd_truncate_gram(gram: np.ndarray, eps: float, ctx: Optional[Context] = None):
+    """svd_truncate_gram (truncation.cpp:9-47) on the B200 -> (basis, degenerate)."""
+    g = np.asfortranarray(gram)
+    if g.ndim != 2 or g.shape[0] != g.shape[1] or g.shape[0] < 1:
+        raise ConfigError("svd_truncate_gram: gram matrix must be square and non-empty")
+    cplx = np.iscomplexobj(g)
+    g = np.asfortranarray(g, dtype=np.complex128 if cplx else np.float64)
+    ctx = ctx or default_context()
+    n = g.shape[0]
+    basis = np.zeros((n, n), dtype=g.dtype, order="F")
+    rank, degen = C.c_int(), C.c_int()
+    rc = h2c.lib().h2c_truncate_gram(ctx.handle, int(cplx), g.ctypes.data_as(h2c.P_f64), n, float(eps),
+                                     basis.ctypes.data_as(h2c.P_f64), C.byref(rank), C.byref(degen))
+    raise_for(rc, h2c.last_error(ctx.handle))
+    return basis[:, :rank.value].copy(), bool(degen.value)
+
+
 def random_vector(n: int, seed: int, complex_: bool = False) -> np.ndarray:
     """random_vector (metrics.cpp:11-35)."""
     out = np.zeros(n, dtype=np.complex128 if complex_ else np.float64)

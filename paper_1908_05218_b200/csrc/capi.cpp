@@ -351,3 +351,9 @@ int h2c_random_vector(int n, uint64_t seed, int scalar, double* out) {
   for (int64_t i = 0; i < int64_t(n) * (scalar == H2C_COMPLEX ? 2 : 1); ++i) out[i] = u();
   return H2C_OK;
 }
+
+int h2c_truncate_gram(h2c_context* ctx, int scalar, const double* gram, int n, double eps, double* basis, int* rank,
+                      int* degenerate) {
+  if (!ctx) return H2C_ERR_CUDA;
+  return guarded(ctx, [&] { ctx->ctx->truncate_gram(scalar, gram, n, eps, basis, rank, degenerate); });
+}

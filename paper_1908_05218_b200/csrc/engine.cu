@@ -868,33 +868,42 @@ struct EngineRun {
 
   // 64 < n <= 224 (real): packed shared-memory Jacobi + parallel replay of the rotations
   void packed_jacobi(const DBuf& G, int count, int n, Trunc& t) {
-    constexpr int kSweeps = 20;
+    constexpr int kSweeps = 30;
     const int h = n / 2;
-    DBuf log(size_t(count) * kSweeps * (n - 1) * h * 3, s);
+    const bool vsm = n <= 128;  // packed A + V both fit in shared memory
+    DBuf log;
+    if (!vsm) log.alloc(size_t(count) * kSweeps * (n - 1) * h * 3, s);
     DVec<int> steps, order;
     steps.alloc(count, s);
     order.alloc(size_t(count) * n, s);
     JacobiPackedParams jp{};
     jp.G = G;
-    jp.log = log;
+    jp.log = log.p;
     jp.steps_out = steps.p;
     jp.order_out = order.p;
     jp.val_out = t.val;
+    jp.vec_out = t.vec;
     jp.rank_out = t.rank.p;
     jp.degen_io = t.degen.p;
     jp.n = n;
     jp.eps = jp_eps();
     jp.max_sweeps = kSweeps;
-    const int smem = n * (n + 1) / 2 * int(sizeof(double));
-    CK(cudaFuncSetAttribute(jacobi_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaFuncSetAttribute(jacobi_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(32 * n * sizeof(double))));
+    const int smem = (n * (n + 1) / 2 + (vsm ? n * (n + 1) : 0)) * int(sizeof(double));
     pre("jacobi_packed", 0);
-    jacobi_packed_kernel<<<count, 512, smem, s>>>(jp);
+    if (vsm) {
+      CK(cudaFuncSetAttribute(jacobi_packed_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      jacobi_packed_kernel<true><<<count, 512, smem, s>>>(jp);
+    } else {
+      CK(cudaFuncSetAttribute(jacobi_packed_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      jacobi_packed_kernel<false><<<count, 512, smem, s>>>(jp);
+    }
     CK(cudaGetLastError());
     post();
     launches++;
+    if (vsm) return;
     const int rows = 32;
+    CK(cudaFuncSetAttribute(jacobi_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(rows * n * sizeof(double))));
     pre("jacobi_replay", 0);
     jacobi_replay_kernel<<<dim3((n + rows - 1) / rows, count), 256, rows * n * sizeof(double), s>>>(
         log, steps.p, order.p, n, kSweeps, rows, t.vec);
@@ -1600,6 +1609,36 @@ struct EngineRun {
     launches++;
   }
 
+  // ---- single Gram truncation on the device (truncation.cpp:9-47) ------------
+  // The Gram is zero-padded to a multiple of 8 (padding adds exact zero
+  // eigenvalues, never kept) and sent through the same path as the product's
+  // Grams; g2 = g3 = 0 so the normalised sum is G/||G||_F (same eigenvectors,
+  // same relative threshold).
+  void truncate_one(const double* gram_host, int n, double* basis_host, int* rank, int* degenerate) {
+    const int np = pad8(n);
+    std::vector<double> g(size_t(np) * np * W, 0.0);
+    for (int c = 0; c < n; ++c)
+      for (int r = 0; r < n; ++r)
+        for (int w = 0; w < W; ++w) g[(r + size_t(c) * np) * W + w] = gram_host[(r + size_t(c) * n) * W + w];
+    DBuf g1(g.size(), s), g2(g.size(), s, true), g3(g.size(), s, true);
+    CK(cudaMemcpyAsync(g1.p, g.data(), g.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    DVec<uint8_t> opdeg;
+    opdeg.upload(std::vector<uint8_t>{0}, s);
+    Trunc t = truncate(g1, g2, g3, 1, np, opdeg);
+    std::vector<double> v(size_t(np) * np * W);
+    int rk = 0;
+    uint8_t dg = 0;
+    CK(cudaMemcpyAsync(v.data(), t.vec.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&rk, t.rank.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&dg, t.degen.p, 1, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < rk; ++c)
+      for (int r = 0; r < n; ++r)
+        for (int w = 0; w < W; ++w) basis_host[(r + size_t(c) * n) * W + w] = v[(r + size_t(c) * np) * W + w];
+    *rank = rk;
+    *degenerate = dg;
+  }
+
   // per (phase, kernel) totals of the profiled launches
   void collect_profile(std::vector<ProfileEntry>& out) {
     out.clear();
@@ -1988,6 +2027,22 @@ void Context::mvp(const std::shared_ptr<DevOperand>& a, const double* x_host, in
   R.mvp(X.p, nv, Y.p, perm.p);
   CK(cudaMemcpyAsync(y_host, Y.p, bytes, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  launches_ = R.launches;
+}
+
+void Context::truncate_gram(int scalar, const double* gram, int n, double eps, double* basis, int* rank,
+                            int* degenerate) {
+  if (n < 1) throw ConfigErr("svd_truncate_gram: gram matrix must be square and non-empty");
+  if (!(eps > 0.0 && eps < 1.0)) throw ConfigErr("svd_truncate_gram: eps must be in (0,1)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  CK(cudaSetDevice(device_));
+  // a one-cluster dummy run context: only the truncation path is used
+  static Plan empty_plan;
+  static DevPlan empty_dplan;
+  DevOperand dummy;
+  dummy.scalar = scalar;
+  EngineRun R(*this, empty_plan, empty_dplan, dummy, dummy, eps, true, s);
+  R.truncate_one(gram, n, basis, rank, degenerate);
   launches_ = R.launches;
 }
 

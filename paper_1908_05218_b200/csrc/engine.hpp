@@ -79,6 +79,8 @@ class Context {
   // runs the pipeline on resident operands; returns device seconds (CUDA events)
   double run_resident(const std::shared_ptr<DevOperand>& a, const std::shared_ptr<DevOperand>& b,
                       double eps, int adaptive, HostResult* download_to);
+  // svd_truncate_gram on the device (truncation.cpp:9-47); basis: n x n buffer
+  void truncate_gram(int scalar, const double* gram, int n, double eps, double* basis, int* rank, int* degenerate);
   // exact H^2 MVP Y = A X on a resident operand (host X, Y: N x nv, original ordering)
   void mvp(const std::shared_ptr<DevOperand>& a, const double* x, int nv, double* y);
   void* stream() const { return stream_; }

@@ -747,7 +747,9 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
     fro = f;
   }
   __syncthreads();
-  const double tol_abs = 1e-22 * sqrt(fro);
+  // rotation threshold at the rounding level of ||G||_F: below it rotations only
+  // reshuffle round-off (the null space of a PSD Gram) and never converge
+  const double tol_abs = 2.2e-16 * sqrt(fro);
   const int half = n / 2;
   if (nonzero) {
     for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
@@ -888,6 +890,7 @@ struct JacobiPackedParams {
   int* steps_out;      // [batch] rotation steps taken
   int* order_out;      // [batch][n] position of eigenvalue i in descending order
   double* val_out;     // [batch][n]
+  double* vec_out;     // VSM: [batch][n*n] sorted eigenvectors
   int* rank_out;
   uint8_t* degen_io;
   int n;
@@ -897,9 +900,12 @@ struct JacobiPackedParams {
 
 __device__ __forceinline__ int pk(int r, int c) { return r >= c ? r * (r + 1) / 2 + c : c * (c + 1) / 2 + r; }
 
+template <bool VSM>
 __global__ void __launch_bounds__(512) jacobi_packed_kernel(const JacobiPackedParams p) {
   extern __shared__ __align__(16) double Ap[];
   const int n = p.n, h = n / 2, b = blockIdx.x;
+  double* Vs = Ap + n * (n + 1) / 2;  // VSM: V in shared memory, ld n + 1
+  const int vld = n + 1;
   const int tid = threadIdx.x, nt = blockDim.x;
   __shared__ double cs_c[128], cs_s[128], cs_g[128];
   __shared__ int pp[128], qq[128];
@@ -936,10 +942,26 @@ __global__ void __launch_bounds__(512) jacobi_packed_kernel(const JacobiPackedPa
     fro = f;
   }
   __syncthreads();
-  const double tol_abs = 1e-22 * sqrt(fro);
-  double* log = p.log + (size_t)b * (size_t)p.max_sweeps * (n - 1) * h * 3;
+  // rotation threshold at the rounding level of ||G||_F: below it rotations only
+  // reshuffle round-off (the null space of a PSD Gram) and never converge
+  const double tol_abs = 2.2e-16 * sqrt(fro);
+  double* log = VSM ? nullptr : p.log + (size_t)b * (size_t)p.max_sweeps * (n - 1) * h * 3;
   int nsteps = 0;
   const int nblk = h * (h + 1) / 2;
+  if (VSM)
+    for (int x = tid; x < n * vld; x += nt) Vs[x] = (x % vld == x / vld) ? 1.0 : 0.0;
+  // this thread's 2x2 blocks (i, j), j <= i, decoded once
+  constexpr int kMaxBlk = 13;  // ceil(112 * 113 / 2 / 512)
+  int bi_[kMaxBlk], bj_[kMaxBlk], nmine = 0;
+  for (int t = tid; t < nblk && nmine < kMaxBlk; t += nt) {
+    int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    while (i * (i + 1) / 2 > t) --i;
+    bi_[nmine] = i;
+    bj_[nmine] = t - i * (i + 1) / 2;
+    ++nmine;
+  }
+  __syncthreads();
   if (nonzero) {
     for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
       __syncthreads();
@@ -966,18 +988,27 @@ __global__ void __launch_bounds__(512) jacobi_packed_kernel(const JacobiPackedPa
           cs_c[i] = c_;
           cs_s[i] = s_;
           cs_g[i] = g_;
-          double* lg = log + ((size_t)nsteps * h + i) * 3;
-          lg[0] = c_;
-          lg[1] = s_;
-          lg[2] = g_;
+          if (!VSM) {
+            double* lg = log + ((size_t)nsteps * h + i) * 3;
+            lg[0] = c_;
+            lg[1] = s_;
+            lg[2] = g_;
+          }
         }
         __syncthreads();
         // rotation G = [[c, -s g], [s, c g]] on the (p, q) plane: B' = G_i B G_j^T
-        for (int t = tid; t < nblk; t += nt) {
-          int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-          while ((i + 1) * (i + 2) / 2 <= t) ++i;
-          while (i * (i + 1) / 2 > t) --i;
-          const int j = t - i * (i + 1) / 2;  // j <= i
+        if (VSM)  // V <- V G^T on the pair columns (rows independent)
+          for (int x = tid; x < n * h; x += nt) {
+            const int r = x / h, i = x % h;
+            const double c_ = cs_c[i], s_ = cs_s[i], g_ = cs_g[i];
+            if (s_ == 0.0) continue;
+            double* v = Vs + r * vld;
+            const double vp = v[pp[i]], vq = v[qq[i]];
+            v[pp[i]] = c_ * vp - s_ * g_ * vq;
+            v[qq[i]] = s_ * vp + c_ * g_ * vq;
+          }
+        for (int u = 0; u < nmine; ++u) {
+          const int i = bi_[u], j = bj_[u];  // j <= i
           const double ci = cs_c[i], si = cs_s[i], gi = cs_g[i];
           const double cj = cs_c[j], sj = cs_s[j], gj = cs_g[j];
           if (si == 0.0 && sj == 0.0) continue;
@@ -1029,6 +1060,11 @@ __global__ void __launch_bounds__(512) jacobi_packed_kernel(const JacobiPackedPa
     p.val_out[(size_t)b * n + pos] = li;
     p.order_out[(size_t)b * n + i] = pos;
     if (li > p.eps * top) atomicAdd(&rank_s, 1);
+    if (VSM) {
+      double* out = p.vec_out + (size_t)b * n * n;
+      for (int r = 0; r < n; ++r)
+        out[r + (size_t)pos * n] = unit ? ((r == 0 && pos == 0) ? 1.0 : 0.0) : Vs[r * vld + i];
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -1054,12 +1090,18 @@ __global__ void __launch_bounds__(256) jacobi_replay_kernel(const double* log, c
   }
   __syncthreads();
   const double* lg = log + (size_t)b * (size_t)max_sweeps * (n - 1) * h * 3;
+  __shared__ double rot[2][112 * 3];
+  if (ns > 0)
+    for (int x = tid; x < h * 3; x += nt) rot[0][x] = lg[x];
+  __syncthreads();
   for (int st = 0; st < ns; ++st) {
     const int step = st % (n - 1);
+    const double* cur = rot[st & 1];
+    if (st + 1 < ns)  // stage the next step's rotations
+      for (int x = tid; x < h * 3; x += nt) rot[(st + 1) & 1][x] = lg[(size_t)(st + 1) * h * 3 + x];
     for (int x = tid; x < nr * h; x += nt) {
       const int rr = x / h, i = x % h;
-      const double* g = lg + ((size_t)st * h + i) * 3;
-      const double c_ = g[0], s_ = g[1], g_ = g[2];
+      const double c_ = cur[3 * i], s_ = cur[3 * i + 1], g_ = cur[3 * i + 2];
       if (s_ == 0.0) continue;
       auto idx = [&](int y) { return y == 0 ? 0 : 1 + ((y - 1 + step) % (n - 1)); };
       const int a = idx(i), cc = idx(n - 1 - i);

@@ -420,6 +420,9 @@ def lib() -> C.CDLL:
         L.h2c_mvp_resident.argtypes = [C.c_void_p, C.c_void_p, P_f64, C.c_int, P_f64]
         L.h2c_random_vector.restype = C.c_int
         L.h2c_random_vector.argtypes = [C.c_int, C.c_uint64, C.c_int, P_f64]
+        L.h2c_truncate_gram.restype = C.c_int
+        L.h2c_truncate_gram.argtypes = [C.c_void_p, C.c_int, P_f64, C.c_int, C.c_double, P_f64, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int)]
         L.h2c_plan_stats.restype = C.c_int
         L.h2c_plan_stats.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_i64, C.c_int]
         L.h2c_host_alloc.restype = C.c_void_p

@@ -375,3 +375,34 @@ def test_relative_error_matches_oracle(ctx):
     e_gpu = P.relative_error(A, A, C, 99, ctx)
     e_ora = O.relative_error(A, A, C, 99)
     assert abs(e_gpu - e_ora) <= 1e-9 * max(e_ora, 1e-30) + 1e-15
+
+
+# ---- the device truncation (truncation.cpp:9-47) on the reference's KATs and random Grams
+def test_device_truncation_known_answers(ctx):
+    assert P.svd_truncate_gram(np.eye(4), 1e-2, ctx)[0].shape[1] == 4
+    assert P.svd_truncate_gram(np.diag([1.0, 1e-1, 1e-3, 0.0]), 1e-2, ctx)[0].shape[1] == 2
+    tie = np.diag([1.0, 1e-2])
+    assert P.svd_truncate_gram(tie, 1e-2, ctx)[0].shape[1] == 1
+    assert P.svd_truncate_gram(tie, 0.5e-2, ctx)[0].shape[1] == 2
+    b, dg = P.svd_truncate_gram(np.zeros((5, 5)), 1e-4, ctx)
+    assert dg and b.shape == (5, 1) and b[0, 0] == 1.0 and np.all(b[1:] == 0)
+    with pytest.raises(P.ConfigError):
+        P.svd_truncate_gram(np.eye(3), 1.0, ctx)
+
+
+@pytest.mark.parametrize("n", [6, 33, 64, 100, 150, 224, 300])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_device_truncation_matches_oracle(ctx, n, cplx):
+    rng = np.random.default_rng(n)
+    k = max(1, (2 * n) // 3)
+    m = rng.standard_normal((n, k)) * np.logspace(0, -9, k)
+    if cplx:
+        m = m + 1j * rng.standard_normal((n, k)) * np.logspace(0, -9, k)
+    g = m @ m.conj().T
+    for eps in (1e-4, 1e-8):
+        bg, dg = P.svd_truncate_gram(g, eps, ctx)
+        bo, do = O.svd_truncate_gram(g, eps)
+        assert bg.shape == bo.shape and dg == do
+        assert np.abs(bg.conj().T @ bg - np.eye(bg.shape[1])).max() <= 1e-12
+        # same subspace: projector difference
+        assert np.linalg.norm(bg @ bg.conj().T - bo @ bo.conj().T) <= 1e-6
