@@ -900,6 +900,19 @@ struct EngineRun {
     CK(cudaGetLastError());
     post();
     launches++;
+    if (debug_check) {
+      std::vector<int> st(count);
+      CK(cudaMemcpyAsync(st.data(), steps.p, count * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      long tot = 0;
+      int mx = 0;
+      for (int v : st) {
+        tot += v;
+        mx = std::max(mx, v);
+      }
+      std::fprintf(stderr, "[jacobi_packed] n=%d count=%d sweeps mean %.1f max %.1f\n", n, count,
+                   double(tot) / count / (n - 1), double(mx) / (n - 1));
+    }
     if (vsm) return;
     const int rows = 32;
     CK(cudaFuncSetAttribute(jacobi_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
