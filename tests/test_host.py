@@ -157,3 +157,22 @@ def test_config_errors():
 def test_random_vector_matches_reference_stream():
     for seed, cplx in ((5, False), (99, False), (3, True)):
         assert np.array_equal(P.random_vector(257, seed, cplx), O.random_vector(257, seed, cplx))
+
+
+def test_h2bin_roundtrip_and_corruption(tmp_path):
+    from paper_1908_05218_b200 import h2io
+    pts = P.random_cloud(512, 3)
+    t = P.build_cluster_tree(pts, 32)
+    s = P.build_block_tree(t, t, 1.0)
+    A = P.build_chebyshev(t, s, pts, 3)
+    f = str(tmp_path / "a.npz")
+    h2io.save_h2(f, A)
+    B = h2io.load_h2(f, t, s)
+    assert B.tree is t and B.structure is s
+    assert np.array_equal(B.values, A.values) and np.array_equal(B.block_offset, A.block_offset)
+    C = h2io.load_h2(f)
+    assert C.tree.same_as(t) and np.array_equal(C.values.view(np.uint64), A.values.view(np.uint64))
+    raw = open(f, "rb").read()
+    open(f, "wb").write(raw[: len(raw) // 2])
+    with pytest.raises(h2io.LoadError):
+        h2io.load_h2(f)
