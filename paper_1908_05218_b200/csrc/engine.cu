@@ -595,6 +595,9 @@ struct EngineRun {
   }
   const bool debug_sync = std::getenv("H2B_DEBUG_SYNC") != nullptr;
   const bool debug_check = std::getenv("H2B_DEBUG_CHECK") != nullptr;
+  // solver selection knobs (A/B): library solver also for n <= 64; packed Jacobi for 64 < n <= 224
+  const bool force_library = std::getenv("H2B_EIG_LIBRARY") != nullptr;
+  const bool use_packed = std::getenv("H2B_EIG_PACKED") != nullptr;
 
   // C
   std::vector<int> KCr, KCc;
@@ -842,7 +845,7 @@ struct EngineRun {
     jp.eps = adaptive ? eps : 0.5;
     jp.max_sweeps = 40;
     const size_t smem = size_t(2) * n * (n + 1) * W * sizeof(double);
-    if (n <= kJacobiMaxN) {
+    if (n <= kJacobiMaxN && !force_library) {
       pre("jacobi_eig", 0);
       if (cplx) {
         CK(cudaFuncSetAttribute(jacobi_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -854,7 +857,7 @@ struct EngineRun {
       CK(cudaGetLastError());
       post();
       launches++;
-    } else if (!cplx && n <= kJacobiPackedMaxN) {
+    } else if (!cplx && n <= kJacobiPackedMaxN && use_packed) {
       packed_jacobi(G, count, n, t);
     } else if (defer) {
       t.G = std::move(G);  // solved later by solve_deferred (possibly concurrently)

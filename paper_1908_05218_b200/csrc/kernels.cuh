@@ -747,9 +747,10 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
     fro = f;
   }
   __syncthreads();
-  // rotation threshold at the rounding level of ||G||_F: below it rotations only
-  // reshuffle round-off (the null space of a PSD Gram) and never converge
-  const double tol_abs = 2.2e-16 * sqrt(fro);
+  // rotation threshold a few ulps of ||G||_F (LAPACK-level backward error):
+  // below it rotations only reshuffle round-off in the null space of the PSD
+  // Gram and never converge
+  const double tol_abs = 2e-15 * sqrt(fro);
   const int half = n / 2;
   if (nonzero) {
     for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
@@ -942,9 +943,10 @@ __global__ void __launch_bounds__(512) jacobi_packed_kernel(const JacobiPackedPa
     fro = f;
   }
   __syncthreads();
-  // rotation threshold at the rounding level of ||G||_F: below it rotations only
-  // reshuffle round-off (the null space of a PSD Gram) and never converge
-  const double tol_abs = 2.2e-16 * sqrt(fro);
+  // rotation threshold a few ulps of ||G||_F (LAPACK-level backward error):
+  // below it rotations only reshuffle round-off in the null space of the PSD
+  // Gram and never converge
+  const double tol_abs = 2e-15 * sqrt(fro);
   double* log = VSM ? nullptr : p.log + (size_t)b * (size_t)p.max_sweeps * (n - 1) * h * 3;
   int nsteps = 0;
   const int nblk = h * (h + 1) / 2;
