@@ -690,9 +690,32 @@ struct EngineRun {
     else launch_v2_cfg<64, 128, CX, 8, 4, 2, 4>(sp, grid);
   }
 
+  // v3 (default): v2's pipeline without the per-chunk integer work; needs every
+  // inner dimension to be a multiple of the k-chunk (8), which the padded layout
+  // guarantees.  H2B_SEG_V2=1 selects v2 for A/B runs.
+  const bool seg_v2 = std::getenv("H2B_SEG_V2") != nullptr;
+  template <int TM, int TN, bool CX, int KC, int ST>
+  void launch_v3_cfg(const SegParams& sp, dim3 grid) {
+    constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST>::SMEM;
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(seg_gemm3_kernel<TM, TN, CX, KC, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      attr = true;
+    }
+    seg_gemm3_kernel<TM, TN, CX, KC, ST><<<grid, 128, sm, s>>>(sp);
+  }
   template <int TM, int TN>
   void launch_seg(const SegParams& sp, int tiles) {
     dim3 grid(sp.n_out, tiles);
+    bool v3 = !seg_v1 && !seg_v2;
+    for (int g = 0; g < sp.ngroups; ++g) v3 = v3 && sp.g[g].K % 8 == 0;
+    if (v3) {
+      if (cplx) launch_v3_cfg<TM, TN, true, 8, 4>(sp, grid);
+      else launch_v3_cfg<TM, TN, false, 8, 4>(sp, grid);
+      CK(cudaGetLastError());
+      launches++;
+      return;
+    }
     if (!seg_v1) {
       if (cplx) launch_v2<TM, TN, true>(sp, grid);
       else launch_v2<TM, TN, false>(sp, grid);
