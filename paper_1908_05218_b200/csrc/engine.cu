@@ -22,6 +22,7 @@
 // sum_j (V^C^H F_ij)(F_jk conj(V^C)), and the leaf Gram
 // G1 = sum_{j,k} (F F)(F F)^H is evaluated as sum_j F_ij (sum_k F_jk F_jk^H) F_ij^H.
 #include <cuda_runtime.h>
+#include <cuda.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -604,7 +605,9 @@ struct EngineRun {
   std::vector<std::vector<int64_t>> rcr, rcc;
   std::vector<DVec<uint8_t>> dgr, dgc;
   DBuf Vr, Vc, F;
-  std::vector<DBuf> Tr, Tc, Tg;
+  std::vector<DBuf> Tr, Tc, Tg, Tp;  // Tg: [adm | NL] targets, Tp: pending targets
+  // H2B_NO_DEFER=1: admissible / NL targets on the main stream (A/B runs)
+  const bool defer_targets = std::getenv("H2B_NO_DEFER") == nullptr;
   // per-level intermediates
   std::vector<DBuf> Bp, PA, PB, LA, RB;
   // auxiliary stream for the C-independent leaf full targets
@@ -614,11 +617,14 @@ struct EngineRun {
   std::vector<DBuf> hold;
   void join() {
     if (joined) return;
+    CK(cudaEventRecord(ev_full, s_aux));  // everything queued on the auxiliary stream so far
     CK(cudaStreamWaitEvent(s, ev_full, 0));
     hold.clear();  // frees on the main stream, ordered after the join
     joined = true;
   }
   ~EngineRun() {
+    // deferred work may still read held buffers (error paths): drain it first
+    if (s_aux) cudaStreamSynchronize(s_aux);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_full) cudaEventDestroy(ev_full);
   }
@@ -639,6 +645,7 @@ struct EngineRun {
     Tr.resize(D + 1);
     Tc.resize(D + 1);
     Tg.resize(D + 1);
+    Tp.resize(D + 1);
     Bp.resize(D + 1);
     PA.resize(D + 1);
     PB.resize(D + 1);
@@ -1172,38 +1179,109 @@ struct EngineRun {
   //        = P^A_i [V1 P^B_k + U2] + U1 P^B_k (+ merged + leaf F x F)
   //   V1 = sum_{A,B adm} SB_ij S^B_jk,  U1 = sum_{A near} coll_a_ij S^B_jk,
   //   U2 = sum_{A adm, B near} S^A_ij coll_b_jk
+  // Target slots of a level: [0, na) admissible, [na, na + np) pending, then NL.
+  // The pending targets feed the parent level's merge (critical path) and run
+  // on the main stream into Tp[l]; the admissible and NL targets are only read
+  // by split() and the download, so they run on the low-priority auxiliary
+  // stream into the compact store Tg[l] = [adm | NL], overlapping the parent
+  // levels' Gram / eigensolver / collect chain.
   void targets(int l, const DBuf& SB, const DBuf* WA, const DBuf* WB, const DBuf* Z, int Kq) {
     const LevelPlan& L = P.lv[l];
+    const int na = static_cast<int>(L.adm.size()), np = static_cast<int>(L.pend_row.size());
+    const int nl = static_cast<int>(L.nl_block.size());
+    const int Kr = KCr[l], Kc = KCc[l];
+    Tp[l].alloc(sz(np, Kr, Kc), s);
+    targets_range(l, na, np, Tp[l], 0, SB, WA, WB, Z, Kq);
+    Tg[l].alloc(sz(na + nl, Kr, Kc), s);
+    if (!defer_targets) {
+      targets_range(l, 0, na, Tg[l], 0, SB, WA, WB, Z, Kq);
+      targets_range(l, na + np, nl, Tg[l], na, SB, WA, WB, Z, Kq);
+      return;
+    }
+    on_aux(phase + "_deferred", [&] {
+      targets_range(l, 0, na, Tg[l], 0, SB, WA, WB, Z, Kq);
+      targets_range(l, na + np, nl, Tg[l], na, SB, WA, WB, Z, Kq);
+    });
+  }
+
+  // run `fn` on the auxiliary stream, ordered after everything issued so far on
+  // the main stream; buffers it allocates are stream-ordered on the auxiliary
+  // stream, main-stream inputs it reads must stay in `hold` until join().
+  template <class Fn>
+  void on_aux(const std::string& ph, Fn&& fn) {
+    CK(cudaEventRecord(ev_fork, s));
+    CK(cudaStreamWaitEvent(s_aux, ev_fork, 0));
+    cudaStream_t keep = s;
+    const std::string keep_phase = phase;
+    s = s_aux;
+    phase = ph;
+    try {
+      fn();
+    } catch (...) {
+      s = keep;
+      phase = keep_phase;
+      throw;
+    }
+    s = keep;
+    phase = keep_phase;
+    joined = false;
+  }
+
+  static DevCsr sub_csr(const DevCsr& d, const Csr& h, int t0, int cnt) {
+    DevCsr r;
+    r.ptr = d.ptr ? d.ptr + t0 : nullptr;
+    r.li = d.li;
+    r.ri = d.ri;
+    r.n_out = cnt;
+    r.entries = h.ptr.empty() ? 0 : int64_t(h.ptr[t0 + cnt]) - h.ptr[t0];
+    return r;
+  }
+
+  // coupling targets t0 .. t0+cnt-1 of level l into out slots slot0.. (mmp.cpp:319-334, 573-612)
+  // The projections depend only on the target, so they leave the sum over j:
+  //   T_ik = P^A_i (sum_RR S^A B_j S^B + ...) P^B_k
+  //        = P^A_i [V1 P^B_k + U2] + U1 P^B_k (+ merged + leaf F x F)
+  //   V1 = sum_{A,B adm} SB_ij S^B_jk,  U1 = sum_{A near} coll_a_ij S^B_jk,
+  //   U2 = sum_{A adm, B near} S^A_ij coll_b_jk
+  void targets_range(int l, int t0, int cnt, double* out, long long slot0, const DBuf& SB, const DBuf* WA,
+                     const DBuf* WB, const DBuf* Z, int Kq) {
+    if (cnt <= 0) return;
+    const LevelPlan& L = P.lv[l];
     const DevLevel& Q = DP.lv[l];
-    const int nt = L.n_targets();
     const int KAr = A.Kr[l], KAc = A.Kc[l], KBr = B.Kr[l], KBc = B.Kc[l], Kr = KCr[l], Kc = KCc[l];
+    const DevCsr lyr = sub_csr(Q.lyr, L.lyr, t0, cnt), lyn = sub_csr(Q.lyn, L.lyn, t0, cnt),
+                 xr = sub_csr(Q.xr, L.xr, t0, cnt);
+    const int* trow = Q.target_row + t0;
+    const int* tcol = Q.target_col + t0;
     const Ref BS_ = ref(B.S[l], (long long)KBr * KBc, KBr, OP_N);
-    DBuf V1(sz(nt, KAr, KBc), s), U1(sz(nt, Kr, KBc), s), U2(sz(nt, KAr, Kc), s);
-    segd(V1, KAr, KBc, nt, {Grp{ref(SB, (long long)KAr * KBr, KAr, OP_N), BS_, KBr, &Q.lyr, nullptr, nullptr}});
-    segd(U1, Kr, KBc, nt, {Grp{ref(LA[l], (long long)Kr * KBr, Kr, OP_N), BS_, KBr, &Q.lyn, nullptr, nullptr}});
-    segd(U2, KAr, Kc, nt,
-         {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(RB[l], (long long)KAc * Kc, KAc, OP_N), KAc, &Q.xr,
+    DBuf V1(sz(cnt, KAr, KBc), s), U1(sz(cnt, Kr, KBc), s), U2(sz(cnt, KAr, Kc), s);
+    segd(V1, KAr, KBc, cnt, {Grp{ref(SB, (long long)KAr * KBr, KAr, OP_N), BS_, KBr, &lyr, nullptr, nullptr}});
+    segd(U1, Kr, KBc, cnt, {Grp{ref(LA[l], (long long)Kr * KBr, Kr, OP_N), BS_, KBr, &lyn, nullptr, nullptr}});
+    segd(U2, KAr, Kc, cnt,
+         {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(RB[l], (long long)KAc * Kc, KAc, OP_N), KAc, &xr,
               nullptr, nullptr}});
     const Ref PBk = ref(PB[l], (long long)KBc * Kc, KBc, OP_N);
-    seg(U2, (long long)KAr * Kc, 0, KAr, nullptr, KAr, Kc, nt, true,
-        {Grp{ref(V1, (long long)KAr * KBc, KAr, OP_N), PBk, KBc, nullptr, nullptr, Q.target_col}});
+    seg(U2, (long long)KAr * Kc, 0, KAr, nullptr, KAr, Kc, cnt, true,
+        {Grp{ref(V1, (long long)KAr * KBc, KAr, OP_N), PBk, KBc, nullptr, nullptr, tcol}});
     V1.release();
-    Tg[l].alloc(sz(nt, Kr, Kc), s);
+    const long long os = (long long)Kr * Kc;
     const Grp gA{ref(PA[l], (long long)Kr * KAr, Kr, OP_N), ref(U2, (long long)KAr * Kc, KAr, OP_N), KAr, nullptr,
-                 Q.target_row, nullptr};
-    const Grp gB{ref(U1, (long long)Kr * KBc, Kr, OP_N), PBk, KBc, nullptr, nullptr, Q.target_col};
+                 trow, nullptr};
+    const Grp gB{ref(U1, (long long)Kr * KBc, Kr, OP_N), PBk, KBc, nullptr, nullptr, tcol};
     if (Z) {
-      segd(Tg[l], Kr, Kc, nt,
-           {gA, gB,
-            Grp{ref(*Z, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, &Q.mg, nullptr,
-                nullptr}});
+      const DevCsr mg = sub_csr(Q.mg, L.mg, t0, cnt);
+      seg(out, os, slot0 * os, Kr, nullptr, Kr, Kc, cnt, false,
+          {gA, gB,
+           Grp{ref(*Z, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, &mg, nullptr,
+               nullptr}});
     } else if (WA) {
-      segd(Tg[l], Kr, Kc, nt,
-           {gA, gB,
-            Grp{ref(*WA, (long long)Kr * NL, Kr, OP_N), ref(*WB, (long long)NL * Kc, NL, OP_N), NL, &Q.ww, nullptr,
-                nullptr}});
+      const DevCsr ww = sub_csr(Q.ww, L.ww, t0, cnt);
+      seg(out, os, slot0 * os, Kr, nullptr, Kr, Kc, cnt, false,
+          {gA, gB,
+           Grp{ref(*WA, (long long)Kr * NL, Kr, OP_N), ref(*WB, (long long)NL * Kc, NL, OP_N), NL, &ww, nullptr,
+               nullptr}});
     } else {
-      segd(Tg[l], Kr, Kc, nt, {gA, gB});
+      seg(out, os, slot0 * os, Kr, nullptr, Kr, Kc, cnt, false, {gA, gB});
     }
   }
 
@@ -1321,8 +1399,8 @@ struct EngineRun {
 
     mark("leaf.coupling_targets");
     targets(l, SB, &WA, &WB, nullptr, 0);
-    WA.release();
-    WB.release();
+    hold.push_back(std::move(WA));
+    hold.push_back(std::move(WB));
     // the auxiliary stream still reads these: release after the join
     hold.push_back(std::move(FV));
     hold.push_back(std::move(VF));
@@ -1385,12 +1463,14 @@ struct EngineRun {
     mark("L" + std::to_string(l) + ".assemble");
     // merged children couplings and assembled collected blocks (mmp.cpp:344-404)
     DBuf Mg, Aa, Ab;
-    gather(Mg, nm, Tg[l + 1].p + size_t(Lc.adm.size()) * Kn * Kq * W, (long long)Kn * Kq, Kn, Kq, Q.merged_quad);
-    compact_targets(l + 1);
+    gather(Mg, nm, Tp[l + 1].p, (long long)Kn * Kq, Kn, Kq, Q.merged_quad);
+    Tp[l + 1].release();
+    (void)Lc;
     gather(Aa, ns, LA[l + 1], (long long)Kn * KBr1, Kn, KBr1, Q.sub_child);
     gather(Ab, ns, RB[l + 1], (long long)KAc1 * Kq, KAc1, Kq, Q.sub_child);
-    LA[l + 1].release();
-    RB[l + 1].release();
+    // still read by level l+1's deferred targets: released after the join
+    hold.push_back(std::move(LA[l + 1]));
+    hold.push_back(std::move(RB[l + 1]));
 
     // X = asm_a T^B_row (row Gram term 2, collect); Xc = asm_b^T T^A_col
     DBuf X(sz(ns, 2 * Kn, KBr), s), Xc(sz(ns, 2 * Kq, KAc), s);
@@ -1479,8 +1559,8 @@ struct EngineRun {
       identity(PA[l], n, KAr, A.rr_d[l]);
       identity(PB[l], n, KBc, B.rc_d[l]);
     }
-    PA[l + 1].release();
-    PB[l + 1].release();
+    hold.push_back(std::move(PA[l + 1]));
+    hold.push_back(std::move(PB[l + 1]));
     Bp[l + 1].release();
     const int Kr = KCr[l], Kc = KCc[l];
 
@@ -1507,26 +1587,8 @@ struct EngineRun {
               nullptr}});
     Mg.release();
     targets(l, SB, nullptr, nullptr, &Z, Kq);
-  }
-
-  // Drop the pending part of a level's target store once the parent level has
-  // gathered it (mmp.cpp:344-365): keeps [admissible couplings | non-leaf
-  // couplings] and frees the (largest) pending slots early.
-  std::vector<char> compacted;
-  void compact_targets(int l) {
-    if (compacted.empty()) compacted.assign(D + 1, 0);
-    if (compacted[l]) return;
-    compacted[l] = 1;
-    const LevelPlan& L = P.lv[l];
-    const size_t one = size_t(KCr[l]) * KCc[l] * W;
-    const size_t na = L.adm.size(), np = L.pend_row.size(), nl = L.nl_block.size();
-    if (np == 0) return;
-    DBuf T(one * (na + nl), s);
-    if (na) CK(cudaMemcpyAsync(T.p, Tg[l].p, na * one * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    if (nl)
-      CK(cudaMemcpyAsync(T.p + na * one, Tg[l].p + (na + np) * one, nl * one * sizeof(double), cudaMemcpyDeviceToDevice,
-                         s));
-    Tg[l] = std::move(T);
+    hold.push_back(std::move(Z));
+    hold.push_back(std::move(SB));
   }
 
   // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------
@@ -1572,8 +1634,6 @@ struct EngineRun {
     basis_products();
     leaf_phase();
     for (int l = D - 1; l >= 1; --l) upper_level(l);
-    for (int l = std::max(1, D == 0 ? 0 : 1); l <= D; ++l) compact_targets(l);
-    if (D == 0) compact_targets(0);
     split();
     join();
   }
@@ -1874,8 +1934,13 @@ uint64_t structure_hash(const h2c_tree& t, const h2c_blocks& b) {
 
 Context::Context(int device) : device_(device) {
   CK(cudaSetDevice(device));
+  // the main (critical-path) stream gets the highest priority: its Gram /
+  // eigensolver / collect kernels take SM slots ahead of the deferred target
+  // sums queued on the low-priority auxiliary stream
+  int least = 0, greatest = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
   cudaStream_t st;
-  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, greatest));
   stream_ = st;
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -1893,6 +1958,52 @@ void* Context::solver() {
   return solver_;
 }
 
+// Auxiliary stream on a green context with H2B_AUX_SMS SMs (0 / unset or >= the
+// device's count: no partition, the default — on cfg2 the partition measured no
+// better than stream priorities alone, profiles/r01/ab_defer_partition.txt).
+// Returns nullptr when not partitioned.
+void* Context::make_aux_stream(int priority) {
+  int want = 0;
+  if (const char* e = std::getenv("H2B_AUX_SMS")) want = std::atoi(e);
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+  if (want <= 0 || want >= sms) return nullptr;
+  // driver entry points through the runtime (no link-time libcuda dependency:
+  // the library must load on hosts without a driver for the CPU test tier)
+  auto sym = [](const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError(std::string("driver entry point ") + name + " unavailable");
+    return fn;
+  };
+  auto cu = [](CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw CudaError(std::string(what) + " failed: CUresult " + std::to_string(int(r)));
+  };
+  const auto getDev = reinterpret_cast<decltype(&cuDeviceGet)>(sym("cuDeviceGet"));
+  const auto getRes = reinterpret_cast<decltype(&cuDeviceGetDevResource)>(sym("cuDeviceGetDevResource"));
+  const auto split = reinterpret_cast<decltype(&cuDevSmResourceSplitByCount)>(sym("cuDevSmResourceSplitByCount"));
+  const auto genDesc = reinterpret_cast<decltype(&cuDevResourceGenerateDesc)>(sym("cuDevResourceGenerateDesc"));
+  const auto gcCreate = reinterpret_cast<decltype(&cuGreenCtxCreate)>(sym("cuGreenCtxCreate"));
+  const auto gcStream = reinterpret_cast<decltype(&cuGreenCtxStreamCreate)>(sym("cuGreenCtxStreamCreate"));
+  green_destroy_ = sym("cuGreenCtxDestroy");
+  CUdevice dev;
+  cu(getDev(&dev, device_), "cuDeviceGet");
+  CUdevResource all, grp, rem;
+  cu(getRes(dev, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
+  unsigned nb = 1;
+  cu(split(&grp, &nb, &all, &rem, 0, static_cast<unsigned>(want)), "cuDevSmResourceSplitByCount");
+  CUdevResourceDesc desc;
+  cu(genDesc(&desc, &grp, 1), "cuDevResourceGenerateDesc");
+  CUgreenCtx g;
+  cu(gcCreate(&g, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+  green_ctx_ = g;
+  aux_sms_ = static_cast<int>(grp.sm.smCount);
+  CUstream st;
+  cu(gcStream(&st, g, CU_STREAM_NON_BLOCKING, priority), "cuGreenCtxStreamCreate");
+  return st;
+}
+
 void* Context::side_stream(int i) {
   side_solver(i);
   return side_streams_[i];
@@ -1900,9 +2011,11 @@ void* Context::side_stream(int i) {
 
 void* Context::side_solver(int i) {
   if (side_solvers_.empty()) {
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     for (int k = 0; k < kSideStreams; ++k) {
-      cudaStream_t st;
-      CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      cudaStream_t st = k == 0 ? static_cast<cudaStream_t>(make_aux_stream(least)) : nullptr;
+      if (!st) CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, k == 0 ? least : greatest));
       cusolverDnHandle_t h;
       if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
       cusolverDnSetStream(h, st);
@@ -1918,6 +2031,8 @@ Context::~Context() {
   delete static_cast<Arena*>(arena_);
   for (void* h : side_solvers_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(h));
   for (void* st : side_streams_) cudaStreamDestroy(static_cast<cudaStream_t>(st));
+  if (green_ctx_ && green_destroy_)
+    reinterpret_cast<decltype(&cuGreenCtxDestroy)>(green_destroy_)(static_cast<CUgreenCtx>(green_ctx_));
   if (solver_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_));
   dplan_.reset();
   if (stream_) {

@@ -87,11 +87,16 @@ class Context {
   int device() const { return device_; }
   void* solver();  // cusolverDn handle bound to the stream (lazy)
   struct Arena* arena();  // large-buffer arena of the main stream (lazy)
-  // side streams with their own cusolverDn handles: independent per-matrix
-  // eigensolves of one level run concurrently instead of back to back
-  static constexpr int kSideStreams = 16;
+  // side streams with their own cusolverDn handles.  0: auxiliary stream of
+  // the off-critical-path work (leaf full targets, deferred coupling-target
+  // sums) at low priority, optionally bound to a green context holding a
+  // subset of the SMs (H2B_AUX_SMS) so the critical path keeps SMs of its own;
+  // 1: the column eigensolve of a level, concurrent with the row one
+  static constexpr int kSideStreams = 2;
+  int aux_sms() const { return aux_sms_; }
   void* side_stream(int i);
   void* side_solver(int i);
+  void* make_aux_stream(int priority);
   int64_t last_kernel_launches() const { return launches_; }
   std::shared_ptr<PinnedPool> pinned = std::make_shared<PinnedPool>();
   // per (phase, kernel) timings of the last run, filled when profiling is on
@@ -106,6 +111,9 @@ class Context {
   void* arena_ = nullptr;
   bool arena_tried_ = false;
   std::vector<void*> side_streams_, side_solvers_;
+  void* green_ctx_ = nullptr;
+  void* green_destroy_ = nullptr;
+  int aux_sms_ = 0;  // SMs of the auxiliary stream's green context (0: whole device)
   std::string err_;
   uint64_t plan_key_ = 0;
   std::unique_ptr<Plan> plan_;

@@ -1,0 +1,35 @@
+"""A/B of engine knobs on one resident workload: build the operand once, then for
+each configuration (environment overrides) a fresh context, resident upload and
+`reps` products; prints the median device seconds per configuration.
+
+  python tools/ab.py N LEAF ORDER EPS 'label:VAR=v,VAR2=w' 'label2:...' ...
+"""
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1908_05218_b200 as P
+
+n, leaf, order, eps = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), float(sys.argv[4])
+reps = int(os.environ.get("AB_REPS", "3"))
+pts = P.random_cloud(n, 1)
+t = P.build_cluster_tree(pts, leaf)
+s = P.build_block_tree(t, t, 1.0)
+A = P.build_chebyshev(t, s, pts, order)
+KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_SEG_V2", "H2B_EIG_LIBRARY", "H2B_SEG_CFG")
+for spec in sys.argv[5:]:
+    label, _, kv = spec.partition(":")
+    for k in KNOBS:
+        os.environ.pop(k, None)
+    for item in filter(None, kv.split(",")):
+        k, v = item.split("=")
+        os.environ[k] = v
+    ctx = P.Context(0)
+    dA = P.ResidentOperand(A, ctx)
+    times = []
+    for _ in range(reps + 1):
+        secs, _ = P.mmp_resident(dA, dA, eps)
+        times.append(secs)
+    print(f"{label:24s} median {statistics.median(times[1:]):.4f} s  runs {[round(x, 4) for x in times]}", flush=True)
+    del dA, ctx
