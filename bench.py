@@ -12,6 +12,9 @@ seeded uniform points (reference RNG, geometry.cpp:39-52, seed 1), leaf size
   e2e   : same metric through the drop-in C-ABI call h2c_mmp with pinned host
           buffers (H2D of A, D2H of C inside the timed region).
 
+`--config cfg4` runs configs[3] instead: C = A*B on the 64^3 grid (N=262,144), A the
+7-point FD Laplacian in H^2 form, B the Laplace Chebyshev operand (k=64), eps 1e-6.
+
 `--impl reference` times the CPU oracle (a C++ restatement of the reference,
 whose Eigen build cannot be compiled here) on a bounded sample of the same
 workload with every host core running an independent product.
@@ -36,27 +39,48 @@ CONFIGS = {
     # name: (N, leaf, order, eps, description)
     "cfg1": (4096, 32, 3, 1e-6, "Laplace 1/(4 pi r), N=4096 cloud seed 1, leaf 32, eta 1, Chebyshev order 3 (k=27), eps 1e-6"),
     "cfg2": (65536, 64, 4, 1e-8, "Laplace 1/(4 pi r), N=65536 cloud seed 1, leaf 64, eta 1, Chebyshev order 4 (k=64), eps 1e-8"),
+    "cfg4": (262144, 64, 4, 1e-6, "C = A*B on the 64^3 grid (h = 1/65), leaf 64, eta 1: A = 7-point FD Laplacian "
+                                  "(6 / -1, exact near field, rank-1 degenerate far field), B = Laplace 1/(4 pi r) "
+                                  "Chebyshev order 4 (k=64), eps 1e-6"),
+    # configs[3]'s construction on the 48^3 grid: the 64^3 product's live pending couplings alone
+    # (two consecutive levels, ~125 GB) exceed one B200's HBM next to A, B and C
+    "cfg4s": (110592, 64, 4, 1e-6, "configs[3] construction on the 48^3 grid (h = 1/49): C = A*B, A = 7-point FD "
+                                   "Laplacian, B = Laplace Chebyshev order 4 (k=64), leaf 64, eta 1, eps 1e-6"),
 }
 # bounded CPU sample of the same construction (oracle single-thread ~10-30 s)
-CPU_SAMPLE = {"cfg1": 4096, "cfg2": 4096}
+CPU_SAMPLE = {"cfg1": 4096, "cfg2": 4096, "cfg4": 4096, "cfg4s": 4096}
 
 
-def build_workload(name: str):
+def grid_points(m: int) -> tuple[np.ndarray, float]:
+    """m^3 interior grid of the unit cube, h = 1/(m+1)."""
+    h = 1.0 / (m + 1)
+    g = np.stack(np.meshgrid(*[np.arange(1, m + 1) * h] * 3, indexing="ij"), -1).reshape(-1, 3)
+    return np.ascontiguousarray(g), h
+
+
+def build_operands(name: str, n: int):
+    """(points, tree, structure, A, B) of configuration `name` at N = n points (B is A for C = A*A)."""
     import paper_1908_05218_b200 as P
-    n, leaf, order, eps, desc = CONFIGS[name]
-    pts = points_for(n)
-    t0 = time.perf_counter()
+    _, leaf, order, _, _ = CONFIGS[name]
+    if name in ("cfg4", "cfg4s"):
+        m = round(n ** (1.0 / 3.0))
+        pts, h = grid_points(m)
+        tree = P.build_cluster_tree(pts, leaf)
+        st = P.build_block_tree(tree, tree, 1.0)
+        return pts, tree, st, P.build_fd_laplacian(tree, st, pts, h), P.build_chebyshev(tree, st, pts, order)
+    pts = P.random_cloud(n, 1)  # make_random_cloud (geometry.cpp:39-52)
     tree = P.build_cluster_tree(pts, leaf)
     st = P.build_block_tree(tree, tree, 1.0)
     A = P.build_chebyshev(tree, st, pts, order)
-    return dict(name=name, points=pts, tree=tree, structure=st, A=A, eps=eps, desc=desc,
+    return pts, tree, st, A, A
+
+
+def build_workload(name: str):
+    n, leaf, order, eps, desc = CONFIGS[name]
+    t0 = time.perf_counter()
+    pts, tree, st, A, B = build_operands(name, n)
+    return dict(name=name, points=pts, tree=tree, structure=st, A=A, B=B, eps=eps, desc=desc,
                 build_seconds=time.perf_counter() - t0, n=n, leaf=leaf, order=order)
-
-
-def points_for(n: int) -> np.ndarray:
-    """make_random_cloud (geometry.cpp:39-52) through the product library."""
-    import paper_1908_05218_b200 as P
-    return P.random_cloud(n, 1)
 
 
 # ---------------------------------------------------------------------------
@@ -121,12 +145,9 @@ def cpu_sample(name: str, threads_note: int = 1) -> dict:
     import paper_1908_05218_b200 as P
     n_full, leaf, order, eps, _ = CONFIGS[name]
     n = CPU_SAMPLE[name]
-    pts = P.random_cloud(n, 1)
-    tree = P.build_cluster_tree(pts, leaf)
-    st = P.build_block_tree(tree, tree, 1.0)
-    A = P.build_chebyshev(tree, st, pts, order)
+    _, _, _, A, B = build_operands(name, n)
     t0 = time.perf_counter()
-    r = O.mmp(A, A, eps)
+    r = O.mmp(A, B, eps)
     dt = time.perf_counter() - t0
     return {"gflops": 2.0 * r.report.flops / dt / 1e9, "seconds": dt, "flops": r.report.flops, "n": n,
             "wall_seconds_report": r.report.wall_seconds}
@@ -207,14 +228,15 @@ def run_b200(args) -> None:
         torch.cuda.set_device(local)
 
     W = build_workload(args.config)
-    A, eps = W["A"], W["eps"]
+    A, B, eps = W["A"], W["B"], W["eps"]
     ctx = P.Context(local)
     dA = P.ResidentOperand(A, ctx)
+    dB = dA if B is A else P.ResidentOperand(B, ctx)
 
     # one product with report (counters, exec MACs) + warm-up
-    _, rep = P.mmp_resident(dA, dA, eps, want_report=True)
+    _, rep = P.mmp_resident(dA, dB, eps, want_report=True)
     for _ in range(max(0, args.warmup - 1)):
-        P.mmp_resident(dA, dA, eps)
+        P.mmp_resident(dA, dB, eps)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -225,7 +247,7 @@ def run_b200(args) -> None:
     with ClockSampler(local) as clocks:
         e0.record(stream)
         for _ in range(args.steps):
-            P.mmp_resident(dA, dA, eps)
+            P.mmp_resident(dA, dB, eps)
             launches += ctx.kernel_launches()
         e1.record(stream)
         torch.cuda.synchronize()
@@ -237,7 +259,7 @@ def run_b200(args) -> None:
 
     # roofline of the dominant kernel: one profiled (untimed) product
     ctx.set_profile(True)
-    P.mmp_resident(dA, dA, eps)
+    P.mmp_resident(dA, dB, eps)
     prof_all = ctx.profile()
     ctx.set_profile(False)
     prof = [e for e in prof_all if not e["name"].startswith(("wall:", "host:"))]
@@ -256,14 +278,16 @@ def run_b200(args) -> None:
                     "pipeline_frac": round(2.0 * rep.flops_exec / (ms * 1e-3) / 1e12 / peak, 4)}
 
     # end-to-end through the drop-in C-ABI call with pinned host buffers
+    del dA, dB
     Ap, _pin = P.pin_matrix(A)
-    P.mmp(Ap, Ap, eps, ctx)  # warm (plan cached, pool warm)
+    Bp, _pinb = (Ap, None) if B is A else P.pin_matrix(B)
+    P.mmp(Ap, Bp, eps, ctx)  # warm (plan cached, pool warm)
     e2e_times = []
     h2d = d2h = 0
     for _ in range(max(1, min(args.steps, 3))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = P.mmp(Ap, Ap, eps, ctx)
+        res = P.mmp(Ap, Bp, eps, ctx)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
         h2d, d2h = res.report.h2d_bytes, res.report.d2h_bytes
@@ -286,7 +310,7 @@ def run_b200(args) -> None:
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": W["desc"], "N": W["n"], "eps": eps,
                        "flops_per_step": int(rep.flops), "flops_exec_per_step": int(rep.flops_exec),
-                       "max_rank": rep.max_rank(), "l2": "inputs (%.1f GB) >> 126 MB L2" % (A.values.nbytes / 1e9),
+                       "max_rank": rep.max_rank(), "l2": "inputs (%.1f GB) >> 126 MB L2" % ((A.values.nbytes + (0 if B is A else B.values.nbytes)) / 1e9),
                        "parallelism": f"replicas{world}"},
             "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "seconds": round(e2e_s, 4)},

@@ -111,6 +111,11 @@ int h2c_truncate_gram(h2c_context* ctx, int scalar, const double* gram, int n, d
  * (metrics.cpp:37-55) at sizes where a dense check is impossible. */
 int h2c_mvp(h2c_context* ctx, const h2c_matrix* a, const double* x, int nv, double* y);
 int h2c_mvp_resident(h2c_context* ctx, const h2c_operand* a, const double* x, int nv, double* y);
+/* ---- h2_to_dense on the device (h2_matrix.cpp:124-137) -------------------
+ * out = A as a dense N x N column-major matrix in the ORIGINAL point ordering
+ * (complex interleaved), computed as A * I through the device MVP in column
+ * panels of unit vectors generated on the device (N <= 32768). */
+int h2c_to_dense(h2c_context* ctx, const h2c_matrix* a, double* out);
 /* random_vector (metrics.cpp:11-35): U[-1,1] from std::mt19937_64(seed), 53-bit
  * mantissas; complex draws re then im. */
 int h2c_random_vector(int n, uint64_t seed, int scalar, double* out);

@@ -202,6 +202,16 @@ def mvp(a: H2Matrix, x: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray
     return y
 
 
+def h2_to_dense(a: H2Matrix, ctx: Optional[Context] = None) -> np.ndarray:
+    """Dense N x N materialisation on the B200 (h2_matrix.cpp:124-137), original point ordering."""
+    ctx = ctx or default_context()
+    n = a.size()
+    out = np.zeros((n, n), dtype=a.dtype, order="F")
+    rc = h2c.lib().h2c_to_dense(ctx.handle, C.byref(a.desc()), out.ctypes.data_as(h2c.P_f64))
+    raise_for(rc, h2c.last_error(ctx.handle))
+    return out
+
+
 def relative_error(a: H2Matrix, b: H2Matrix, c: H2Matrix, seed: int, ctx: Optional[Context] = None) -> float:
     """||C x - A (B x)|| / ||A (B x)|| with x = random_vector(seed) (metrics.cpp:37-55), on the B200."""
     if not (a.tree is b.tree is c.tree):

@@ -341,6 +341,14 @@ int h2c_mvp(h2c_context* ctx, const h2c_matrix* a, const double* x, int nv, doub
   });
 }
 
+int h2c_to_dense(h2c_context* ctx, const h2c_matrix* a, double* out) {
+  if (!ctx) return H2C_ERR_CUDA;
+  return guarded(ctx, [&] {
+    auto op = ctx->ctx->upload(*a);
+    ctx->ctx->to_dense(op, out);
+  });
+}
+
 int h2c_random_vector(int n, uint64_t seed, int scalar, double* out) {
   if (n < 0) {
     g_err = "random_vector: negative length";

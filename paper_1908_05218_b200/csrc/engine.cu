@@ -91,6 +91,7 @@ class Arena {
   void* alloc(size_t bytes) {
     bytes = (bytes + 255) & ~size_t(255);
     std::lock_guard<std::mutex> g(mu_);
+    reclaim_locked(false);
     auto best = free_.end();
     for (auto it = free_.begin(); it != free_.end(); ++it)
       if (it->second >= bytes && (best == free_.end() || it->second < best->second)) best = it;
@@ -101,11 +102,56 @@ class Arena {
     used_[off] = bytes;
     return static_cast<char*>(base_) + off;
   }
+  // (total free bytes, largest free block)
+  std::pair<size_t, size_t> stats() {
+    std::lock_guard<std::mutex> g(mu_);
+    size_t tot = 0, big = 0;
+    for (auto& kv : free_) {
+      tot += kv.second;
+      big = std::max(big, kv.second);
+    }
+    return {tot, big};
+  }
+  size_t capacity() const { return cap_; }
   bool owns(const void* p) const {
     return base_ && p >= base_ && p < static_cast<const char*>(base_) + cap_;
   }
   void free(void* p) {
     std::lock_guard<std::mutex> g(mu_);
+    free_locked(p);
+  }
+  // A block last used on another stream (the auxiliary stream) returns to the
+  // free list only once `ev`, recorded there after its last use, has completed
+  // (checked on later allocations) or after the main stream has joined it.
+  void free_after(void* p, cudaEvent_t ev) {
+    std::lock_guard<std::mutex> g(mu_);
+    pending_.push_back({p, ev});
+  }
+  bool has_pending() {
+    std::lock_guard<std::mutex> g(mu_);
+    return !pending_.empty();
+  }
+  // all_done: the main stream has waited for everything issued on the other streams
+  void reclaim(bool all_done) {
+    std::lock_guard<std::mutex> g(mu_);
+    reclaim_locked(all_done);
+  }
+
+ private:
+  void reclaim_locked(bool all_done) {
+    size_t k = 0;
+    for (size_t i = 0; i < pending_.size(); ++i) {
+      if (all_done || cudaEventQuery(pending_[i].second) == cudaSuccess) {
+        free_locked(pending_[i].first);
+        cudaEventDestroy(pending_[i].second);
+      } else {
+        pending_[k++] = pending_[i];
+      }
+    }
+    pending_.resize(k);
+    cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not sticky, but clear it
+  }
+  void free_locked(void* p) {
     size_t off = static_cast<char*>(p) - static_cast<char*>(base_);
     auto u = used_.find(off);
     if (u == used_.end()) return;
@@ -126,23 +172,30 @@ class Arena {
     free_[off] = sz;
   }
 
- private:
   void* base_ = nullptr;
   size_t cap_ = 0;
   std::map<size_t, size_t> free_, used_;
+  std::vector<std::pair<void*, cudaEvent_t>> pending_;
   std::mutex mu_;
 };
 
 // the arena of the context running on this thread, and its main stream
 thread_local Arena* t_arena = nullptr;
 thread_local cudaStream_t t_arena_stream = nullptr;
+// the auxiliary stream of the run on this thread: its buffers also come from the
+// arena and are returned through Arena::free_after
+thread_local cudaStream_t t_aux_stream = nullptr;
 constexpr size_t kArenaMin = size_t(8) << 20;
+// per-buffer scratch bound of the chunked target / full-block / case-1 loops:
+// one chunk per level at cfg2, bounded scratch at the larger configurations
+constexpr size_t kChunkBytes = size_t(8) << 30;
 
 struct DBuf {
   double* p = nullptr;
   size_t n = 0;  // doubles
   cudaStream_t s = nullptr;
   Arena* arena = nullptr;
+  bool aux = false;  // arena block used on the auxiliary stream
   DBuf() = default;
   DBuf(size_t doubles, cudaStream_t st, bool zero = false) { alloc(doubles, st, zero); }
   DBuf(const DBuf&) = delete;
@@ -155,6 +208,7 @@ struct DBuf {
       n = o.n;
       s = o.s;
       arena = o.arena;
+      aux = o.aux;
       o.p = nullptr;
       o.n = 0;
       o.arena = nullptr;
@@ -165,21 +219,53 @@ struct DBuf {
     release();
     s = st;
     n = std::max<size_t>(doubles, 2);
-    if (t_arena && st == t_arena_stream && n * sizeof(double) >= kArenaMin) {
+    if (t_arena && (st == t_arena_stream || (st && st == t_aux_stream)) && n * sizeof(double) >= kArenaMin) {
       p = static_cast<double*>(t_arena->alloc(n * sizeof(double)));
-      if (p) arena = t_arena;
+      if (!p && t_aux_stream && t_arena->has_pending()) {
+        // memory pressure: let the deferred work drain, reclaim its blocks, retry
+        CK(cudaStreamSynchronize(t_aux_stream));
+        t_arena->reclaim(false);
+        p = static_cast<double*>(t_arena->alloc(n * sizeof(double)));
+      }
+      if (p) {
+        arena = t_arena;
+        aux = st != t_arena_stream;
+      }
     }
-    if (!p) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(double), s));
+    if (!p) {
+      const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(double), s);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        std::string msg = "device allocation of " + std::to_string(n * sizeof(double) >> 20) + " MiB failed (" +
+                          cudaGetErrorString(e) + ")";
+        if (t_arena) {
+          const auto st = t_arena->stats();
+          msg += "; arena " + std::to_string(t_arena->capacity() >> 20) + " MiB, free " + std::to_string(st.first >> 20) +
+                 " MiB, largest free block " + std::to_string(st.second >> 20) + " MiB";
+        }
+        throw CudaError(msg);
+      }
+    }
     if (zero) CK(cudaMemsetAsync(p, 0, n * sizeof(double), s));
   }
   void release() {
     if (p) {
-      if (arena) arena->free(p);
-      else cudaFreeAsync(p, s);
+      if (arena && aux) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, s));
+        arena->free_after(p, ev);
+      } else if (arena) {
+        arena->free(p);
+      } else {
+        cudaFreeAsync(p, s);
+      }
     }
     p = nullptr;
     n = 0;
     arena = nullptr;
+    aux = false;
   }
   ~DBuf() { release(); }
   operator double*() const { return p; }
@@ -242,6 +328,11 @@ struct DevLevel {
   const int *near_row = nullptr, *near_col = nullptr, *adm_row = nullptr, *adm_col = nullptr;
   const int *nearb = nullptr, *adm = nullptr, *merged_row = nullptr, *merged_quad = nullptr;
   const int *sub_child = nullptr, *nl_col = nullptr;
+  const int* pend_mq = nullptr;  // pending target -> 4 * merged idx (level-1) + quadrant
+  struct MZ {
+    const int *row = nullptr, *col = nullptr, *m = nullptr, *out = nullptr;
+    int n = 0;
+  } mz_adm, mz_pend;  // LevelPlan::MergedInto
   // split from this level into level+1, per quadrant
   const int *sp_src[4] = {}, *sp_prow[4] = {}, *sp_omap[4] = {};
   int sp_n[4] = {0, 0, 0, 0};
@@ -313,6 +404,16 @@ static std::unique_ptr<DevPlan> upload_plan(const Plan& P, cudaStream_t s) {
     put(&Q.adm, L.adm);
     put(&Q.merged_row, L.merged_row);
     put(&Q.merged_quad, L.merged_quad);
+    put(&Q.pend_mq, L.pend_mq);
+    auto put_mz = [&](DevLevel::MZ& d, const LevelPlan::MergedInto& z) {
+      put(&d.row, z.row);
+      put(&d.col, z.col);
+      put(&d.m, z.m);
+      put(&d.out, z.out);
+      d.n = static_cast<int>(z.m.size());
+    };
+    put_mz(Q.mz_adm, L.mz_adm);
+    put_mz(Q.mz_pend, L.mz_pend);
     put(&Q.sub_child, L.sub_child);
     put(&Q.nl_col, nlc);
     {
@@ -575,8 +676,16 @@ struct EngineRun {
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
   std::chrono::steady_clock::time_point host_t0 = std::chrono::steady_clock::now();
   std::vector<std::pair<std::string, double>> host_marks;
+  const bool mem_trace = std::getenv("H2B_MEM_TRACE") != nullptr;
   void mark(const std::string& name) {
     phase = name;
+    if (mem_trace && t_arena) {
+      const auto st = t_arena->stats();
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      std::fprintf(stderr, "[mem] %-24s arena free %7zu MiB (largest %7zu MiB) of %7zu MiB; device free %7zu MiB\n",
+                   name.c_str(), st.first >> 20, st.second >> 20, t_arena->capacity() >> 20, fr >> 20);
+    }
     if (profiling)
       host_marks.push_back({name, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count()});
     if (!profiling) return;
@@ -605,26 +714,54 @@ struct EngineRun {
   std::vector<std::vector<int64_t>> rcr, rcc;
   std::vector<DVec<uint8_t>> dgr, dgc;
   DBuf Vr, Vc, F;
-  std::vector<DBuf> Tr, Tc, Tg, Tp;  // Tg: [adm | NL] targets, Tp: pending targets
+  // Tg: [adm | NL] coupling targets per level; Mg[l]: merged 2x2 blocks of level l,
+  // written directly by level l+1's pending targets (mmp.cpp:344-365)
+  std::vector<DBuf> Tr, Tc, Tg, Mg;
   // H2B_NO_DEFER=1: admissible / NL targets on the main stream (A/B runs)
-  const bool defer_targets = std::getenv("H2B_NO_DEFER") == nullptr;
+  const bool no_defer_env = std::getenv("H2B_NO_DEFER") != nullptr;
+  bool defer_targets = true;  // set in run(): off when profiling or H2B_NO_DEFER
   // per-level intermediates
   std::vector<DBuf> Bp, PA, PB, LA, RB;
   // auxiliary stream for the C-independent leaf full targets
-  cudaStream_t s_aux = nullptr;
+  cudaStream_t s_aux = nullptr, prev_aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_full = nullptr;
-  bool joined = false;
+  bool joined = true;  // nothing queued on the auxiliary stream yet
   std::vector<DBuf> hold;
+  // A main-stream buffer the main stream no longer needs but deferred work on
+  // the auxiliary stream (all of it already issued) may still read: an arena
+  // block returns to the free list once the auxiliary stream passes this point
+  // (main-stream reuse is ordered by the stream, auxiliary reuse by the next
+  // fork); anything else waits for join().
+  void retire(DBuf&& x) {
+    if (!x.p) return;
+    if (joined) {
+      x.release();
+      return;
+    }
+    if (x.arena && !x.aux) {
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev, s_aux));
+      x.arena->free_after(x.p, ev);
+      x.p = nullptr;
+      x.n = 0;
+      x.arena = nullptr;
+      return;
+    }
+    hold.push_back(std::move(x));
+  }
   void join() {
     if (joined) return;
     CK(cudaEventRecord(ev_full, s_aux));  // everything queued on the auxiliary stream so far
     CK(cudaStreamWaitEvent(s, ev_full, 0));
+    if (t_arena) t_arena->reclaim(true);
     hold.clear();  // frees on the main stream, ordered after the join
     joined = true;
   }
   ~EngineRun() {
     // deferred work may still read held buffers (error paths): drain it first
     if (s_aux) cudaStreamSynchronize(s_aux);
+    t_aux_stream = prev_aux;
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_full) cudaEventDestroy(ev_full);
   }
@@ -645,13 +782,15 @@ struct EngineRun {
     Tr.resize(D + 1);
     Tc.resize(D + 1);
     Tg.resize(D + 1);
-    Tp.resize(D + 1);
+    Mg.resize(D + 1);
     Bp.resize(D + 1);
     PA.resize(D + 1);
     PB.resize(D + 1);
     LA.resize(D + 2);
     RB.resize(D + 2);
     s_aux = static_cast<cudaStream_t>(c.side_stream(0));
+    prev_aux = t_aux_stream;
+    t_aux_stream = s_aux;
     CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_full, cudaEventDisableTiming));
   }
@@ -739,10 +878,20 @@ struct EngineRun {
     launches++;
   }
 
+  // one-shot quadrant scatter for the next seg() (see SegParams::oquad)
+  struct Quad {
+    const int* mq = nullptr;
+    int qm = 0, qn = 0;
+  } quad;
   void seg(double* out, long long Os, long long Ooff, int Old, const int* omap, int M, int N, int n_out,
            bool acc, std::initializer_list<Grp> gs, bool sym = false) {
+    const Quad qd = quad;
+    quad = Quad{};
     if (n_out <= 0) return;
     SegParams sp{};
+    sp.oquad = qd.mq;
+    sp.qm = qd.qm;
+    sp.qn = qd.qn;
     sp.sym = sym ? 1 : 0;
     sp.out = out;
     sp.Os = Os;
@@ -961,58 +1110,79 @@ struct EngineRun {
   // Runs a deferred library eigensolve on side stream 1 in a host thread, so
   // the row and column eigensolves of a level overlap (cuSOLVER's batched
   // solver is launch-latency bound).
-  std::thread solve_async(Trunc& t, std::exception_ptr& err) {
+  // Library eigensolver buffers, allocated on the calling (main) thread from the
+  // main-stream arena so a solve on a side stream never needs pool memory
+  // outside it; released on the main thread after the solve has completed.
+  struct EigWork {
+    DBuf V, w, work;
+    DVec<int> info;
+    size_t dev_bytes = 0, host_bytes = 0;
+  };
+  static void cusolver_check(cusolverStatus_t st, const char* what) {
+    if (st != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string("cuSOLVER ") + what + " failed: " + std::to_string(int(st)));
+  }
+  void prepare_eig(EigWork& wk, int count, int n, cusolverDnHandle_t h) {
+    wk.V.alloc(sz(count, n, n), s);
+    wk.w.alloc(size_t(count) * n, s);
+    wk.info.alloc(count, s);
+    const cudaDataType dt = cplx ? CUDA_C_64F : CUDA_R_64F;
+    cusolver_check(cusolverDnXsyevBatched_bufferSize(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt,
+                                                     wk.V.p, n, CUDA_R_64F, wk.w.p, dt, &wk.dev_bytes, &wk.host_bytes,
+                                                     count),
+                   "syevBatched_bufferSize");
+    wk.work.alloc(wk.dev_bytes / sizeof(double) + 2, s);
+  }
+
+  // Runs a deferred library eigensolve on side stream 1 in a host thread, so
+  // the row and column eigensolves of a level overlap (cuSOLVER's batched
+  // solver is launch-latency bound).
+  std::thread solve_async(Trunc& t, EigWork& wk, std::exception_ptr& err) {
     if (!t.G.p) return std::thread();
     cudaStream_t st = static_cast<cudaStream_t>(ctx.side_stream(1));
     cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.side_solver(1));
+    prepare_eig(wk, t.count, t.n, h);
     CK(cudaEventRecord(ev_fork, s));
     CK(cudaStreamWaitEvent(st, ev_fork, 0));
     CK(cudaSetDevice(ctx.device()));
-    return std::thread([this, &t, &err, st, h] {
+    return std::thread([this, &t, &wk, &err, st, h] {
       try {
         CK(cudaSetDevice(ctx.device()));
-        library_eig_on(t.G, t.count, t.n, t, st, h);
+        library_eig_on(t.G, t.count, t.n, t, st, h, wk);
       } catch (...) {
         err = std::current_exception();
       }
     });
   }
-  void finish_async(std::thread& th, std::exception_ptr& err, Trunc& t) {
-    if (th.joinable()) th.join();
+  void finish_async(std::thread& th, std::exception_ptr& err, Trunc& t, EigWork& wk) {
+    if (th.joinable()) th.join();  // the solve ended with a synchronize of its stream
     if (err) std::rethrow_exception(err);
     t.G.release();
+    wk = EigWork{};
   }
 
   // Gram dimensions beyond the shared-memory Jacobi (upper levels, where C's
   // ranks grow): batched Hermitian eigensolver from cuSOLVER, then the same
   // truncation rule on the device.
   void library_eig(const DBuf& G, int count, int n, Trunc& t) {
-    library_eig_on(G, count, n, t, s, static_cast<cusolverDnHandle_t>(ctx.solver()));
+    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.solver());
+    EigWork wk;
+    prepare_eig(wk, count, n, h);
+    library_eig_on(G, count, n, t, s, h, wk);
   }
-  void library_eig_on(const DBuf& G, int count, int n, Trunc& t, cudaStream_t s, cusolverDnHandle_t h) {
+  void library_eig_on(const DBuf& G, int count, int n, Trunc& t, cudaStream_t s, cusolverDnHandle_t h, EigWork& wk) {
     const bool main_thread = s == this->s;
-    DBuf V(sz(count, n, n), s), w(size_t(count) * n, s);
-    CK(cudaMemcpyAsync(V.p, G.p, sz(count, n, n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(wk.V.p, G.p, sz(count, n, n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
     const cudaDataType dt = cplx ? CUDA_C_64F : CUDA_R_64F;
-    size_t dev_bytes = 0, host_bytes = 0;
-    auto chk = [](cusolverStatus_t st, const char* what) {
-      if (st != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string("cuSOLVER ") + what + " failed: " + std::to_string(int(st)));
-    };
-    DVec<int> info;
-    info.alloc(count, s);
     if (main_thread) pre("syev_batched", 0);
     {
-      chk(cusolverDnXsyevBatched_bufferSize(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p,
-                                            n, CUDA_R_64F, w.p, dt, &dev_bytes, &host_bytes, count),
-          "syevBatched_bufferSize");
-      DBuf work(dev_bytes / sizeof(double) + 2, s);
-      std::vector<char> hwork(host_bytes + 1);
-      chk(cusolverDnXsyevBatched(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, V.p, n,
-                                 CUDA_R_64F, w.p, dt, work.p, dev_bytes, hwork.data(), host_bytes, info.p, count),
-          "syevBatched");
+      std::vector<char> hwork(wk.host_bytes + 1);
+      cusolver_check(cusolverDnXsyevBatched(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, wk.V.p,
+                                            n, CUDA_R_64F, wk.w.p, dt, wk.work.p, wk.dev_bytes, hwork.data(),
+                                            wk.host_bytes, wk.info.p, count),
+                     "syevBatched");
       CK(cudaStreamSynchronize(s));  // host workspace lifetime
       std::vector<int> hinfo(count);
-      CK(cudaMemcpy(hinfo.data(), info.p, count * sizeof(int), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(hinfo.data(), wk.info.p, count * sizeof(int), cudaMemcpyDeviceToHost));
       for (int b = 0; b < count; ++b)
         if (hinfo[b] != 0)
           throw std::logic_error("svd_truncate_gram: eigendecomposition failed (syev info " + std::to_string(hinfo[b]) + ")");
@@ -1020,13 +1190,13 @@ struct EngineRun {
     if (main_thread) post();  // library kernels are not counted in `launches`
     if (main_thread) pre("eig_finalize", 0);
     if (cplx)
-      eig_finalize_kernel<true><<<count, 256, 0, s>>>(G, V, w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
+      eig_finalize_kernel<true><<<count, 256, 0, s>>>(G, wk.V, wk.w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
     else
-      eig_finalize_kernel<false><<<count, 256, 0, s>>>(G, V, w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
+      eig_finalize_kernel<false><<<count, 256, 0, s>>>(G, wk.V, wk.w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
     CK(cudaGetLastError());
     if (main_thread) post();
     launches++;
-    CK(cudaStreamSynchronize(s));  // host workspace lifetime
+    CK(cudaStreamSynchronize(s));  // the buffers are released by the main thread after this
   }
   double jp_eps() const { return adaptive ? eps : 0.5; }
 
@@ -1185,23 +1355,76 @@ struct EngineRun {
   // by split() and the download, so they run on the low-priority auxiliary
   // stream into the compact store Tg[l] = [adm | NL], overlapping the parent
   // levels' Gram / eigensolver / collect chain.
-  void targets(int l, const DBuf& SB, const DBuf* WA, const DBuf* WB, const DBuf* Z, int Kq) {
+  // output stores of level l's targets: Tg[l] = [adm | NL] and, for pending
+  // targets, the parent's merged blocks Mg[l-1] (zero where a quadrant has no
+  // child).  zero_tg: the targets accumulate onto case-1 values written first.
+  void alloc_targets(int l, bool zero_tg) {
     const LevelPlan& L = P.lv[l];
     const int na = static_cast<int>(L.adm.size()), np = static_cast<int>(L.pend_row.size());
     const int nl = static_cast<int>(L.nl_block.size());
     const int Kr = KCr[l], Kc = KCc[l];
-    Tp[l].alloc(sz(np, Kr, Kc), s);
-    targets_range(l, na, np, Tp[l], 0, SB, WA, WB, Z, Kq);
-    Tg[l].alloc(sz(na + nl, Kr, Kc), s);
-    if (!defer_targets) {
-      targets_range(l, 0, na, Tg[l], 0, SB, WA, WB, Z, Kq);
-      targets_range(l, na + np, nl, Tg[l], na, SB, WA, WB, Z, Kq);
-      return;
+    if (np > 0) {
+      const int nm = static_cast<int>(P.lv[l - 1].merged_row.size());
+      Mg[l - 1].alloc(sz(nm, 2 * Kr, 2 * Kc), s, true);
     }
-    on_aux(phase + "_deferred", [&] {
-      targets_range(l, 0, na, Tg[l], 0, SB, WA, WB, Z, Kq);
-      targets_range(l, na + np, nl, Tg[l], na, SB, WA, WB, Z, Kq);
-    });
+    Tg[l].alloc(sz(na + nl, Kr, Kc), s, zero_tg);
+  }
+
+  // case 1 of the upper levels (mmp.cpp:573-585): T^C_i^H M conj(T^C_k) of every
+  // merged block, written into its (admissible or pending) target before the
+  // triple sums accumulate onto it; in chunks (Zc = T^C_i^H M scratch)
+  void merged_into_targets(int l, const DBuf& M) {
+    const DevLevel& Q = DP.lv[l];
+    const int Kn = KCr[l + 1], Kq = KCc[l + 1], Kr = KCr[l], Kc = KCc[l];
+    const long long MM = 4LL * Kn * Kq;
+    for (int pend = 0; pend < 2; ++pend) {
+      const DevLevel::MZ& z = pend ? Q.mz_pend : Q.mz_adm;
+      if (z.n == 0) continue;
+      const size_t per = sz(1, Kr, 2 * Kq) * sizeof(double);
+      const int step = static_cast<int>(std::max<size_t>(4096, kChunkBytes / per));
+      for (int e0 = 0; e0 < z.n; e0 += step) {
+        const int cnt = std::min(step, z.n - e0);
+        DBuf Zc(sz(cnt, Kr, 2 * Kq), s);
+        segd(Zc, Kr, 2 * Kq, cnt,
+             {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), ref(M, MM, 2 * Kn, OP_N), 2 * Kn, nullptr, z.row + e0,
+                  z.m + e0}});
+        const Grp g{ref(Zc, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, nullptr, nullptr,
+                    z.col + e0};
+        if (pend) {
+          quad = {z.out + e0, Kr, Kc};
+          seg(Mg[l - 1], 4LL * Kr * Kc, 0, 2 * Kr, nullptr, Kr, Kc, cnt, false, {g});
+        } else {
+          seg(Tg[l], (long long)Kr * Kc, 0, Kr, z.out + e0, Kr, Kc, cnt, false, {g});
+        }
+      }
+    }
+  }
+
+  // acc: accumulate onto the stores (upper levels, after merged_into_targets)
+  void targets(int l, const DBuf& SB, const DBuf* WA, const DBuf* WB, bool acc) {
+    const LevelPlan& L = P.lv[l];
+    const DevLevel& Q = DP.lv[l];
+    const int na = static_cast<int>(L.adm.size()), np = static_cast<int>(L.pend_row.size());
+    const int nl = static_cast<int>(L.nl_block.size());
+    if (np > 0)  // pending targets straight into the parent's merged blocks (critical path)
+      chunks(l, na, np, [&](int t0, int cnt) {
+        targets_range(l, t0, cnt, Mg[l - 1], 0, SB, WA, WB, acc, Q.pend_mq + (t0 - na));
+      });
+    auto rest = [&] {
+      chunks(l, 0, na, [&](int t0, int cnt) { targets_range(l, t0, cnt, Tg[l], t0, SB, WA, WB, acc); });
+      chunks(l, na + np, nl, [&](int t0, int cnt) { targets_range(l, t0, cnt, Tg[l], t0 - np, SB, WA, WB, acc); });
+    };
+    if (!defer_targets) rest();  // (profiling runs serialise: clean per-kernel timings)
+    else on_aux(phase + "_deferred", rest);
+  }
+
+  // target ranges in chunks that bound the per-target scratch (V1, U1, U2) to kChunkBytes each
+  template <class Fn>
+  void chunks(int l, int t0, int cnt, Fn&& fn) {
+    const size_t per = size_t(W) * sizeof(double) *
+                       std::max({size_t(A.Kr[l]) * B.Kc[l], size_t(KCr[l]) * B.Kc[l], size_t(A.Kr[l]) * KCc[l]});
+    const int step = static_cast<int>(std::max<size_t>(4096, kChunkBytes / std::max<size_t>(per, 1)));
+    for (int c = 0; c < cnt; c += step) fn(t0 + c, std::min(step, cnt - c));
   }
 
   // run `fn` on the auxiliary stream, ordered after everything issued so far on
@@ -1209,6 +1432,13 @@ struct EngineRun {
   // stream, main-stream inputs it reads must stay in `hold` until join().
   template <class Fn>
   void on_aux(const std::string& ph, Fn&& fn) {
+    if (profiling) {  // profiled runs are serial: per-kernel event times without overlap
+      const std::string keep_phase = phase;
+      phase = ph;
+      fn();
+      phase = keep_phase;
+      return;
+    }
     CK(cudaEventRecord(ev_fork, s));
     CK(cudaStreamWaitEvent(s_aux, ev_fork, 0));
     cudaStream_t keep = s;
@@ -1243,8 +1473,9 @@ struct EngineRun {
   //        = P^A_i [V1 P^B_k + U2] + U1 P^B_k (+ merged + leaf F x F)
   //   V1 = sum_{A,B adm} SB_ij S^B_jk,  U1 = sum_{A near} coll_a_ij S^B_jk,
   //   U2 = sum_{A adm, B near} S^A_ij coll_b_jk
+  // oq: quadrant scatter of the outputs into merged 2x2 blocks (pending targets), else slots slot0..
   void targets_range(int l, int t0, int cnt, double* out, long long slot0, const DBuf& SB, const DBuf* WA,
-                     const DBuf* WB, const DBuf* Z, int Kq) {
+                     const DBuf* WB, bool acc, const int* oq = nullptr) {
     if (cnt <= 0) return;
     const LevelPlan& L = P.lv[l];
     const DevLevel& Q = DP.lv[l];
@@ -1264,24 +1495,21 @@ struct EngineRun {
     seg(U2, (long long)KAr * Kc, 0, KAr, nullptr, KAr, Kc, cnt, true,
         {Grp{ref(V1, (long long)KAr * KBc, KAr, OP_N), PBk, KBc, nullptr, nullptr, tcol}});
     V1.release();
-    const long long os = (long long)Kr * Kc;
+    const long long os = oq ? 4LL * Kr * Kc : (long long)Kr * Kc;
+    const int old = oq ? 2 * Kr : Kr;
+    if (oq) slot0 = 0;
     const Grp gA{ref(PA[l], (long long)Kr * KAr, Kr, OP_N), ref(U2, (long long)KAr * Kc, KAr, OP_N), KAr, nullptr,
                  trow, nullptr};
     const Grp gB{ref(U1, (long long)Kr * KBc, Kr, OP_N), PBk, KBc, nullptr, nullptr, tcol};
-    if (Z) {
-      const DevCsr mg = sub_csr(Q.mg, L.mg, t0, cnt);
-      seg(out, os, slot0 * os, Kr, nullptr, Kr, Kc, cnt, false,
-          {gA, gB,
-           Grp{ref(*Z, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, &mg, nullptr,
-               nullptr}});
-    } else if (WA) {
+    quad = {oq, Kr, Kc};
+    if (WA) {
       const DevCsr ww = sub_csr(Q.ww, L.ww, t0, cnt);
-      seg(out, os, slot0 * os, Kr, nullptr, Kr, Kc, cnt, false,
+      seg(out, os, slot0 * os, old, nullptr, Kr, Kc, cnt, acc,
           {gA, gB,
            Grp{ref(*WA, (long long)Kr * NL, Kr, OP_N), ref(*WB, (long long)NL * Kc, NL, OP_N), NL, &ww, nullptr,
                nullptr}});
     } else {
-      seg(out, os, slot0 * os, Kr, nullptr, Kr, Kc, cnt, false, {gA, gB});
+      seg(out, os, slot0 * os, old, nullptr, Kr, Kc, cnt, acc, {gA, gB});
     }
   }
 
@@ -1303,17 +1531,8 @@ struct EngineRun {
     segd(VF, KAc, NL, nn, {Grp{ref(A.Vc, (long long)NL * KAc, NL, OP_T), BF, NL, nullptr, Q.near_row, nullptr}});
     DBuf SB;
     make_sb(l, SB);
-    {  // full targets on the auxiliary stream, overlapping everything until split()
-      CK(cudaEventRecord(ev_fork, s));
-      CK(cudaStreamWaitEvent(s_aux, ev_fork, 0));
-      cudaStream_t keep = s;
-      const std::string ph = phase;
-      s = s_aux;
-      leaf_full_targets(FV, VF, SB);
-      s = keep;
-      phase = ph;
-      CK(cudaEventRecord(ev_full, s_aux));
-    }
+    // full targets on the auxiliary stream, overlapping everything until split()
+    on_aux("leaf.full_targets", [&] { leaf_full_targets(FV, VF, SB); });
 
     if (adaptive) {
       mark("leaf.row_gram");
@@ -1398,13 +1617,14 @@ struct EngineRun {
     adm_factors(l, SB);
 
     mark("leaf.coupling_targets");
-    targets(l, SB, &WA, &WB, nullptr, 0);
-    hold.push_back(std::move(WA));
-    hold.push_back(std::move(WB));
+    alloc_targets(l, false);
+    targets(l, SB, &WA, &WB, false);
+    retire(std::move(WA));
+    retire(std::move(WB));
     // the auxiliary stream still reads these: release after the join
-    hold.push_back(std::move(FV));
-    hold.push_back(std::move(VF));
-    hold.push_back(std::move(SB));
+    retire(std::move(FV));
+    retire(std::move(VF));
+    retire(std::move(SB));
 
   }
 
@@ -1422,21 +1642,29 @@ struct EngineRun {
     const Ref AF = ref(A.F, NN, NL, OP_N), BF = ref(B.F, NN, NL, OP_N);
     phase = "leaf.full_targets";
     const Ref BS = ref(B.S[l], (long long)KBr * KBc, KBr, OP_N);
-    DBuf T2(sz(nn, NL, KBc), s), T4(sz(nn, KAr, KBc), s), U(sz(nn, KAr, NL), s);
-    segd(T2, NL, KBc, nn, {Grp{ref(FV, (long long)NL * KBr, NL, OP_N), BS, KBr, &Q.fr, nullptr, nullptr}});
-    segd(T4, KAr, KBc, nn, {Grp{ref(SB, (long long)KAr * KBr, KAr, OP_N), BS, KBr, &Q.rr, nullptr, nullptr}});
-    segd(U, KAr, NL, nn,
-         {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(VF, (long long)KAc * NL, KAc, OP_N), KAc, &Q.rf,
-              nullptr, nullptr},
-          Grp{ref(T4, (long long)KAr * KBc, KAr, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
-              nullptr, Q.near_col}});
     F.alloc(sz(nn, NL, NL), s);
-    segd(F, NL, NL, nn,
-         {Grp{AF, BF, NL, &Q.ff, nullptr, nullptr},
-          Grp{ref(T2, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
-              nullptr, Q.near_col},
-          Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(U, (long long)KAr * NL, KAr, OP_N), KAr, nullptr,
-              Q.near_row, nullptr}});
+    // in chunks of full blocks: bounded T2 / T4 / U scratch (kChunkBytes each)
+    const size_t per = size_t(W) * sizeof(double) * std::max(size_t(NL) * KBc, size_t(KAr) * std::max(KBc, NL));
+    const int step = static_cast<int>(std::max<size_t>(4096, kChunkBytes / per));
+    for (int t0 = 0; t0 < nn; t0 += step) {
+      const int cnt = std::min(step, nn - t0);
+      const DevCsr fr = sub_csr(Q.fr, L.fr, t0, cnt), rr = sub_csr(Q.rr, L.rr, t0, cnt),
+                   rf = sub_csr(Q.rf, L.rf, t0, cnt), ff = sub_csr(Q.ff, L.ff, t0, cnt);
+      DBuf T2(sz(cnt, NL, KBc), s), T4(sz(cnt, KAr, KBc), s), U(sz(cnt, KAr, NL), s);
+      segd(T2, NL, KBc, cnt, {Grp{ref(FV, (long long)NL * KBr, NL, OP_N), BS, KBr, &fr, nullptr, nullptr}});
+      segd(T4, KAr, KBc, cnt, {Grp{ref(SB, (long long)KAr * KBr, KAr, OP_N), BS, KBr, &rr, nullptr, nullptr}});
+      segd(U, KAr, NL, cnt,
+           {Grp{ref(A.S[l], (long long)KAr * KAc, KAr, OP_N), ref(VF, (long long)KAc * NL, KAc, OP_N), KAc, &rf,
+                nullptr, nullptr},
+            Grp{ref(T4, (long long)KAr * KBc, KAr, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
+                nullptr, Q.near_col + t0}});
+      seg(F, NN, NN * t0, NL, nullptr, NL, NL, cnt, false,
+          {Grp{AF, BF, NL, &ff, nullptr, nullptr},
+           Grp{ref(T2, (long long)NL * KBc, NL, OP_N), ref(B.Vc, (long long)NL * KBc, NL, OP_T), KBc, nullptr,
+               nullptr, Q.near_col + t0},
+           Grp{ref(A.Vr, (long long)NL * KAr, NL, OP_N), ref(U, (long long)KAr * NL, KAr, OP_N), KAr, nullptr,
+               Q.near_row + t0, nullptr}});
+    }
   }
 
   void formatted_bases(int l) {
@@ -1462,15 +1690,15 @@ struct EngineRun {
 
     mark("L" + std::to_string(l) + ".assemble");
     // merged children couplings and assembled collected blocks (mmp.cpp:344-404)
-    DBuf Mg, Aa, Ab;
-    gather(Mg, nm, Tp[l + 1].p, (long long)Kn * Kq, Kn, Kq, Q.merged_quad);
-    Tp[l + 1].release();
+    DBuf Aa, Ab;
+    DBuf Mg = std::move(this->Mg[l]);  // filled by level l+1's pending targets
     (void)Lc;
+    (void)nm;
     gather(Aa, ns, LA[l + 1], (long long)Kn * KBr1, Kn, KBr1, Q.sub_child);
     gather(Ab, ns, RB[l + 1], (long long)KAc1 * Kq, KAc1, Kq, Q.sub_child);
     // still read by level l+1's deferred targets: released after the join
-    hold.push_back(std::move(LA[l + 1]));
-    hold.push_back(std::move(RB[l + 1]));
+    retire(std::move(LA[l + 1]));
+    retire(std::move(RB[l + 1]));
 
     // X = asm_a T^B_row (row Gram term 2, collect); Xc = asm_b^T T^A_col
     DBuf X(sz(ns, 2 * Kn, KBr), s), Xc(sz(ns, 2 * Kq, KAc), s);
@@ -1517,7 +1745,8 @@ struct EngineRun {
                 nullptr}});
       Trunc tr = truncate(g1, g2, g3, n, 2 * Kn, A.dgr_d[l], /*defer=*/true);
       std::exception_ptr row_err;
-      std::thread row_th = solve_async(tr, row_err);
+      EigWork row_wk;
+      std::thread row_th = solve_async(tr, row_wk, row_err);
       // column transfer Gram (mmp.cpp:459-512)
       DBuf c1(sz(n, 2 * Kq, 2 * Kq), s), c2(sz(n, 2 * Kq, 2 * Kq), s), c3(sz(n, 2 * Kq, 2 * Kq), s);
       segh(c1, 2 * Kq, n,
@@ -1535,7 +1764,7 @@ struct EngineRun {
         if (row_th.joinable()) row_th.join();
         throw;
       }
-      finish_async(row_th, row_err, tr);
+      finish_async(row_th, row_err, tr, row_wk);
       KCr[l] = fetch_ranks(tr.rank, n, rcr[l]);
       KCc[l] = fetch_ranks(tc.rank, n, rcc[l]);
       pack(tr, n, 2 * Kn, Tr[l], 2 * Kn, KCr[l]);
@@ -1559,8 +1788,8 @@ struct EngineRun {
       identity(PA[l], n, KAr, A.rr_d[l]);
       identity(PB[l], n, KBc, B.rc_d[l]);
     }
-    hold.push_back(std::move(PA[l + 1]));
-    hold.push_back(std::move(PB[l + 1]));
+    retire(std::move(PA[l + 1]));
+    retire(std::move(PB[l + 1]));
     Bp[l + 1].release();
     const int Kr = KCr[l], Kc = KCc[l];
 
@@ -1580,15 +1809,13 @@ struct EngineRun {
     adm_factors(l, SB);
 
     mark("L" + std::to_string(l) + ".targets");
-    // case 1 over merged children couplings: Z = T^C_row^H M (mmp.cpp:573-585)
-    DBuf Z(sz(nm, Kr, 2 * Kq), s);
-    segd(Z, Kr, 2 * Kq, nm,
-         {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), ref(Mg, MM, 2 * Kn, OP_N), 2 * Kn, nullptr, Q.merged_row,
-              nullptr}});
+    // case 1 over merged children couplings first (mmp.cpp:573-585), then the
+    // triple sums of cases 2-4 accumulate onto the same stores
+    alloc_targets(l, true);
+    merged_into_targets(l, Mg);
     Mg.release();
-    targets(l, SB, nullptr, nullptr, &Z, Kq);
-    hold.push_back(std::move(Z));
-    hold.push_back(std::move(SB));
+    targets(l, SB, nullptr, nullptr, true);
+    retire(std::move(SB));
   }
 
   // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------
@@ -1631,11 +1858,16 @@ struct EngineRun {
   }
 
   void run() {
-    basis_products();
-    leaf_phase();
-    for (int l = D - 1; l >= 1; --l) upper_level(l);
-    split();
-    join();
+    defer_targets = !no_defer_env && !profiling;
+    try {
+      basis_products();
+      leaf_phase();
+      for (int l = D - 1; l >= 1; --l) upper_level(l);
+      split();
+      join();
+    } catch (const CudaError& e) {
+      throw CudaError(std::string(e.what()) + " [phase " + phase + "]");
+    }
   }
 
   // ---- exact H^2 matrix-vector product Y = A X (h2_matrix.cpp:213-278) -----
@@ -2119,9 +2351,16 @@ struct ArenaScope {
 Arena* Context::arena() {
   if (!arena_tried_) {
     arena_tried_ = true;
+    // return what the stream-ordered pool keeps cached (release threshold is
+    // unlimited) so the arena can claim it
+    CK(cudaDeviceSynchronize());
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device_));
+    CK(cudaMemPoolTrimTo(pool, 0));
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
-    const size_t reserve = size_t(28) << 30;  // pool (aux stream, solver) + operands headroom
+    // outside the arena: cuSOLVER workspaces, index vectors, small buffers
+    const size_t reserve = size_t(4) << 30;
     if (fr > reserve + (size_t(4) << 30)) {
       auto* a = new Arena;
       if (a->init(fr - reserve)) arena_ = a;
@@ -2180,6 +2419,32 @@ void Context::mvp(const std::shared_ptr<DevOperand>& a, const double* x_host, in
   EngineRun R(*this, *plan_, *dplan_, *a, *a, 0.5, true, s);
   R.mvp(X.p, nv, Y.p, perm.p);
   CK(cudaMemcpyAsync(y_host, Y.p, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  launches_ = R.launches;
+}
+
+void Context::to_dense(const std::shared_ptr<DevOperand>& a, double* out) {
+  if (!plan_ || a->key != plan_key_) throw ConfigErr("to_dense: operand was uploaded for another structure");
+  const int N = plan_->n_points;
+  if (N > 32768) throw ConfigErr("to_dense: N > 32768 (use the MVP)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  CK(cudaSetDevice(device_));
+  ArenaScope scope(arena(), s);
+  const int W = a->scalar == H2C_COMPLEX ? 2 : 1;
+  const int panel = std::min(N, 2048);
+  DBuf X(size_t(N) * panel * W, s), Y(size_t(N) * panel * W, s);
+  DVec<int32_t> perm;
+  perm.upload(perm_, s);
+  EngineRun R(*this, *plan_, *dplan_, *a, *a, 0.5, true, s);
+  for (int c0 = 0; c0 < N; c0 += panel) {
+    const int cw = std::min(panel, N - c0);
+    CK(cudaMemsetAsync(X.p, 0, size_t(N) * cw * W * sizeof(double), s));
+    unit_columns_kernel<<<(cw + 255) / 256, 256, 0, s>>>(X.p, N, c0, cw, W);
+    CK(cudaGetLastError());
+    R.launches++;
+    R.mvp(X.p, cw, Y.p, perm.p);
+    CK(cudaMemcpyAsync(out + size_t(c0) * N * W, Y.p, size_t(N) * cw * W * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
   CK(cudaStreamSynchronize(s));
   launches_ = R.launches;
 }

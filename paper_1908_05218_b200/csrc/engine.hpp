@@ -83,6 +83,8 @@ class Context {
   void truncate_gram(int scalar, const double* gram, int n, double eps, double* basis, int* rank, int* degenerate);
   // exact H^2 MVP Y = A X on a resident operand (host X, Y: N x nv, original ordering)
   void mvp(const std::shared_ptr<DevOperand>& a, const double* x, int nv, double* y);
+  // h2_to_dense (h2_matrix.cpp:124-137): A * I through the device MVP, N x N host output
+  void to_dense(const std::shared_ptr<DevOperand>& a, double* out);
   void* stream() const { return stream_; }
   int device() const { return device_; }
   void* solver();  // cusolverDn handle bound to the stream (lazy)

@@ -42,8 +42,22 @@ struct SegParams {
   int accumulate;      // out (+)= sum
   int sym;             // Hermitian output (Gram): only tiles m0 >= n0 are computed, mirrored
   int ngroups;
+  // optional quadrant scatter (children targets written straight into their
+  // parents' merged 2x2 blocks): output t -> block oquad[t] >> 2, quadrant
+  // q = oquad[t] & 3 at row offset (q >> 1) * qm and column offset (q & 1) * qn
+  const int* oquad;
+  int qm, qn;
   SegGroup g[kMaxGroups];
 };
+
+__device__ __forceinline__ long long seg_out_offset(const SegParams& p, int t) {
+  if (p.oquad) {
+    const int v = p.oquad[t];
+    const int q = v & 3;
+    return p.Os * (v >> 2) + p.Ooff + (q >> 1) * p.qm + (long long)((q & 1) * p.qn) * p.Old;
+  }
+  return p.Os * (p.omap ? p.omap[t] : t) + p.Ooff;
+}
 
 // ---------------------------------------------------------------------------
 // scalar helpers (complex values are interleaved re, im)
@@ -291,8 +305,7 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(const SegParams p) {
   }
 
   // ---- epilogue: out (+)= acc
-  const int o = p.omap ? p.omap[t] : t;
-  double* Op = p.out + (p.Os * o + p.Ooff) * C::W;
+  double* Op = p.out + seg_out_offset(p, t) * C::W;
 #pragma unroll
   for (int i = 0; i < C::FM; ++i)
 #pragma unroll
@@ -577,8 +590,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm2_kernel(const SegPara
   }
   cp_async_wait<0>();
 
-  const int o = p.omap ? p.omap[t] : t;
-  double* Op = p.out + (p.Os * o + p.Ooff) * W;
+  double* Op = p.out + seg_out_offset(p, t) * W;
 #pragma unroll
   for (int i = 0; i < C::FM; ++i)
 #pragma unroll
@@ -858,8 +870,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
   }
   cp_async_wait<0>();
 
-  const int o = p.omap ? p.omap[t] : t;
-  double* Op = p.out + (p.Os * o + p.Ooff) * W;
+  double* Op = p.out + seg_out_offset(p, t) * W;
 #pragma unroll
   for (int i = 0; i < C::FM; ++i)
 #pragma unroll
@@ -1518,6 +1529,12 @@ __global__ void mvp_scatter_kernel(const double* YL, int NL, int NV, const int* 
 }
 
 // identity matrices (formatted product: P = I, mmp.cpp:280-283)
+// columns c0 .. c0+cw-1 of the N x N identity into a zeroed N x cw panel
+__global__ void unit_columns_kernel(double* X, int N, int c0, int cw, int W) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < cw) X[(size_t(c0 + j) + size_t(j) * N) * W] = 1.0;
+}
+
 __global__ void set_identity_kernel(double* out, int n, int ld, const int* rank, int W) {
   const int b = blockIdx.x;
   double* o = out + (size_t)b * n * ld * W;

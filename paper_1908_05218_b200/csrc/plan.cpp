@@ -246,10 +246,14 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
           throw InvariantError("mmp: merged coupling with an impossible target");
         if (s == kInside) cand.push_back(par[m]);
       }
+      LevelPlan& Ch = P.lv[l + 1];
+      Ch.pend_mq.assign(pend[l + 1].size(), -1);
       for (size_t q = 0; q < pend[l + 1].size(); ++q) {
         const auto [ci, ck] = pend[l + 1][q];
         const auto it = std::lower_bound(par.begin(), par.end(), std::make_pair(ci >> 1, ck >> 1));
-        L.merged_quad[4 * (it - par.begin()) + 2 * (ci & 1) + (ck & 1)] = static_cast<int32_t>(q);
+        const int32_t mq = static_cast<int32_t>(4 * (it - par.begin()) + 2 * (ci & 1) + (ck & 1));
+        L.merged_quad[mq] = static_cast<int32_t>(q);
+        Ch.pend_mq[q] = mq;
       }
     }
     std::sort(cand.begin(), cand.end());
@@ -420,6 +424,17 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
       std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return L.merged_col[a] < L.merged_col[b]; });
       for (int m : idx) cm.add(L.merged_col[m], m, m);
       L.mg = mg.done(nt);
+      const int na_ = static_cast<int>(L.adm.size()), np_ = static_cast<int>(L.pend_row.size());
+      for (int m = 0; m < nm; ++m) {
+        const int t = L.merged_target[m];
+        const bool adm_t = t < na_;
+        if (!adm_t && t >= na_ + np_) throw InvariantError("mmp: merged coupling into a non-leaf target");
+        LevelPlan::MergedInto& z = adm_t ? L.mz_adm : L.mz_pend;
+        z.row.push_back(L.merged_row[m]);
+        z.col.push_back(L.merged_col[m]);
+        z.m.push_back(m);
+        z.out.push_back(adm_t ? t : L.pend_mq[t - na_]);
+      }
       L.row_merged = rm.done(L.n);
       L.col_merged = cm.done(L.n);
       // children of subdivided blocks

@@ -43,6 +43,7 @@ struct LevelPlan {
   // ---- coupling targets: [0, n_adm) admissible C blocks (adm order),
   //      [n_adm, n_adm + n_pend) pending pairs, then NL (subdivided) blocks
   std::vector<int32_t> pend_row, pend_col;  // pending pairs (inside-admissible), sorted
+  std::vector<int32_t> pend_mq;             // pending q -> 4 * (merged idx at level-1) + quadrant
   std::vector<int32_t> nl_block;            // subdivided blocks holding NL content (sorted)
   std::vector<int32_t> nl_of_block;         // block -> nl slot or -1
   int n_targets() const { return static_cast<int>(adm.size() + pend_row.size() + nl_block.size()); }
@@ -66,6 +67,13 @@ struct LevelPlan {
   std::vector<int32_t> merged_row, merged_col;
   std::vector<int32_t> merged_quad;  // [n_merged][4] pending index at level+1 (q = 2*ri + ci)
   std::vector<int32_t> merged_target;  // coupling-target slot at this level
+  // case-1 contributions T^C_i^H M conj(T^C_k) written straight into their
+  // targets before the triple sums accumulate: merged blocks whose target is
+  // admissible (out = Tg slot) and whose target is pending (out = parent's
+  // merged quadrant, see pend_mq); per entry: row pos, col pos, merged idx, out
+  struct MergedInto {
+    std::vector<int32_t> row, col, m, out;
+  } mz_adm, mz_pend;
   // case-1 into targets: CSR over coupling targets of merged indices (0 or 1 each)
   Csr mg;  // (merged idx, target col position)
 

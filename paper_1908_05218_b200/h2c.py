@@ -416,6 +416,8 @@ def lib() -> C.CDLL:
         L.h2c_count_report.argtypes = [C.POINTER(h2c_matrix)] * 3 + [C.c_int, C.c_double, C.POINTER(C.c_void_p)]
         L.h2c_mvp.restype = C.c_int
         L.h2c_mvp.argtypes = [C.c_void_p, C.POINTER(h2c_matrix), P_f64, C.c_int, P_f64]
+        L.h2c_to_dense.restype = C.c_int
+        L.h2c_to_dense.argtypes = [C.c_void_p, C.POINTER(h2c_matrix), P_f64]
         L.h2c_mvp_resident.restype = C.c_int
         L.h2c_mvp_resident.argtypes = [C.c_void_p, C.c_void_p, P_f64, C.c_int, P_f64]
         L.h2c_random_vector.restype = C.c_int

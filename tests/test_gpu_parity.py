@@ -369,6 +369,22 @@ def test_mvp_matches_oracle(ctx, kind):
     assert np.linalg.norm(y1 - O.mvp(A, X[:, 0])) <= 1e-13 * np.linalg.norm(y1)
 
 
+@pytest.mark.parametrize("kind", ["real", "complex", "product"])
+def test_device_h2_to_dense_matches_oracle(ctx, kind):
+    """h2_to_dense on the device (A * I through the MVP, h2_matrix.cpp:124-137) vs the oracle's block sum."""
+    if kind == "real":
+        A = laplace(1024, 5, 16, 1.2)
+    elif kind == "complex":
+        _, _, A = helmholtz(3, 20, 1.5)
+    else:
+        B = chebyshev(4096, 32, 3)
+        A = P.mmp(B, B, 1e-6, ctx).product
+    D = P.h2_to_dense(A, ctx)
+    ref = O.h2_to_dense(A)
+    assert D.shape == ref.shape and D.dtype == ref.dtype
+    assert rel(D, ref) <= 1e-14
+
+
 def test_relative_error_matches_oracle(ctx):
     A = chebyshev(4096, 32, 3)
     C = P.mmp(A, A, 1e-6, ctx).product
