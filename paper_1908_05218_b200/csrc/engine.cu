@@ -947,11 +947,44 @@ struct EngineRun {
       post();
       return;
     }
+    if (sym && (M != N || acc)) throw std::logic_error("seg: symmetric launch needs a square, fresh output");
+    // Outputs wider than one 64 tile whose last tile row / column would be at
+    // most half full (e.g. a padded rank of 208 = 3*64 + 16): the full 64-tiles
+    // and the remainder strip run as separate launches on shifted views, the
+    // strip with a 16/32-wide tile class instead of a mostly-padding 64 tile.
+    const int rm = M % 64, rn = N % 64;
+    const bool splitM = !sym && !seg_v1 && !no_strips && M > 64 && rm > 0 && rm <= 32;
+    const bool splitN = !sym && !seg_v1 && !no_strips && N > 64 && rn > 0 && rn <= 32;
+    if (!splitM && !splitN) {
+      launch_tiles(sp);
+    } else {
+      const int mcuts[3] = {0, splitM ? M - rm : M, M}, ncuts[3] = {0, splitN ? N - rn : N, N};
+      for (int a = 0; a < (splitM ? 2 : 1); ++a)
+        for (int b = 0; b < (splitN ? 2 : 1); ++b) {
+          const int r0 = mcuts[a], r1 = splitM ? mcuts[a + 1] : M;
+          const int c0 = ncuts[b], c1 = splitN ? ncuts[b + 1] : N;
+          SegParams q = sp;
+          q.M = r1 - r0;
+          q.N = c1 - c0;
+          q.Ooff = sp.Ooff + r0 + (long long)c0 * sp.Old;
+          for (int g = 0; g < q.ngroups; ++g) {
+            SegGroup& G = q.g[g];
+            const bool lt = G.opL == OP_T || G.opL == OP_H, rt = G.opR == OP_T || G.opR == OP_H;
+            G.Loff += lt ? (long long)r0 * G.Lld : r0;
+            G.Roff += rt ? c0 : (long long)c0 * G.Rld;
+          }
+          launch_tiles(q);
+        }
+    }
+    post();
+  }
+  const bool no_strips = std::getenv("H2B_NO_STRIPS") != nullptr;  // A/B: single launch per product
+  void launch_tiles(const SegParams& sp) {
+    const int M = sp.M, N = sp.N;
     const int TM = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
     const int TN = N <= 16 ? 16 : (N <= 32 ? 32 : 64);
     const int tm_ = (M + TM - 1) / TM;
-    const int tiles = sym ? tm_ * (tm_ + 1) / 2 : tm_ * ((N + TN - 1) / TN);
-    if (sym && (M != N || acc)) throw std::logic_error("seg: symmetric launch needs a square, fresh output");
+    const int tiles = sp.sym ? tm_ * (tm_ + 1) / 2 : tm_ * ((N + TN - 1) / TN);
     if (TM == 16 && TN == 16) launch_seg<16, 16>(sp, tiles);
     else if (TM == 16 && TN == 32) launch_seg<16, 32>(sp, tiles);
     else if (TM == 16 && TN == 64) launch_seg<16, 64>(sp, tiles);
@@ -961,7 +994,6 @@ struct EngineRun {
     else if (TM == 64 && TN == 16) launch_seg<64, 16>(sp, tiles);
     else if (TM == 64 && TN == 32) launch_seg<64, 32>(sp, tiles);
     else launch_seg<64, 64>(sp, tiles);
-    post();
   }
   // convenience: densely stored output [n_out][M x N]
   void segd(double* out, int M, int N, int n_out, std::initializer_list<Grp> gs) {
@@ -1001,10 +1033,27 @@ struct EngineRun {
     DBuf G(sz(count, n, n), s);
     t.degen.alloc(count, s);
     pre("gram_combine", 0);
-    if (cplx)
+    // few large Grams (upper levels): spread each over P CTAs (two passes)
+    const int P = static_cast<int>(std::min<long long>(std::max(1, 1184 / std::max(count, 1)),
+                                                       std::max<long long>(1, (long long)n * n * W / 4096)));
+    if (P > 1) {
+      DBuf part(size_t(count) * P * 3, s);
+      const dim3 grid(count, P);
+      if (cplx) {
+        gram_norm_partial_kernel<true><<<grid, 256, 0, s>>>(g1, g2, g3, (long long)n * n, n * n, part.p);
+        gram_combine_grid_kernel<true><<<grid, 256, 0, s>>>(g1, g2, g3, G, (long long)n * n, n * n, part.p, opdeg.p,
+                                                            t.degen.p);
+      } else {
+        gram_norm_partial_kernel<false><<<grid, 256, 0, s>>>(g1, g2, g3, (long long)n * n, n * n, part.p);
+        gram_combine_grid_kernel<false><<<grid, 256, 0, s>>>(g1, g2, g3, G, (long long)n * n, n * n, part.p, opdeg.p,
+                                                             t.degen.p);
+      }
+      launches++;
+    } else if (cplx) {
       gram_combine_kernel<true><<<count, 256, 0, s>>>(g1, g2, g3, G, (long long)n * n, n * n, opdeg.p, nullptr, t.degen.p);
-    else
+    } else {
       gram_combine_kernel<false><<<count, 256, 0, s>>>(g1, g2, g3, G, (long long)n * n, n * n, opdeg.p, nullptr, t.degen.p);
+    }
     CK(cudaGetLastError());
     post();
     launches++;

@@ -964,6 +964,65 @@ __global__ void gram_combine_kernel(const double* g1, const double* g2, const do
   }
 }
 
+// Grid-wide form of gram_combine for few large Grams (upper levels): grid
+// (count, P); pass 1 writes per-chunk sums of squares, pass 2 reads the P
+// partials of its Gram in a fixed order (deterministic) and combines its chunk.
+__device__ __forceinline__ void chunk_range(long long total, int P, int p, long long& x0, long long& x1) {
+  const long long per = (total + P - 1) / P;
+  x0 = min(total, per * p);
+  x1 = min(total, x0 + per);
+}
+template <bool CPLX>
+__global__ void __launch_bounds__(256) gram_norm_partial_kernel(const double* g1, const double* g2, const double* g3,
+                                                                long long stride, int elems, double* partial) {
+  constexpr int W = CPLX ? 2 : 1;
+  const int t = blockIdx.x, P = gridDim.y, p = blockIdx.y;
+  const double* src[3] = {g1 + stride * t * W, g2 + stride * t * W, g3 + stride * t * W};
+  long long x0, x1;
+  chunk_range((long long)elems * W, P, p, x0, x1);
+  double s[3] = {0, 0, 0};
+  for (long long x = x0 + threadIdx.x; x < x1; x += blockDim.x)
+    for (int q = 0; q < 3; ++q) s[q] += src[q][x] * src[q][x];
+  __shared__ double red[3][8];
+  for (int q = 0; q < 3; ++q)
+    for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0)
+    for (int q = 0; q < 3; ++q) red[q][warp] = s[q];
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0;
+    for (int w = 0; w < 8; ++w) v += red[threadIdx.x][w];
+    partial[(size_t(t) * P + p) * 3 + threadIdx.x] = v;
+  }
+}
+template <bool CPLX>
+__global__ void __launch_bounds__(256) gram_combine_grid_kernel(const double* g1, const double* g2, const double* g3,
+                                                                double* G, long long stride, int elems,
+                                                                const double* partial, const uint8_t* op_degen,
+                                                                uint8_t* pre_degen) {
+  constexpr int W = CPLX ? 2 : 1;
+  const int t = blockIdx.x, P = gridDim.y, p = blockIdx.y;
+  __shared__ double nrm[3];
+  if (threadIdx.x < 3) {
+    double v = 0;
+    for (int k = 0; k < P; ++k) v += partial[(size_t(t) * P + k) * 3 + threadIdx.x];
+    nrm[threadIdx.x] = sqrt(v);
+  }
+  __syncthreads();
+  const double* src[3] = {g1 + stride * t * W, g2 + stride * t * W, g3 + stride * t * W};
+  double* out = G + stride * t * W;
+  long long x0, x1;
+  chunk_range((long long)elems * W, P, p, x0, x1);
+  for (long long x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < 3; ++q)
+      if (nrm[q] > 0.0) v += src[q][x] / nrm[q];
+    out[x] = v;
+  }
+  if (p == 0 && threadIdx.x == 0) pre_degen[t] = (nrm[0] == 0.0 && nrm[1] == 0.0 && op_degen[t]) ? 1 : 0;
+}
+
 // ---------------------------------------------------------------------------
 // Batched Hermitian eigensolver for the truncation (truncation.cpp:9-47):
 // two-sided cyclic Jacobi, round-robin parallel ordering (n/2 disjoint

@@ -17,7 +17,7 @@ pts = P.random_cloud(n, 1)
 t = P.build_cluster_tree(pts, leaf)
 s = P.build_block_tree(t, t, 1.0)
 A = P.build_chebyshev(t, s, pts, order)
-KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_SEG_V2", "H2B_EIG_LIBRARY", "H2B_SEG_CFG")
+KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_SEG_V2", "H2B_EIG_LIBRARY", "H2B_SEG_CFG", "H2B_NO_STRIPS")
 for spec in sys.argv[5:]:
     label, _, kv = spec.partition(":")
     for k in KNOBS:
