@@ -840,15 +840,26 @@ struct EngineRun {
   // inner dimension to be a multiple of the k-chunk (8), which the padded layout
   // guarantees.  H2B_SEG_V2=1 selects v2 for A/B runs.
   const bool seg_v2 = std::getenv("H2B_SEG_V2") != nullptr;
-  template <int TM, int TN, bool CX, int KC, int ST>
+  template <int TM, int TN, bool CX, int KC, int ST, int WM = 2, int WN = 2>
   void launch_v3_cfg(const SegParams& sp, dim3 grid) {
-    constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST>::SMEM;
+    constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST, WM, WN>::SMEM;
     static bool attr = false;
     if (!attr) {
-      CK(cudaFuncSetAttribute(seg_gemm3_kernel<TM, TN, CX, KC, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(seg_gemm3_kernel<TM, TN, CX, KC, ST, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              sm));
       attr = true;
     }
-    seg_gemm3_kernel<TM, TN, CX, KC, ST><<<grid, 128, sm, s>>>(sp);
+    seg_gemm3_kernel<TM, TN, CX, KC, ST, WM, WN><<<grid, 32 * WM * WN, sm, s>>>(sp);
+  }
+  // 8-wide tile classes (v3 only): outputs with a padded dimension of 8, e.g.
+  // the rank-1 (padded 8) FD operand of cfg4, would waste half a 16-wide tile
+  template <int TM, int TN, int WM, int WN>
+  void launch_seg8(const SegParams& sp, int tiles) {
+    dim3 grid(sp.n_out, tiles);
+    if (cplx) launch_v3_cfg<TM, TN, true, 8, 4, WM, WN>(sp, grid);
+    else launch_v3_cfg<TM, TN, false, 8, 4, WM, WN>(sp, grid);
+    CK(cudaGetLastError());
+    launches++;
   }
   template <int TM, int TN>
   void launch_seg(const SegParams& sp, int tiles) {
@@ -981,10 +992,21 @@ struct EngineRun {
   const bool no_strips = std::getenv("H2B_NO_STRIPS") != nullptr;  // A/B: single launch per product
   void launch_tiles(const SegParams& sp) {
     const int M = sp.M, N = sp.N;
-    const int TM = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
-    const int TN = N <= 16 ? 16 : (N <= 32 ? 32 : 64);
+    const bool v3 = !seg_v1 && !seg_v2;
+    const int TM = (M <= 8 && v3) ? 8 : M <= 16 ? 16 : (M <= 32 ? 32 : 64);
+    const int TN = (N <= 8 && v3) ? 8 : N <= 16 ? 16 : (N <= 32 ? 32 : 64);
     const int tm_ = (M + TM - 1) / TM;
     const int tiles = sp.sym ? tm_ * (tm_ + 1) / 2 : tm_ * ((N + TN - 1) / TN);
+    if (TM == 8 || TN == 8) {
+      if (TM == 8 && TN == 8) launch_seg8<8, 8, 1, 1>(sp, tiles);
+      else if (TM == 8 && TN == 16) launch_seg8<8, 16, 1, 2>(sp, tiles);
+      else if (TM == 8 && TN == 32) launch_seg8<8, 32, 1, 4>(sp, tiles);
+      else if (TM == 8) launch_seg8<8, 64, 1, 4>(sp, tiles);
+      else if (TM == 16) launch_seg8<16, 8, 2, 1>(sp, tiles);
+      else if (TM == 32) launch_seg8<32, 8, 4, 1>(sp, tiles);
+      else launch_seg8<64, 8, 4, 1>(sp, tiles);
+      return;
+    }
     if (TM == 16 && TN == 16) launch_seg<16, 16>(sp, tiles);
     else if (TM == 16 && TN == 32) launch_seg<16, 32>(sp, tiles);
     else if (TM == 16 && TN == 64) launch_seg<16, 64>(sp, tiles);
