@@ -44,11 +44,58 @@ CONFIGS = {
                                   "Chebyshev order 4 (k=64), eps 1e-6"),
     # configs[3]'s construction on the 48^3 grid: the 64^3 product's live pending couplings alone
     # (two consecutive levels, ~125 GB) exceed one B200's HBM next to A, B and C
+    "cfg3": (262144, 32, 3, 1e-6, "16 parallel unit plates (z = 0.1 p) of 128 x 128 panel centroids, Laplace 1/(4 pi r) "
+                                  "with self term 2 ln(1+sqrt2)/(pi h), leaf 32, eta 1, Chebyshev order 3 recompressed "
+                                  "at 1e-6; C = A*B, B on the centroids with 0.05 h seeded jitter (seed 2) over A's "
+                                  "tree/structure; eps 1e-6"),
+    "cfg5": (1048576, 64, 0, 1e-4, "Helmholtz exp(-i k r)/(4 pi r), k = 2 pi, complex128, N = 2^20 Fibonacci-sphere "
+                                   "points (seeded rotation, seed 3), diameter 16 wavelengths, leaf 64, eta 1, "
+                                   "Chebyshev order per level clamp(ceil(2.5 + 1.2 k h_l), 4, 7) recompressed at "
+                                   "1e-4; C = A*A, eps 1e-4"),
+    # configs[4]'s construction at a quarter of the points on a sphere of half the radius (same
+    # points per wavelength)
+    "cfg5s": (262144, 64, 0, 1e-4, "configs[4] construction at N = 2^18 on a sphere of diameter 8 wavelengths "
+                                   "(same points per wavelength): Helmholtz k = 2 pi, complex128, leaf 64, orders "
+                                   "clamp(ceil(2.5 + 1.2 k h_l), 4, 7), recompressed at 1e-4; C = A*A, eps 1e-4"),
     "cfg4s": (110592, 64, 4, 1e-6, "configs[3] construction on the 48^3 grid (h = 1/49): C = A*B, A = 7-point FD "
                                    "Laplacian, B = Laplace Chebyshev order 4 (k=64), leaf 64, eta 1, eps 1e-6"),
 }
 # bounded CPU sample of the same construction (oracle single-thread ~10-30 s)
-CPU_SAMPLE = {"cfg1": 4096, "cfg2": 4096, "cfg4": 4096, "cfg4s": 4096}
+CPU_SAMPLE = {"cfg1": 4096, "cfg2": 4096, "cfg3": 4096, "cfg4": 4096, "cfg4s": 4096, "cfg5": 4096, "cfg5s": 4096}
+KAPPA = 2.0 * np.pi  # cfg5: wavelength 1
+
+
+def plate_points(n: int) -> tuple[np.ndarray, float]:
+    """16 parallel unit plates z = 0.1 p, m x m panel centroids each (m^2 = n / 16), h = 1/m."""
+    m = round((n / 16) ** 0.5)
+    h = 1.0 / m
+    i, j = np.meshgrid(np.arange(m), np.arange(m), indexing="ij")
+    pl = np.stack([(i.ravel() + 0.5) * h, (j.ravel() + 0.5) * h, np.zeros(m * m)], 1)
+    pts = np.concatenate([pl + np.array([0.0, 0.0, 0.1 * p]) for p in range(16)])
+    return np.ascontiguousarray(pts), h
+
+
+def sphere_points(n: int, seed: int = 3) -> np.ndarray:
+    """Fibonacci lattice on a sphere of radius 8 sqrt(n / 2^20) (diameter 16 wavelengths at
+    N = 2^20; fixed points per wavelength), rotated by a seeded random orthogonal matrix."""
+    radius = 8.0 * (n / 2.0 ** 20) ** 0.5
+    i = np.arange(n) + 0.5
+    phi = np.arccos(1.0 - 2.0 * i / n)
+    th = np.pi * (1.0 + 5.0 ** 0.5) * i
+    x = radius * np.stack([np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)], 1)
+    q, r = np.linalg.qr(np.random.default_rng(seed).standard_normal((3, 3)))
+    q = q * np.sign(np.diag(r))
+    return np.ascontiguousarray(x @ q.T)
+
+
+def helmholtz_orders(tree, kappa: float = KAPPA, lo: int = 3, hi: int = 5) -> np.ndarray:
+    """Chebyshev order per level from the largest box half-width h_l in wavelengths."""
+    bb = np.asarray(tree.bbox).reshape(-1, 6)
+    out = np.full(tree.depth + 1, lo, dtype=np.int32)
+    for l in range(tree.depth + 1):
+        hl = 0.5 * (bb[tree.level == l, 3:] - bb[tree.level == l, :3]).max()
+        out[l] = min(hi, max(lo, int(np.ceil(1.0 + 1.2 * kappa * hl))))
+    return out
 
 
 def grid_points(m: int) -> tuple[np.ndarray, float]:
@@ -68,6 +115,22 @@ def build_operands(name: str, n: int):
         tree = P.build_cluster_tree(pts, leaf)
         st = P.build_block_tree(tree, tree, 1.0)
         return pts, tree, st, P.build_fd_laplacian(tree, st, pts, h), P.build_chebyshev(tree, st, pts, order)
+    if name == "cfg3":
+        pts, h = plate_points(n)
+        tree = P.build_cluster_tree(pts, leaf)
+        st = P.build_block_tree(tree, tree, 1.0)
+        diag = 2.0 * np.log(1.0 + np.sqrt(2.0)) / (np.pi * h)
+        A = P.build_chebyshev(tree, st, pts, order, diagonal=diag, eps_recompress=1e-6)
+        jit = pts + 0.05 * h * np.random.default_rng(2).uniform(-1.0, 1.0, pts.shape)
+        B = P.build_chebyshev(tree, st, jit, order, diagonal=diag, eps_recompress=1e-6)
+        return pts, tree, st, A, B
+    if name in ("cfg5", "cfg5s"):
+        pts = sphere_points(n)
+        tree = P.build_cluster_tree(pts, leaf)
+        st = P.build_block_tree(tree, tree, 1.0)
+        A = P.build_chebyshev(tree, st, pts, helmholtz_orders(tree), kernel="helmholtz", kappa=KAPPA,
+                              eps_recompress=1e-4)
+        return pts, tree, st, A, A
     pts = P.random_cloud(n, 1)  # make_random_cloud (geometry.cpp:39-52)
     tree = P.build_cluster_tree(pts, leaf)
     st = P.build_block_tree(tree, tree, 1.0)
@@ -139,6 +202,20 @@ def fp64_peak_tflops() -> tuple[float, str]:
         return 40.0, "fallback: nominal B200 FP64"
 
 
+def measured_traffic(kernel: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant
+    phase's kernel from the committed `ncu --set full` capture (profiles/TRAFFIC.json, written
+    by tools/ncu_traffic.py from the .ncu-rep of tools/gpu_round.sh), or None."""
+    p = os.path.join(ROOT, "profiles", "TRAFFIC.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        e = t[kernel]
+        return float(e["dram_bytes_per_launch"]), e.get("source")
+    except Exception:
+        return None, None
+
+
 def cpu_sample(name: str, threads_note: int = 1) -> dict:
     """Single-thread oracle on the bounded sample; returns GFLOP/s and details."""
     from oracle import pyoracle as O
@@ -149,7 +226,8 @@ def cpu_sample(name: str, threads_note: int = 1) -> dict:
     t0 = time.perf_counter()
     r = O.mmp(A, B, eps)
     dt = time.perf_counter() - t0
-    return {"gflops": 2.0 * r.report.flops / dt / 1e9, "seconds": dt, "flops": r.report.flops, "n": n,
+    fpm = 8.0 if A.scalar == P.H2C_COMPLEX else 2.0
+    return {"gflops": fpm * r.report.flops / dt / 1e9, "fpm": fpm, "seconds": dt, "flops": r.report.flops, "n": n,
             "wall_seconds_report": r.report.wall_seconds}
 
 
@@ -181,12 +259,12 @@ def run_reference(args) -> None:
         dt = time.perf_counter() - t0
         if step >= args.warmup:
             times.append(dt)
-            total_flops = sum(r["flops"] for r in res)
+            total_flops = sum(r["flops"] * r["fpm"] / 2.0 for r in res)
     mean = sum(times) / len(times)
     value = 2.0 * total_flops / mean / 1e9
     sample = (f"{cores} concurrent single-thread oracle products of the {name} construction at "
               f"N={CPU_SAMPLE[name]} (leaf {CONFIGS[name][1]}, order {CONFIGS[name][2]}, eps {CONFIGS[name][3]})")
-    line = {"metric": "H2-MMP FP64 GFLOP/s (2*MmpReport.flops / wall)", "value": value, "unit": "GFLOP/s",
+    line = {"metric": "H2-MMP FP64 GFLOP/s (F_alg = 2 real / 8 complex x MmpReport.flops per product / wall)", "value": value, "unit": "GFLOP/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": {"workload": name, "desc": CONFIGS[name][4]},
@@ -254,7 +332,9 @@ def run_b200(args) -> None:
     if dist:
         dist.barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, "cuda")
-    flops = 2.0 * rep.flops
+    # F_alg: 2 flops per real MAC, 8 per complex MAC
+    fpm = 8.0 if A.scalar == P.H2C_COMPLEX else 2.0
+    flops = fpm * rep.flops
     value = job_throughput(flops, world, ms * 1e-3)
 
     # roofline of the dominant kernel: one profiled (untimed) product
@@ -269,13 +349,16 @@ def run_b200(args) -> None:
     prof_ms = sum(e["ms"] for e in prof) if prof else 0.0
     roofline = None
     if dom:
-        ach = 2.0 * dom["macs"] / (dom["ms"] * 1e-3) / 1e12
+        ach = fpm * dom["macs"] / (dom["ms"] * 1e-3) / 1e12
+        traffic, traffic_src = measured_traffic(f"{args.config}:{dom['name']}")
         roofline = {"bound": "tensor", "kernel": dom["name"], "launches": dom["launches"],
                     "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-                    "traffic": None, "peak_source": peak_src,
+                    "traffic": traffic, "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
+                    "flops_per_launch": fpm * dom["macs"] / dom["launches"],
+                    "peak_source": peak_src,
                     "share_of_step": round(dom["ms"] / prof_ms, 4) if prof_ms else None,
-                    "pipeline_exec_tflops": round(2.0 * rep.flops_exec / (ms * 1e-3) / 1e12, 3),
-                    "pipeline_frac": round(2.0 * rep.flops_exec / (ms * 1e-3) / 1e12 / peak, 4)}
+                    "pipeline_exec_tflops": round(fpm * rep.flops_exec / (ms * 1e-3) / 1e12, 3),
+                    "pipeline_frac": round(fpm * rep.flops_exec / (ms * 1e-3) / 1e12 / peak, 4)}
 
     # end-to-end through the drop-in C-ABI call with pinned host buffers
     del dA, dB
@@ -291,8 +374,13 @@ def run_b200(args) -> None:
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
         h2d, d2h = res.report.h2d_bytes, res.report.d2h_bytes
+        last = res
         del res
     e2e_s = max_over_ranks(sum(e2e_times) / len(e2e_times), dist, "cuda")
+    # accuracy of the product, size-independent: eps_rel = ||C x - A (B x)|| / ||A (B x)|| with the
+    # reference's seeded random_vector (metrics.cpp:37-55), exact H^2 MVPs on the device (untimed)
+    eps_rel = P.relative_error(A, B, last.product, 1, ctx)
+    del last
     e2e_value = job_throughput(flops, world, e2e_s)
 
     cpu = None
@@ -304,12 +392,13 @@ def run_b200(args) -> None:
 
     if rank == 0:
         line = {
-            "metric": "H2-MMP FP64 GFLOP/s (2*MmpReport.flops / wall)", "value": round(value, 3),
+            "metric": "H2-MMP FP64 GFLOP/s (F_alg = 2 real / 8 complex x MmpReport.flops per product / wall)", "value": round(value, 3),
             "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
+            "dtype": "c128" if A.scalar == P.H2C_COMPLEX else "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": W["desc"], "N": W["n"], "eps": eps,
-                       "flops_per_step": int(rep.flops), "flops_exec_per_step": int(rep.flops_exec),
+                       "macs_per_step": int(rep.flops), "macs_exec_per_step": int(rep.flops_exec),
+                       "flops_per_mac": fpm, "eps_rel": eps_rel,
                        "max_rank": rep.max_rank(), "l2": "inputs (%.1f GB) >> 126 MB L2" % ((A.values.nbytes + (0 if B is A else B.values.nbytes)) / 1e9),
                        "parallelism": f"replicas{world}"},
             "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),

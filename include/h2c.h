@@ -67,6 +67,14 @@ int h2c_random_cloud(int n, uint64_t seed, double* xyz);
 h2c_h2* h2c_build_chebyshev(const h2c_tree* tree, const h2c_blocks* blocks, const double* xyz,
                             int kernel, double kappa, double diagonal, int order,
                             double eps_recompress, int threads);
+/* Same with an interpolation order per tree level (orders[0..depth]; e.g. growing
+ * with the box size in wavelengths for Helmholtz).  With eps_recompress > 0 the
+ * interpolation operand is recompressed by the rule of the reference's build_h2
+ * (h2_matrix.cpp:83-121: far-field row Gram incl. inherited partners, truncated
+ * by svd_truncate_gram at eps_recompress), without forming dense blocks. */
+h2c_h2* h2c_build_chebyshev_orders(const h2c_tree* tree, const h2c_blocks* blocks, const double* xyz,
+                                   int kernel, double kappa, double diagonal, const int* orders,
+                                   double eps_recompress, int threads);
 /* 7-point finite-difference Laplacian (6 on the diagonal, -1 for grid
  * neighbours) on an m x m x m grid in H^2 form: full blocks exact,
  * admissible blocks zero with rank-1 degenerate e_1 bases (the form

@@ -145,15 +145,25 @@ def random_cloud(n: int, seed: int) -> np.ndarray:
     return out
 
 
-def build_chebyshev(tree: ClusterTree, structure: BlockTree, points: np.ndarray, order: int, kernel: str = "laplace",
+def build_chebyshev(tree: ClusterTree, structure: BlockTree, points: np.ndarray, order, kernel: str = "laplace",
                     kappa: float = 0.0, diagonal: float = 0.0, eps_recompress: float = 0.0,
                     threads: int = 0) -> H2Matrix:
-    """Nested tensor-Chebyshev H^2 matrix with orthonormal bases (input side)."""
+    """Nested tensor-Chebyshev H^2 matrix with orthonormal bases (input side).
+
+    order: one interpolation order, or one per tree level (depth + 1 entries).
+    eps_recompress > 0: recompress with the reference's build_h2 rule (h2_matrix.cpp:83-121)."""
     pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
     k = {"laplace": 0, "helmholtz": 1}[kernel]
-    h = h2c.lib().h2c_build_chebyshev(C.byref(tree.desc()), C.byref(structure.desc()),
-                                      pts.ctypes.data_as(h2c.P_f64), k, float(kappa), float(diagonal), int(order),
-                                      float(eps_recompress), int(threads))
+    if np.ndim(order) == 0:
+        orders = np.full(tree.depth + 1, int(order), dtype=np.int32)
+    else:
+        orders = np.ascontiguousarray(order, dtype=np.int32)
+        if orders.shape != (tree.depth + 1,):
+            raise ConfigError(f"orders must have depth + 1 = {tree.depth + 1} entries")
+    h = h2c.lib().h2c_build_chebyshev_orders(C.byref(tree.desc()), C.byref(structure.desc()),
+                                             pts.ctypes.data_as(h2c.P_f64), k, float(kappa), float(diagonal),
+                                             orders.ctypes.data_as(C.POINTER(C.c_int32)), float(eps_recompress),
+                                             int(threads))
     return _take_h2(h, tree, structure)
 
 

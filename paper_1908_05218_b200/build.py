@@ -28,6 +28,16 @@ CU_SOURCES = ["engine.cu"]
 CPP_SOURCES = ["plan.cpp", "counters.cpp", "structure.cpp", "construct.cpp", "capi.cpp"]
 
 
+def _host_blas() -> list[str]:
+    """Link flags for the scipy wheel's OpenBLAS (host BLAS/LAPACK of the input constructor only)."""
+    import scipy
+    libs = Path(scipy.__path__[0]).parent / "scipy.libs"
+    so = sorted(libs.glob("libscipy_openblas*.so"))
+    if not so:
+        raise RuntimeError(f"no libscipy_openblas in {libs}")
+    return [f"-L{libs}", f"-l:{so[0].name}", "-Xlinker", f"-rpath={libs}"]
+
+
 def _headers() -> list[Path]:
     return list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h"))
 
@@ -70,7 +80,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
             _run(["g++", *CXX_FLAGS, "-c", str(s), "-o", str(o)])
         objs.append(o)
     if force or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-lcusolver", "-Xcompiler", "-pthread"])
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-lcusolver", *_host_blas(),
+              "-Xcompiler", "-pthread"])
     return LIB
 
 

@@ -3,6 +3,9 @@
 // H2C_ERR_CONFIG, InvariantError -> H2C_ERR_INVARIANT, CUDA failures ->
 // H2C_ERR_CUDA.  There is no CPU fallback: without a usable device every MMP
 // entry point fails with H2C_ERR_CUDA.
+#include <algorithm>
+#include <thread>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -137,10 +140,24 @@ int h2c_random_cloud(int n, uint64_t seed, double* xyz) {
 h2c_h2* h2c_build_chebyshev(const h2c_tree* tree, const h2c_blocks* blocks, const double* xyz, int kernel,
                             double kappa, double diagonal, int order, double eps_recompress, int threads) {
   try {
-    auto* m = new h2c_h2;
-    m->m = build_chebyshev(*tree, *blocks, xyz, kernel, kappa, diagonal, order, eps_recompress,
-                           threads > 0 ? threads : 8);
-    return m;
+    if (order < 1) throw std::invalid_argument("chebyshev order must be >= 1");
+    const std::vector<int> orders(tree->depth + 1, order);
+    return h2c_build_chebyshev_orders(tree, blocks, xyz, kernel, kappa, diagonal, orders.data(), eps_recompress,
+                                      threads);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+h2c_h2* h2c_build_chebyshev_orders(const h2c_tree* tree, const h2c_blocks* blocks, const double* xyz, int kernel,
+                                   double kappa, double diagonal, const int* orders, double eps_recompress,
+                                   int threads) {
+  try {
+    auto m = std::make_unique<h2c_h2>();
+    m->m = build_chebyshev(*tree, *blocks, xyz, kernel, kappa, diagonal, orders, eps_recompress,
+                           threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency())));
+    return m.release();
   } catch (const std::exception& e) {
     g_err = e.what();
     return nullptr;

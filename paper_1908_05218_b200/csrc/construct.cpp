@@ -12,10 +12,15 @@
 //    zero admissible blocks with the degenerate e_1 bases build_h2 produces for
 //    a zero far field, truncation.cpp:16-23).
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <complex>
 #include <stdexcept>
 #include <thread>
+#include <type_traits>
+#include <algorithm>
 
 #include "structure.hpp"
 
@@ -27,11 +32,12 @@ template <class F>
 void pfor(int64_t n, int threads, F&& f) {
   threads = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(threads, n)));
   std::atomic<int64_t> next{0};
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(64, n / (8 * int64_t(threads))));
   auto work = [&] {
     for (;;) {
-      const int64_t i = next.fetch_add(64);
+      const int64_t i = next.fetch_add(chunk);
       if (i >= n) break;
-      for (int64_t k = i; k < std::min(n, i + 64); ++k) f(k);
+      for (int64_t k = i; k < std::min(n, i + chunk); ++k) f(k);
     }
   };
   if (threads == 1) {
@@ -149,39 +155,177 @@ void HostH2::desc(h2c_matrix* d) const {
   d->n_values = static_cast<int64_t>(values.size()) / (scalar == H2C_COMPLEX ? 2 : 1);
 }
 
-std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, const double* xyz, int kernel,
-                                        double kappa, double diagonal, int order, double eps_recompress,
-                                        int threads) {
-  if (order < 1) throw std::invalid_argument("chebyshev order must be >= 1");
-  if (eps_recompress > 0) throw std::invalid_argument("recompression is not available in this build");
-  const bool cplx = kernel == 1;
-  const int W = cplx ? 2 : 1;
-  const int m = order, k = m * m * m;
+namespace {
+
+using cd = std::complex<double>;
+
+// host BLAS/LAPACK for the input constructor (the scipy wheel's OpenBLAS, symbols prefixed
+// `scipy_`); never used by the product path
+extern "C" {
+void scipy_cblas_dgemm(int order, int ta, int tb, int m, int n, int k, double alpha, const double* a, int lda,
+                       const double* b, int ldb, double beta, double* c, int ldc);
+void scipy_cblas_zgemm(int order, int ta, int tb, int m, int n, int k, const void* alpha, const void* a, int lda,
+                       const void* b, int ldb, const void* beta, void* c, int ldc);
+void scipy_dsyevd_(const char* jobz, const char* uplo, const int* n, double* a, const int* lda, double* w,
+                   double* work, const int* lwork, int* iwork, const int* liwork, int* info, size_t, size_t);
+void scipy_zheevd_(const char* jobz, const char* uplo, const int* n, void* a, const int* lda, double* w, void* work,
+                   const int* lwork, double* rwork, const int* lrwork, int* iwork, const int* liwork, int* info,
+                   size_t, size_t);
+void scipy_openblas_set_num_threads(int);
+}
+
+// column-major dense matrix of scalar S
+template <class S>
+struct M {
+  int r = 0, c = 0;
+  std::vector<S> d;
+  M() = default;
+  M(int rows, int cols) : r(rows), c(cols), d(size_t(rows) * cols, S(0)) {}
+  S& operator()(int i, int j) { return d[i + size_t(j) * r]; }
+  const S& operator()(int i, int j) const { return d[i + size_t(j) * r]; }
+};
+
+enum Op { kN = 111, kT = 112, kC = 113 };
+
+// C = op(A) op(B) (+ C if acc)
+template <class S>
+void gemm(Op oa, Op ob, const M<S>& a, const M<S>& b, M<S>& c, bool acc = false) {
+  const int m = oa == kN ? a.r : a.c, k = oa == kN ? a.c : a.r, n = ob == kN ? b.c : b.r;
+  if (!acc) c = M<S>(m, n);
+  if (m == 0 || n == 0 || k == 0) return;
+  if constexpr (std::is_same_v<S, double>) {
+    scipy_cblas_dgemm(102, oa == kC ? kT : oa, ob == kC ? kT : ob, m, n, k, 1.0, a.d.data(), a.r, b.d.data(), b.r,
+                      acc ? 1.0 : 0.0, c.d.data(), c.r);
+  } else {
+    const cd one(1.0), beta(acc ? 1.0 : 0.0);
+    scipy_cblas_zgemm(102, oa, ob, m, n, k, &one, a.d.data(), a.r, b.d.data(), b.r, &beta, c.d.data(), c.r);
+  }
+}
+
+template <class S>
+M<S> lift(const Dm& a) {
+  M<S> o(a.r, a.c);
+  for (size_t i = 0; i < a.d.size(); ++i) o.d[i] = S(a.d[i]);
+  return o;
+}
+
+// svd_truncate_gram (truncation.cpp:9-47) on the host: keep lambda_i > eps * lambda_max (>= 1);
+// zero Gram -> e_1, degenerate.  Returns the basis (n x rank), eigenvectors descending.
+template <class S>
+M<S> truncate_gram(const M<S>& g, double eps, bool& degenerate) {
+  const int n = g.r;
+  degenerate = false;
+  bool zero = true;
+  for (const S& x : g.d)
+    if (x != S(0)) {
+      zero = false;
+      break;
+    }
+  auto unit = [&] {
+    M<S> e(n, 1);
+    e(0, 0) = S(1);
+    degenerate = true;
+    return e;
+  };
+  if (zero) return unit();
+  M<S> a = g;
+  std::vector<double> w(n);
+  int info = 0, lwork = -1, liwork = -1, lrwork = -1, iwq = 0;
+  const int lda = n;
+  if constexpr (std::is_same_v<S, double>) {
+    double wq = 0;
+    scipy_dsyevd_("V", "L", &n, a.d.data(), &lda, w.data(), &wq, &lwork, &iwq, &liwork, &info, 1, 1);
+    lwork = static_cast<int>(wq);
+    liwork = iwq;
+    std::vector<double> work(std::max(1, lwork));
+    std::vector<int> iwork(std::max(1, liwork));
+    scipy_dsyevd_("V", "L", &n, a.d.data(), &lda, w.data(), work.data(), &lwork, iwork.data(), &liwork, &info, 1,
+                  1);
+  } else {
+    cd wq = 0;
+    double rq = 0;
+    scipy_zheevd_("V", "L", &n, a.d.data(), &lda, w.data(), &wq, &lwork, &rq, &lrwork, &iwq, &liwork, &info, 1, 1);
+    lwork = static_cast<int>(wq.real());
+    lrwork = static_cast<int>(rq);
+    liwork = iwq;
+    std::vector<cd> work(std::max(1, lwork));
+    std::vector<double> rwork(std::max(1, lrwork));
+    std::vector<int> iwork(std::max(1, liwork));
+    scipy_zheevd_("V", "L", &n, a.d.data(), &lda, w.data(), work.data(), &lwork, rwork.data(), &lrwork, iwork.data(),
+                  &liwork, &info, 1, 1);
+  }
+  if (info != 0) throw std::runtime_error("construct: eigensolver failed");
+  for (double& x : w) x = std::max(x, 0.0);
+  const double top = w[n - 1];
+  if (top <= 0.0) return unit();
+  int rank = 0;
+  while (rank < n && w[n - 1 - rank] > eps * top) ++rank;
+  rank = std::max(rank, 1);
+  M<S> out(n, rank);
+  for (int j = 0; j < rank; ++j)
+    for (int i = 0; i < n; ++i) out(i, j) = a(i, n - 1 - j);
+  return out;
+}
+
+struct Cheb {
+  int m = 0;  // order per dimension
+  Box box;
+  double node(int d, int i) const { return cheb_node(box, d, i, m); }
+  double lag(int d, int i, double x) const { return lagrange(box, d, i, m, x); }
+  int k() const { return m * m * m; }
+};
+
+template <class S>
+std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, const double* xyz, int kernel,
+                                       double kappa, double diagonal, const int* orders, double eps_rc,
+                                       int threads) {
+  constexpr bool cplx = !std::is_same_v<S, double>;
+  constexpr int W = cplx ? 2 : 1;
   const int nc = t.n_clusters, D = t.depth;
   auto out = std::make_unique<HostH2>();
   out->scalar = cplx ? H2C_COMPLEX : H2C_REAL;
+  const int* perm = t.perm;
+  const bool trace = std::getenv("H2B_CONSTRUCT_TRACE") != nullptr;  // phase wall times on stderr
+  auto t_last = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[construct] %-22s %8.3f s\n", what, std::chrono::duration<double>(now - t_last).count());
+    t_last = now;
+  };
 
-  // interpolation boxes: cluster bounding boxes (degenerate extents widened)
-  std::vector<Box> box(nc);
+  // interpolation boxes: bounding boxes of the points the matrix is evaluated on (the
+  // tree's own points, or e.g. jittered copies over the same tree), degenerate extents widened
+  std::vector<Cheb> cb(nc);
   for (int c = 0; c < nc; ++c) {
-    const double* bb = &t.bbox[6 * c];
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int p = t.begin[c]; p < t.end[c]; ++p)
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = std::min(lo[d], xyz[3 * perm[p] + d]);
+        hi[d] = std::max(hi[d], xyz[3 * perm[p] + d]);
+      }
     double ext = 0;
-    for (int d = 0; d < 3; ++d) ext = std::max(ext, bb[d + 3] - bb[d]);
+    for (int d = 0; d < 3; ++d) ext = std::max(ext, hi[d] - lo[d]);
     for (int d = 0; d < 3; ++d) {
-      box[c].c[d] = 0.5 * (bb[d] + bb[d + 3]);
-      box[c].h[d] = std::max(0.5 * (bb[d + 3] - bb[d]), 1e-6 * std::max(ext, 1e-300));
+      cb[c].box.c[d] = 0.5 * (lo[d] + hi[d]);
+      cb[c].box.h[d] = std::max(0.5 * (hi[d] - lo[d]), 1e-6 * std::max(ext, 1e-300));
     }
+    cb[c].m = orders[t.level[c]];
+    if (cb[c].m < 1 || cb[c].m > 64) throw std::invalid_argument("chebyshev order must be in [1, 64]");
   }
-  // nested bases bottom-up: Q (stored basis) and R factors
-  std::vector<Dm> Qb(nc), Rb(nc);
-  std::vector<int> lvl_ids_start;
   std::vector<std::vector<int>> levels(D + 1);
   for (int c = 0; c < nc; ++c) levels[t.level[c]].push_back(c);
-  const int* perm = t.perm;
-  for (int l = D; l >= (D == 0 ? 0 : 1); --l) {
+  const int lmin = D == 0 ? 0 : 1;
+
+  // 1. nested interpolation bases, orthonormalised bottom-up: V_c = Q_c R_c (leaf),
+  //    [R_c1 E_c1; R_c2 E_c2] = Q_c R_c (non-leaf; E = parent Lagrange polynomials at the child's nodes)
+  std::vector<Dm> Qb(nc), Rb(nc);
+  for (int l = D; l >= lmin; --l) {
     const auto& ids = levels[l];
     pfor(static_cast<int64_t>(ids.size()), threads, [&](int64_t q) {
       const int c = ids[q];
+      const Cheb& C = cb[c];
+      const int m = C.m, k = C.k();
       if (t.child0[c] < 0) {
         const int n = t.end[c] - t.begin[c];
         Dm V(n, k);
@@ -189,9 +333,9 @@ std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, 
           const double* x = &xyz[3 * perm[t.begin[c] + p]];
           double lx[64], ly[64], lz[64];
           for (int i = 0; i < m; ++i) {
-            lx[i] = lagrange(box[c], 0, i, m, x[0]);
-            ly[i] = lagrange(box[c], 1, i, m, x[1]);
-            lz[i] = lagrange(box[c], 2, i, m, x[2]);
+            lx[i] = C.lag(0, i, x[0]);
+            ly[i] = C.lag(1, i, x[1]);
+            lz[i] = C.lag(2, i, x[2]);
           }
           for (int iz = 0; iz < m; ++iz)
             for (int iy = 0; iy < m; ++iy)
@@ -204,18 +348,23 @@ std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, 
         Dm Z(r1 + r2, k);
         for (int s = 0; s < 2; ++s) {
           const int ch = s ? c2 : c1;
-          Dm E(k, k);  // E[nu', nu] = L^parent_nu(xi^child_nu')
-          for (int jz = 0; jz < m; ++jz)
-            for (int jy = 0; jy < m; ++jy)
-              for (int jx = 0; jx < m; ++jx) {
-                const double px = cheb_node(box[ch], 0, jx, m), py = cheb_node(box[ch], 1, jy, m),
-                             pz = cheb_node(box[ch], 2, jz, m);
+          const Cheb& H = cb[ch];
+          const int mh = H.m;
+          Dm E(H.k(), k);  // E[nu', nu] = L^parent_nu(xi^child_nu')
+          for (int jz = 0; jz < mh; ++jz)
+            for (int jy = 0; jy < mh; ++jy)
+              for (int jx = 0; jx < mh; ++jx) {
+                const double px = H.node(0, jx), py = H.node(1, jy), pz = H.node(2, jz);
+                double lx[64], ly[64], lz[64];
+                for (int i = 0; i < m; ++i) {
+                  lx[i] = C.lag(0, i, px);
+                  ly[i] = C.lag(1, i, py);
+                  lz[i] = C.lag(2, i, pz);
+                }
                 for (int iz = 0; iz < m; ++iz)
                   for (int iy = 0; iy < m; ++iy)
                     for (int ix = 0; ix < m; ++ix)
-                      E(jx + m * (jy + m * jz), ix + m * (iy + m * iz)) =
-                          lagrange(box[c], 0, ix, m, px) * lagrange(box[c], 1, iy, m, py) *
-                          lagrange(box[c], 2, iz, m, pz);
+                      E(jx + mh * (jy + mh * jz), ix + m * (iy + m * iz)) = lx[ix] * ly[iy] * lz[iz];
               }
           const Dm RE = matmul(Rb[ch], E);
           for (int j = 0; j < k; ++j)
@@ -225,17 +374,155 @@ std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, 
       }
     });
   }
+  tick("nested bases");
   // kernel value at distance r
-  auto G = [&](double r, double& re, double& im) {
+  auto G = [&](double r) -> S {
     const double f = 1.0 / (4.0 * M_PI * r);
-    if (!cplx) {
-      re = f;
-      im = 0.0;
-    } else {
-      re = f * std::cos(kappa * r);
-      im = -f * std::sin(kappa * r);
-    }
+    if constexpr (cplx)
+      return S(f * std::cos(kappa * r), -f * std::sin(kappa * r));
+    else
+      return S(f);
   };
+  (void)kernel;
+  // 2. couplings in the orthonormal coordinates: S_ts = R_t K(xi_t, xi_s) R_s^T (recomputed
+  //    when needed instead of stored: at 1M points the un-recompressed set would not fit in RAM)
+  std::vector<int64_t> adm;
+  for (int64_t q = 0; q < b.n_blocks; ++q)
+    if (b.kind[q] == H2C_ADMISSIBLE) adm.push_back(q);
+  auto nodes = [&](const Cheb& X) {
+    Dm xr(3, X.k());
+    for (int iz = 0; iz < X.m; ++iz)
+      for (int iy = 0; iy < X.m; ++iy)
+        for (int ix = 0; ix < X.m; ++ix) {
+          const int i = ix + X.m * (iy + X.m * iz);
+          xr(0, i) = X.node(0, ix), xr(1, i) = X.node(1, iy), xr(2, i) = X.node(2, iz);
+        }
+    return xr;
+  };
+  auto coupling_raw = [&](int64_t q) {
+    const int r = b.row[q], s = b.col[q];
+    const Dm xr = nodes(cb[r]), ys = nodes(cb[s]);
+    const int kr = xr.c, ks = ys.c;
+    const M<double> Rr = lift<double>(Rb[r]), Rs = lift<double>(Rb[s]);
+    // K stacked [Re K; Im K] (W k_r x k_s), X = K R_s^T, S = R_r X (per part)
+    M<double> K(W * kr, ks), X;
+    for (int j = 0; j < ks; ++j)
+      for (int i = 0; i < kr; ++i) {
+        const double dx = xr(0, i) - ys(0, j), dy = xr(1, i) - ys(1, j), dz = xr(2, i) - ys(2, j);
+        const S g = G(std::sqrt(dx * dx + dy * dy + dz * dz));
+        if constexpr (cplx) {
+          K(i, j) = g.real();
+          K(kr + i, j) = g.imag();
+        } else {
+          K(i, j) = g;
+        }
+      }
+    gemm(kN, kT, K, Rs, X);
+    M<S> out_s(Rr.r, Rs.r);
+    for (int part = 0; part < W; ++part) {
+      M<double> Xp(kr, Rs.r), Sp;
+      for (int j = 0; j < Rs.r; ++j)
+        std::copy(&X.d[size_t(j) * X.r + part * kr], &X.d[size_t(j) * X.r + part * kr + kr], &Xp.d[size_t(j) * kr]);
+      gemm(kN, kN, Rr, Xp, Sp);
+      for (size_t i = 0; i < Sp.d.size(); ++i) {
+        if constexpr (cplx)
+          out_s.d[i] += part ? S(0.0, Sp.d[i]) : S(Sp.d[i], 0.0);
+        else
+          out_s.d[i] = Sp.d[i];
+      }
+    }
+    return out_s;
+  };
+  scipy_openblas_set_num_threads(1);  // parallel over clusters / blocks instead
+
+  // 3. optional recompression (the reference's build_h2 rule, h2_matrix.cpp:83-121, applied to the
+  //    interpolation operand): the row Gram of cluster t over its far field (own admissible
+  //    partners plus those inherited from its ancestors, far_partners h2_matrix.cpp:22-46) is
+  //    V_t Z_t V_t^H with Z_t = sum_s S_ts S_ts^H + T_t Z_parent T_t^H (orthonormal V_t), so the
+  //    leaf basis is V_t * trunc(Z_t) and a parent's transfer is trunc(X Z_p X^H) with
+  //    X = [P_c1 T_c1; P_c2 T_c2], P_c = (new basis)^H (old basis).  The kernel and point sets are
+  //    symmetric, so the column basis equals the row basis and S'_ts = P_t S_ts P_s^T.
+  std::vector<M<S>> basis(nc), P(nc);  // final basis blocks (leaf n x k', transfer (k1'+k2') x k')
+  std::vector<uint8_t> dg(nc, 0);
+  const bool rc = eps_rc > 0;
+  if (rc) {
+    std::vector<std::vector<int64_t>> by_row(nc);
+    for (int64_t q : adm) by_row[b.row[q]].push_back(q);
+    std::vector<M<S>> Z(nc);
+    for (int l = lmin; l <= D; ++l) {
+      const auto& ids = levels[l];
+      pfor(static_cast<int64_t>(ids.size()), threads, [&](int64_t qi) {
+        const int c = ids[qi];
+        const int rk = Qb[c].c;
+        M<S> z(rk, rk);
+        for (int64_t q : by_row[c]) {
+          const M<S> Sq = coupling_raw(q);
+          gemm(kN, kC, Sq, Sq, z, true);
+        }
+        const int p = t.parent[c];
+        if (p >= 0 && t.level[p] >= lmin && Z[p].r > 0) {
+          // T_c = rows of Q_p belonging to child c
+          const int off = (t.child0[p] == c) ? 0 : Qb[t.child0[p]].c;
+          M<S> T(rk, Qb[p].c);
+          for (int j = 0; j < T.c; ++j)
+            for (int i = 0; i < rk; ++i) T(i, j) = S(Qb[p](off + i, j));
+          M<S> TZ;
+          gemm(kN, kN, T, Z[p], TZ);
+          gemm(kN, kC, TZ, T, z, true);
+        }
+        Z[c] = std::move(z);
+      });
+    }
+    tick("far-field Grams");
+    for (int l = D; l >= lmin; --l) {
+      const auto& ids = levels[l];
+      pfor(static_cast<int64_t>(ids.size()), threads, [&](int64_t qi) {
+        const int c = ids[qi];
+        bool deg = false;
+        if (t.child0[c] < 0) {
+          const M<S> U = truncate_gram(Z[c], eps_rc, deg);
+          gemm(kN, kN, lift<S>(Qb[c]), U, basis[c]);
+          M<S> Ph(U.c, U.r);
+          for (int i = 0; i < U.r; ++i)
+            for (int j = 0; j < U.c; ++j) {
+              if constexpr (cplx)
+                Ph(j, i) = std::conj(U(i, j));
+              else
+                Ph(j, i) = U(i, j);
+            }
+          P[c] = std::move(Ph);
+        } else {
+          const int c1 = t.child0[c], c2 = t.child1[c];
+          const int r1 = Qb[c1].c;
+          const int k1 = P[c1].r, k2 = P[c2].r;
+          M<S> X(k1 + k2, Qb[c].c);
+          for (int sd = 0; sd < 2; ++sd) {
+            const int ch = sd ? c2 : c1;
+            M<S> T(Qb[ch].c, Qb[c].c);
+            for (int j = 0; j < T.c; ++j)
+              for (int i = 0; i < T.r; ++i) T(i, j) = S(Qb[c]((sd ? r1 : 0) + i, j));
+            M<S> PT;
+            gemm(kN, kN, P[ch], T, PT);
+            for (int j = 0; j < X.c; ++j)
+              for (int i = 0; i < PT.r; ++i) X(i + (sd ? k1 : 0), j) = PT(i, j);
+          }
+          M<S> XZ, Gm;
+          gemm(kN, kN, X, Z[c], XZ);
+          gemm(kN, kC, XZ, X, Gm);
+          const M<S> U = truncate_gram(Gm, eps_rc, deg);
+          basis[c] = U;
+          gemm(kC, kN, U, X, P[c]);
+        }
+        dg[c] = deg ? 1 : 0;
+        Z[c] = M<S>();  // released once used
+      });
+    }
+    tick("truncation");
+  } else {
+    for (int c = 0; c < nc; ++c)
+      if (!(t.parent[c] < 0 && D > 0)) basis[c] = lift<S>(Qb[c]);
+  }
+
   // layout: bases (row == col, shared offsets), then blocks in global order
   int64_t total = 0;
   out->row_rank.assign(nc, 0);
@@ -243,9 +530,10 @@ std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, 
   out->row_off.assign(nc, -1);
   for (int c = 0; c < nc; ++c) {
     if (t.parent[c] < 0 && D > 0) continue;
-    out->row_rank[c] = Qb[c].c;
+    out->row_rank[c] = basis[c].c;
+    out->row_dg[c] = dg[c];
     out->row_off[c] = total;
-    total += int64_t(Qb[c].r) * Qb[c].c;
+    total += int64_t(basis[c].r) * basis[c].c;
   }
   out->block_off.assign(b.n_blocks, -1);
   for (int64_t q = 0; q < b.n_blocks; ++q) {
@@ -259,65 +547,40 @@ std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, 
     }
   }
   out->values.assign(size_t(total) * W, 0.0);
-  double* V = out->values.data();
+  S* V = reinterpret_cast<S*>(out->values.data());
   for (int c = 0; c < nc; ++c) {
     if (out->row_off[c] < 0) continue;
-    const Dm& Q = Qb[c];
-    for (int j = 0; j < Q.c; ++j)
-      for (int i = 0; i < Q.r; ++i) V[(out->row_off[c] + i + int64_t(j) * Q.r) * W] = Q(i, j);
+    std::copy(basis[c].d.begin(), basis[c].d.end(), V + out->row_off[c]);
   }
+  pfor(static_cast<int64_t>(adm.size()), threads, [&](int64_t a) {
+    const int64_t q = adm[a];
+    M<S> Sq = coupling_raw(q);
+    if (rc) {
+      M<S> PS;
+      gemm(kN, kN, P[b.row[q]], Sq, PS);
+      gemm(kN, kT, PS, P[b.col[q]], Sq);
+    }
+    std::copy(Sq.d.begin(), Sq.d.end(), V + out->block_off[q]);
+  });
+  tick("couplings");
   pfor(b.n_blocks, threads, [&](int64_t q) {
+    if (b.kind[q] != H2C_INADMISSIBLE_LEAF) return;
     const int r = b.row[q], s = b.col[q];
-    if (b.kind[q] == H2C_ADMISSIBLE) {
-      // S = kernel at node pairs, then R_r S R_s^T
-      Dm Sre(k, k), Sim(k, k);
-      for (int jz = 0; jz < m; ++jz)
-        for (int jy = 0; jy < m; ++jy)
-          for (int jx = 0; jx < m; ++jx) {
-            const double y[3] = {cheb_node(box[s], 0, jx, m), cheb_node(box[s], 1, jy, m),
-                                 cheb_node(box[s], 2, jz, m)};
-            const int jj = jx + m * (jy + m * jz);
-            for (int iz = 0; iz < m; ++iz)
-              for (int iy = 0; iy < m; ++iy)
-                for (int ix = 0; ix < m; ++ix) {
-                  const double x[3] = {cheb_node(box[r], 0, ix, m), cheb_node(box[r], 1, iy, m),
-                                       cheb_node(box[r], 2, iz, m)};
-                  const double d = std::sqrt((x[0] - y[0]) * (x[0] - y[0]) + (x[1] - y[1]) * (x[1] - y[1]) +
-                                             (x[2] - y[2]) * (x[2] - y[2]));
-                  double re, im;
-                  G(d, re, im);
-                  Sre(ix + m * (iy + m * iz), jj) = re;
-                  Sim(ix + m * (iy + m * iz), jj) = im;
-                }
-          }
-      const Dm& Rr = Rb[r];
-      const Dm& Rs = Rb[s];
-      Dm RsT(Rs.c, Rs.r);
-      for (int i = 0; i < Rs.r; ++i)
-        for (int j = 0; j < Rs.c; ++j) RsT(j, i) = Rs(i, j);
-      for (int part = 0; part < W; ++part) {
-        const Dm C = matmul(matmul(Rr, part ? Sim : Sre), RsT);
-        for (int j = 0; j < C.c; ++j)
-          for (int i = 0; i < C.r; ++i) V[(out->block_off[q] + i + int64_t(j) * C.r) * W + part] = C(i, j);
-      }
-    } else if (b.kind[q] == H2C_INADMISSIBLE_LEAF) {
-      const int nr = t.end[r] - t.begin[r], ns = t.end[s] - t.begin[s];
-      for (int j = 0; j < ns; ++j) {
-        const int pj = perm[t.begin[s] + j];
-        for (int i = 0; i < nr; ++i) {
-          const int pi = perm[t.begin[r] + i];
-          double re = diagonal, im = 0.0;
-          if (pi != pj) {
-            const double* x = &xyz[3 * pi];
-            const double* y = &xyz[3 * pj];
-            const double d = std::sqrt((x[0] - y[0]) * (x[0] - y[0]) + (x[1] - y[1]) * (x[1] - y[1]) +
-                                       (x[2] - y[2]) * (x[2] - y[2]));
-            if (d == 0.0) throw std::runtime_error("duplicate points");
-            G(d, re, im);
-          }
-          V[(out->block_off[q] + i + int64_t(j) * nr) * W] = re;
-          if (cplx) V[(out->block_off[q] + i + int64_t(j) * nr) * W + 1] = im;
+    const int nr = t.end[r] - t.begin[r], ns = t.end[s] - t.begin[s];
+    for (int j = 0; j < ns; ++j) {
+      const int pj = perm[t.begin[s] + j];
+      for (int i = 0; i < nr; ++i) {
+        const int pi = perm[t.begin[r] + i];
+        S v = S(diagonal);
+        if (pi != pj) {
+          const double* x = &xyz[3 * pi];
+          const double* y = &xyz[3 * pj];
+          const double d = std::sqrt((x[0] - y[0]) * (x[0] - y[0]) + (x[1] - y[1]) * (x[1] - y[1]) +
+                                     (x[2] - y[2]) * (x[2] - y[2]));
+          if (d == 0.0) throw std::runtime_error("duplicate points");
+          v = G(d);
         }
+        V[out->block_off[q] + i + int64_t(j) * nr] = v;
       }
     }
   });
@@ -325,6 +588,17 @@ std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, 
   out->col_dg = out->row_dg;
   out->col_off = out->row_off;
   return out;
+}
+
+}  // namespace
+
+std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, const double* xyz, int kernel,
+                                        double kappa, double diagonal, const int* orders, double eps_recompress,
+                                        int threads) {
+  if (!(eps_recompress >= 0.0 && eps_recompress < 1.0)) throw std::invalid_argument("eps_recompress must be in [0,1)");
+  if (kernel == 1) return chebyshev_impl<std::complex<double>>(t, b, xyz, kernel, kappa, diagonal, orders,
+                                                               eps_recompress, threads);
+  return chebyshev_impl<double>(t, b, xyz, kernel, kappa, diagonal, orders, eps_recompress, threads);
 }
 
 std::unique_ptr<HostH2> build_fd_laplacian(const h2c_tree& t, const h2c_blocks& b, const double* xyz, double h) {

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <cuda.h>
 #include <cusolverDn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -663,7 +664,15 @@ struct EngineRun {
   bool profiling = false;
   std::string phase = "setup";
   std::vector<ProfRec> prof;
+  // H2B_NVTX=1: one NVTX range "<phase>:<kernel>" per launch, so ncu can select the
+  // launches of one phase (ncu --nvtx --nvtx-include "L9.targets:seg_gemm]")
+  const bool nvtx = std::getenv("H2B_NVTX") != nullptr;
+  int nvtx_depth = 0;
   void pre(const char* kernel, int64_t macs) {
+    if (nvtx) {
+      nvtxRangePushA((phase + ":" + kernel).c_str());
+      ++nvtx_depth;
+    }
     if (!profiling) return;
     ProfRec r{phase, kernel, macs, nullptr, nullptr};
     CK(cudaEventCreate(&r.a));
@@ -699,6 +708,10 @@ struct EngineRun {
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess)
         throw CudaError(std::string("CUDA error in phase ") + phase + ": " + cudaGetErrorString(e));
+    }
+    if (nvtx_depth > 0) {
+      nvtxRangePop();
+      --nvtx_depth;
     }
     if (!profiling) return;
     CK(cudaEventRecord(prof.back().b, s));

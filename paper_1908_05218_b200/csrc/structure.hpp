@@ -34,8 +34,9 @@ struct HostH2 {
   void desc(h2c_matrix* d) const;
 };
 
+// orders: interpolation order per level (depth + 1 entries)
 std::unique_ptr<HostH2> build_chebyshev(const h2c_tree& t, const h2c_blocks& b, const double* xyz, int kernel,
-                                        double kappa, double diagonal, int order, double eps_recompress,
+                                        double kappa, double diagonal, const int* orders, double eps_recompress,
                                         int threads);
 std::unique_ptr<HostH2> build_fd_laplacian(const h2c_tree& t, const h2c_blocks& b, const double* xyz, double h);
 

@@ -392,6 +392,9 @@ def lib() -> C.CDLL:
         L.h2c_build_chebyshev.restype = C.c_void_p
         L.h2c_build_chebyshev.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_int, C.c_double,
                                           C.c_double, C.c_int, C.c_double, C.c_int]
+        L.h2c_build_chebyshev_orders.restype = C.c_void_p
+        L.h2c_build_chebyshev_orders.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_int,
+                                                 C.c_double, C.c_double, C.POINTER(C.c_int32), C.c_double, C.c_int]
         L.h2c_build_fd_laplacian.restype = C.c_void_p
         L.h2c_build_fd_laplacian.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_double]
         L.h2c_h2_desc.argtypes = [C.c_void_p, C.POINTER(h2c_matrix)]

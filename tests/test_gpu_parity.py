@@ -352,6 +352,21 @@ def test_cfg5_like_helmholtz_chebyshev(ctx):
     assert rel(cg, dense) <= 1.1 * rel(co, dense) + 1e-13
 
 
+@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def test_bench_constructions_at_oracle_sizes(ctx, name):
+    """bench.py's configs[2] / configs[4] constructions (recompressed plates x jittered plates;
+    complex Helmholtz on the Fibonacci sphere with orders growing per level, recompressed at
+    1e-4) at N = 4096, against the oracle and the dense product."""
+    import bench
+    _, _, _, A, B = bench.build_operands(name, 4096)
+    eps = bench.CONFIGS[name][3]
+    got, ref, cg, co = check_against_oracle(A, B, eps, ctx)
+    dense = O.h2_to_dense(A) @ O.h2_to_dense(B)
+    assert rel(cg, dense) <= 1.1 * rel(co, dense) + 1e-13
+    if name == "cfg5":
+        assert A.scalar == P.H2C_COMPLEX
+
+
 # ---- exact H^2 MVP on the device (h2_matrix.cpp:213-278) and eps_rel (metrics.cpp:37-55)
 @pytest.mark.parametrize("kind", ["real", "complex"])
 def test_mvp_matches_oracle(ctx, kind):

@@ -128,6 +128,67 @@ def test_chebyshev_operand_is_orthonormal_nested_and_accurate():
     assert np.linalg.norm(O.h2_to_dense(A) - d) / np.linalg.norm(d) < 2e-3
 
 
+def _fib_sphere(n, radius):
+    i = np.arange(n) + 0.5
+    phi = np.arccos(1 - 2 * i / n)
+    th = np.pi * (1 + 5 ** 0.5) * i
+    return radius * np.stack([np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)], 1)
+
+
+def _max_orth_defect(A, t):
+    return max(np.abs(A.row_basis(c).conj().T @ A.row_basis(c) - np.eye(A.row_rank[c])).max()
+               for c in range(t.n_clusters) if t.parent[c] >= 0)
+
+
+@pytest.mark.parametrize("eps", [1e-4, 1e-6, 1e-8])
+def test_recompressed_chebyshev_follows_build_h2_rule(eps):
+    """Recompression (build_h2's far-field Gram rule, h2_matrix.cpp:83-121) of the interpolation
+    operand: orthonormal nested bases, ranks no larger than the interpolation rank, and the
+    operand stays within ~sqrt(eps) (Gram-eigenvalue threshold) of the un-recompressed one."""
+    pts = P.random_cloud(2048, 1)
+    t = P.build_cluster_tree(pts, 32)
+    s = P.build_block_tree(t, t, 1.0)
+    A0 = P.build_chebyshev(t, s, pts, 3)
+    A = P.build_chebyshev(t, s, pts, 3, eps_recompress=eps)
+    assert _max_orth_defect(A, t) < 1e-12
+    assert A.row_rank.max() <= 27 and A.row_rank[t.parent >= 0].min() >= 1
+    d0 = O.h2_to_dense(A0)
+    err = np.linalg.norm(O.h2_to_dense(A) - d0) / np.linalg.norm(d0)
+    assert err < 30 * np.sqrt(eps), err
+    # tighter eps never lowers a rank
+    if eps > 1e-8:
+        A2 = P.build_chebyshev(t, s, pts, 3, eps_recompress=eps * 1e-2)
+        assert (A2.row_rank >= A.row_rank).all()
+
+
+def test_variable_order_helmholtz_chebyshev():
+    """Orders per level (growing toward the root) for the complex Helmholtz operand, with and
+    without recompression; the operand approximates exp(-i k r)/(4 pi r)."""
+    sph = _fib_sphere(2048, 2.0)
+    t = P.build_cluster_tree(sph, 64)
+    s = P.build_block_tree(t, t, 1.0)
+    orders = [5] * (t.depth + 1)
+    orders[-1] = 4
+    kappa = 2 * np.pi
+    A0 = P.build_chebyshev(t, s, sph, orders, kernel="helmholtz", kappa=kappa)
+    assert A0.scalar == P.H2C_COMPLEX
+    leaf = t.child0 < 0
+    assert set(A0.row_rank[leaf].tolist()) == {64} and A0.row_rank[(~leaf) & (t.parent >= 0)].max() == 125
+    r = np.linalg.norm(sph[:, None, :] - sph[None, :, :], axis=2)
+    np.fill_diagonal(r, 1.0)
+    dense = np.exp(-1j * kappa * r) / (4 * np.pi * r)
+    np.fill_diagonal(dense, 0.0)
+    e0 = np.linalg.norm(O.h2_to_dense(A0) - dense) / np.linalg.norm(dense)
+    assert e0 < 0.1, e0
+    A = P.build_chebyshev(t, s, sph, orders, kernel="helmholtz", kappa=kappa, eps_recompress=1e-8)
+    assert _max_orth_defect(A, t) < 1e-12
+    assert A.row_rank.max() < 125
+    e = np.linalg.norm(O.h2_to_dense(A) - O.h2_to_dense(A0)) / np.linalg.norm(dense)
+    assert e < 1e-3, e
+    with pytest.raises(P.ConfigError):
+        P.build_chebyshev(t, s, sph, orders[:-1], kernel="helmholtz", kappa=kappa)
+
+
 def test_fd_laplacian_operand_is_the_stencil():
     m = 8
     h = 1.0 / (m + 1)
