@@ -2373,9 +2373,25 @@ const Plan& Context::plan_for(const h2c_tree& t, const h2c_blocks& b, double* bu
   return *plan_;
 }
 
+// binds the context's arena to this thread for the duration of a call
+struct ArenaScope {
+  Arena* prev_a;
+  cudaStream_t prev_s;
+  ArenaScope(Arena* a, cudaStream_t s) : prev_a(t_arena), prev_s(t_arena_stream) {
+    t_arena = a;
+    t_arena_stream = s;
+  }
+  ~ArenaScope() {
+    t_arena = prev_a;
+    t_arena_stream = prev_s;
+  }
+};
+
 std::shared_ptr<DevOperand> Context::upload(const h2c_matrix& m) {
   double bs = 0;
   const Plan& P = plan_for(*m.tree, *m.blocks, &bs);
+  // resident operands live in the context's arena too (it holds nearly all free HBM once created)
+  ArenaScope scope(arena(), static_cast<cudaStream_t>(stream_));
   auto X = upload_operand(P, m, static_cast<cudaStream_t>(stream_), &launches_);
   X->key = plan_key_;
   return X;
@@ -2418,19 +2434,6 @@ static void fill_report(const Plan& P, const DevOperand& A, const DevOperand& B,
   }
 }
 
-// binds the context's arena to this thread for the duration of a call
-struct ArenaScope {
-  Arena* prev_a;
-  cudaStream_t prev_s;
-  ArenaScope(Arena* a, cudaStream_t s) : prev_a(t_arena), prev_s(t_arena_stream) {
-    t_arena = a;
-    t_arena_stream = s;
-  }
-  ~ArenaScope() {
-    t_arena = prev_a;
-    t_arena_stream = prev_s;
-  }
-};
 
 Arena* Context::arena() {
   if (!arena_tried_) {
