@@ -499,6 +499,14 @@ struct DevOperand {
   std::vector<DBuf> Tr, Tc, S;
 };
 
+// scalars per host<->device staging batch (H2B_STAGE_SCALARS overrides; tests use a tiny value
+// to exercise the batching)
+static int64_t stage_scalars() {
+  const char* e = std::getenv("H2B_STAGE_SCALARS");
+  const long long v = e ? std::atoll(e) : 0;
+  return v > 0 ? v : (int64_t(1) << 27);
+}
+
 struct CopyList {
   std::vector<CopyJob> jobs;
   void add(const double* src, double* dst, int rows, int cols, int sld, int dld) {
@@ -575,11 +583,20 @@ static std::shared_ptr<DevOperand> upload_operand(const Plan& P, const h2c_matri
   for (int l = 0; l <= D; ++l)
     X->S[l].alloc(size_t(P.lv[l].adm.size()) * X->Kr[l] * X->Kc[l] * W, s, true);
 
-  DBuf raw(size_t(m.n_values) * W, s);
-  if (m.n_values)
-    CK(cudaMemcpyAsync(raw.p, m.values, size_t(m.n_values) * W * sizeof(double), cudaMemcpyHostToDevice, s));
-  CopyList cl;
-  auto src = [&](int64_t off) { return raw.p + off * W; };
+  // copy jobs with HOST source offsets (scalars into m.values), executed in staged chunks below
+  struct HJob {
+    int64_t off;
+    double* dst;
+    int rows, cols, sld, dld;
+  };
+  std::vector<HJob> hj;
+  struct {
+    std::vector<HJob>* v;
+    void add(int64_t off, double* dst, int rows, int cols, int sld, int dld) {
+      if (rows > 0 && cols > 0) v->push_back({off, dst, rows, cols, sld, dld});
+    }
+  } cl{&hj};
+  auto src = [&](int64_t off) { return off; };
   for (int p = 0; p < LL.n; ++p) {
     const int id = LL.id[p];
     if (m.row_offset[id] >= 0)
@@ -619,8 +636,32 @@ static std::shared_ptr<DevOperand> upload_operand(const Plan& P, const h2c_matri
     const int nr = LL.size[LL.brow[b]], nc = LL.size[LL.bcol[b]];
     if (off >= 0) cl.add(src(off), X->F.p + q * size_t(NL) * NL * W, nr, nc, nr, NL);
   }
-  cl.run(s, W, launches);
-  CK(cudaStreamSynchronize(s));  // `raw` and the job list die here
+  // Stage the host values through a bounded device buffer (<= 1 GiB per batch of jobs sorted by
+  // source offset) instead of one copy of the whole operand: the padded layout is all that stays
+  // resident, and no allocation of the operand's full size is needed twice (2^20-point operands
+  // are ~35 GB).
+  std::sort(hj.begin(), hj.end(), [](const HJob& x, const HJob& y) { return x.off < y.off; });
+  const int64_t cap = stage_scalars();  // scalars per staging batch (1 GiB real)
+  auto extent = [](const HJob& j) { return int64_t(j.cols - 1) * j.sld + j.rows; };
+  int64_t span_max = 0;
+  for (const HJob& j : hj) span_max = std::max(span_max, extent(j));
+  DBuf stage(size_t(std::max(cap, span_max)) * W, s);
+  for (size_t i = 0; i < hj.size();) {
+    const int64_t o0 = hj[i].off;
+    int64_t o1 = o0 + extent(hj[i]);
+    size_t e = i + 1;
+    while (e < hj.size() && std::max(o1, hj[e].off + extent(hj[e])) - o0 <= std::max(cap, span_max)) {
+      o1 = std::max(o1, hj[e].off + extent(hj[e]));
+      ++e;
+    }
+    CK(cudaMemcpyAsync(stage.p, m.values + o0 * W, size_t(o1 - o0) * W * sizeof(double), cudaMemcpyHostToDevice, s));
+    CopyList dl;
+    for (size_t q = i; q < e; ++q)
+      dl.add(stage.p + (hj[q].off - o0) * W, hj[q].dst, hj[q].rows, hj[q].cols, hj[q].sld, hj[q].dld);
+    dl.run(s, W, launches);
+    CK(cudaStreamSynchronize(s));  // the staging buffer is reused by the next batch
+    i = e;
+  }
   return X;
 }
 
@@ -720,6 +761,7 @@ struct EngineRun {
   const bool debug_check = std::getenv("H2B_DEBUG_CHECK") != nullptr;
   // solver selection knobs (A/B): library solver also for n <= 64; packed Jacobi for 64 < n <= 224
   const bool force_library = std::getenv("H2B_EIG_LIBRARY") != nullptr;
+  const bool jacobi_v_global = std::getenv("H2B_JACOBI_V") != nullptr;
   const bool use_packed = std::getenv("H2B_EIG_PACKED") != nullptr;
 
   // C
@@ -1110,12 +1152,26 @@ struct EngineRun {
     const size_t smem = size_t(2) * n * (n + 1) * W * sizeof(double);
     if (n <= kJacobiMaxN && !force_library) {
       pre("jacobi_eig", 0);
-      if (cplx) {
-        CK(cudaFuncSetAttribute(jacobi_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        jacobi_kernel<true, true><<<count, 256, smem, s>>>(jp);
+      // H2B_JACOBI_V=global: eigenvectors in a global (L2-resident) scratch, halving the shared
+      // memory per CTA (more CTAs per SM)
+      DBuf vscr;
+      if (jacobi_v_global) {
+        vscr.alloc(size_t(count) * n * (n + 1) * W, s);
+        jp.scratch = vscr.p;
+        const size_t sm1 = smem / 2;
+        if (cplx) {
+          CK(cudaFuncSetAttribute(jacobi_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+          jacobi_kernel<true, 2><<<count, 256, sm1, s>>>(jp);
+        } else {
+          CK(cudaFuncSetAttribute(jacobi_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+          jacobi_kernel<false, 2><<<count, 256, sm1, s>>>(jp);
+        }
+      } else if (cplx) {
+        CK(cudaFuncSetAttribute(jacobi_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        jacobi_kernel<true, 1><<<count, 256, smem, s>>>(jp);
       } else {
-        CK(cudaFuncSetAttribute(jacobi_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        jacobi_kernel<false, true><<<count, 256, smem, s>>>(jp);
+        CK(cudaFuncSetAttribute(jacobi_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        jacobi_kernel<false, 1><<<count, 256, smem, s>>>(jp);
       }
       CK(cudaGetLastError());
       post();
@@ -2177,16 +2233,37 @@ struct EngineRun {
         total += int64_t(nr) * ncl;
       }
     }
-    DBuf flat(size_t(total) * W, s);
-    for (const Job& j : jobs) cl.add(j.src, flat.p + j.dst * W, j.rows, j.cols, j.sld, j.dld);
-    int64_t dl = 0;
-    cl.run(s, W, &dl);
-    launches += dl;
+    (void)cl;
     out.n_values = total;
     out.pool = ctx.pinned;
     out.values = out.pool->take(std::max<size_t>(1, size_t(total) * W * sizeof(double)), &out.values_bytes);
-    if (total)
-      CK(cudaMemcpyAsync(out.values, flat.p, size_t(total) * W * sizeof(double), cudaMemcpyDeviceToHost, s));
+    // pack into the flat layout through a bounded device buffer (jobs are in destination order),
+    // so the download never needs one allocation of C's full size next to the run's buffers
+    auto dext = [](const Job& j) { return int64_t(j.cols - 1) * j.dld + j.rows; };  // span in the flat array
+    int64_t span_max = 0;
+    for (const Job& j : jobs) span_max = std::max(span_max, dext(j));
+    const int64_t cap = std::max<int64_t>(stage_scalars(), span_max);  // scalars per batch
+    // (+ span_max: a job whose span interleaves with the previous one's - the two halves of a
+    // stacked transfer - always joins its batch)
+    DBuf flat(size_t(std::min<int64_t>(std::max<int64_t>(total, 1), cap + span_max)) * W, s);
+    int64_t dl = 0;
+    for (size_t i = 0; i < jobs.size();) {
+      const int64_t d0 = jobs[i].dst;
+      size_t e = i;
+      int64_t d1 = d0;
+      while (e < jobs.size() && (jobs[e].dst < d1 || std::max(d1, jobs[e].dst + dext(jobs[e])) - d0 <= cap)) {
+        d1 = std::max(d1, jobs[e].dst + dext(jobs[e]));
+        ++e;
+      }
+      CopyList bl;
+      for (size_t q = i; q < e; ++q)
+        bl.add(jobs[q].src, flat.p + (jobs[q].dst - d0) * W, jobs[q].rows, jobs[q].cols, jobs[q].sld, jobs[q].dld);
+      bl.run(s, W, &dl);
+      CK(cudaMemcpyAsync(out.values + d0 * W, flat.p, size_t(d1 - d0) * W * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));  // `flat` is reused by the next batch
+      i = e;
+    }
+    launches += dl;
     CK(cudaStreamSynchronize(s));
   }
 };

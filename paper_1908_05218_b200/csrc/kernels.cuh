@@ -1042,7 +1042,9 @@ struct JacobiParams {
   int max_sweeps;
 };
 
-template <bool CPLX, bool SMEM>
+// MODE 1: A and V in shared memory; 2: A in shared memory, V in global scratch (half the
+// shared memory -> more CTAs per SM); 0: both in global scratch
+template <bool CPLX, int MODE>
 __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
   constexpr int W = CPLX ? 2 : 1;
   const int n = p.n, ld = n + 1;
@@ -1050,9 +1052,12 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const JacobiParams p) {
   extern __shared__ __align__(16) double jsm[];
   double* A;
   double* V;
-  if constexpr (SMEM) {
+  if constexpr (MODE == 1) {
     A = jsm;
     V = jsm + (size_t)n * ld * W;
+  } else if constexpr (MODE == 2) {
+    A = jsm;
+    V = p.scratch + (size_t)b * n * ld * W;
   } else {
     A = p.scratch + (size_t)b * 2 * n * ld * W;
     V = A + (size_t)n * ld * W;
