@@ -760,7 +760,10 @@ struct EngineRun {
   const bool debug_sync = std::getenv("H2B_DEBUG_SYNC") != nullptr;
   const bool debug_check = std::getenv("H2B_DEBUG_CHECK") != nullptr;
   // solver selection knobs (A/B): library solver also for n <= 64; packed Jacobi for 64 < n <= 224
-  const bool force_library = std::getenv("H2B_EIG_LIBRARY") != nullptr;
+  // batched library solver for every Gram size by default (A/B: 1.75x faster than the CTA-resident
+  // Jacobi on cfg5s's 64 x 64 complex leaf Grams, 2% on cfg2); H2B_EIG_JACOBI=1 selects the Jacobi
+  // kernel for n <= 64
+  const bool force_library = std::getenv("H2B_EIG_JACOBI") == nullptr;
   const bool jacobi_v_global = std::getenv("H2B_JACOBI_V") != nullptr;
   const bool use_packed = std::getenv("H2B_EIG_PACKED") != nullptr;
 
@@ -2641,8 +2644,13 @@ void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adap
   const Plan& P = plan_for(*a.tree, *a.blocks, &plan_s);
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
   int64_t up_launches = 0;
+  const bool trace = std::getenv("H2B_E2E_TRACE") != nullptr;  // host-side phase times on stderr
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](auto a0, auto a1) { return std::chrono::duration<double>(a1 - a0).count(); };
+  const auto tu0 = now();
   auto A = upload_operand(P, a, s, &up_launches);
   std::shared_ptr<DevOperand> B = (&a == &b || a.values == b.values) ? A : upload_operand(P, b, s, &up_launches);
+  const auto tu1 = now();
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -2651,8 +2659,13 @@ void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adap
   R.profiling = profile;
   R.run();
   CK(cudaEventRecord(e1, s));
+  if (trace) CK(cudaStreamSynchronize(s));
+  const auto tr1 = now();
   std::vector<double*> pool;
   R.download(*a.blocks, out, pool);
+  if (trace)
+    std::fprintf(stderr, "[e2e] plan %.3f s  upload %.3f s  run %.3f s  download %.3f s\n", plan_s, secs(tu0, tu1),
+                 secs(tu1, tr1), secs(tr1, now()));
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);

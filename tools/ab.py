@@ -25,7 +25,7 @@ else:
     s = P.build_block_tree(t, t, 1.0)
     A = B = P.build_chebyshev(t, s, pts, order)
     specs = sys.argv[5:]
-KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_SEG_V2", "H2B_EIG_LIBRARY", "H2B_SEG_CFG", "H2B_NO_STRIPS",
+KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_SEG_V2", "H2B_EIG_JACOBI", "H2B_EIG_LIBRARY", "H2B_SEG_CFG", "H2B_NO_STRIPS",
          "H2B_EIG_PACKED", "H2B_JACOBI_V")
 for spec in specs:
     label, _, kv = spec.partition(":")
