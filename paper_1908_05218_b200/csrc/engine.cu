@@ -703,6 +703,9 @@ struct EngineRun {
     cudaEvent_t a, b;
   };
   bool profiling = false;
+  // H2B_PROF_SHAPES=1: profile entries keyed by launch shape too (M x N, inner dims, entries)
+  const bool prof_shapes = std::getenv("H2B_PROF_SHAPES") != nullptr;
+  std::string shape_tag;
   std::string phase = "setup";
   std::vector<ProfRec> prof;
   // H2B_NVTX=1: one NVTX range "<phase>:<kernel>" per launch, so ncu can select the
@@ -715,7 +718,8 @@ struct EngineRun {
       ++nvtx_depth;
     }
     if (!profiling) return;
-    ProfRec r{phase, kernel, macs, nullptr, nullptr};
+    ProfRec r{phase + shape_tag, kernel, macs, nullptr, nullptr};
+    shape_tag.clear();
     CK(cudaEventCreate(&r.a));
     CK(cudaEventCreate(&r.b));
     CK(cudaEventRecord(r.a, s));
@@ -1004,6 +1008,15 @@ struct EngineRun {
     int64_t macs = 0;
     for (const Grp& g : gs) macs += (g.csr ? g.csr->entries : n_out) * int64_t(M) * N * g.K;
     if (sym) macs = macs / 2 + macs / (2 * ((M + 63) / 64));
+    if (profiling && prof_shapes) {
+      shape_tag = " [" + std::to_string(M) + "x" + std::to_string(N) + " K";
+      int64_t ent = 0;
+      for (const Grp& g : gs) {
+        shape_tag += ":" + std::to_string(g.K);
+        ent += g.csr ? g.csr->entries : n_out;
+      }
+      shape_tag += " e/out " + std::to_string(ent / std::max(1, n_out)) + " out " + std::to_string(n_out) + "]";
+    }
     pre("seg_gemm", macs);
     if (seg_wide && !seg_v1 && !sym && (M > 64 || N > 64)) {
       const int tm = M > 64 ? 128 : 64, tn = N > 64 ? 128 : 64;
@@ -1048,6 +1061,20 @@ struct EngineRun {
     post();
   }
   const bool no_strips = std::getenv("H2B_NO_STRIPS") != nullptr;  // A/B: single launch per product
+  // v4 (warps split the chunks of small output tiles): H2B_SEG_V4=1 enables
+  const bool seg_v4 = std::getenv("H2B_SEG_V4") != nullptr;
+  template <int TM, int TN>
+  void launch_seg4(const SegParams& sp, int tiles) {
+    dim3 grid(sp.n_out, tiles);
+    auto go = [&](auto kern, int sm) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      kern<<<grid, 128, sm, s>>>(sp);
+    };
+    if (cplx) go(seg_gemm4_kernel<TM, TN, true>, Seg4Cfg<TM, TN, true>::SMEM);
+    else go(seg_gemm4_kernel<TM, TN, false>, Seg4Cfg<TM, TN, false>::SMEM);
+    CK(cudaGetLastError());
+    launches++;
+  }
   void launch_tiles(const SegParams& sp) {
     const int M = sp.M, N = sp.N;
     const bool v3 = !seg_v1 && !seg_v2;
@@ -1055,6 +1082,23 @@ struct EngineRun {
     const int TN = (N <= 8 && v3) ? 8 : N <= 16 ? 16 : (N <= 32 ? 32 : 64);
     const int tm_ = (M + TM - 1) / TM;
     const int tiles = sp.sym ? tm_ * (tm_ + 1) / 2 : tm_ * ((N + TN - 1) / TN);
+    if (seg_v4 && v3 && TM <= 32 && TN <= 32) {
+      bool k8 = true;
+      for (int g = 0; g < sp.ngroups; ++g) k8 = k8 && sp.g[g].K % 8 == 0;
+      if (k8) {
+        switch (TM * 100 + TN) {
+          case 808: launch_seg4<8, 8>(sp, tiles); return;
+          case 816: launch_seg4<8, 16>(sp, tiles); return;
+          case 832: launch_seg4<8, 32>(sp, tiles); return;
+          case 1608: launch_seg4<16, 8>(sp, tiles); return;
+          case 1616: launch_seg4<16, 16>(sp, tiles); return;
+          case 1632: launch_seg4<16, 32>(sp, tiles); return;
+          case 3208: launch_seg4<32, 8>(sp, tiles); return;
+          case 3216: launch_seg4<32, 16>(sp, tiles); return;
+          default: launch_seg4<32, 32>(sp, tiles); return;
+        }
+      }
+    }
     if (TM == 8 || TN == 8) {
       if (TM == 8 && TN == 8) launch_seg8<8, 8, 1, 1>(sp, tiles);
       else if (TM == 8 && TN == 16) launch_seg8<8, 16, 1, 2>(sp, tiles);

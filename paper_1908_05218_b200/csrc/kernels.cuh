@@ -906,6 +906,313 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
 }
 
 // ---------------------------------------------------------------------------
+// seg_gemm v4 (small output tiles, TM, TN <= 32): the NW warps of the CTA split the
+// k-CHUNKS of the segment instead of the output tile.  A pipeline stage holds NW
+// consecutive chunks of one group; warp w multiplies chunk w of the stage into its own
+// copy of the whole TM x TN accumulator, so one barrier covers NW chunks of MMA work
+// (v3 with 2x2 warps on a 16 x 16 tile issues 2 DMMAs per warp per barrier).  The NW
+// partial tiles are summed in a fixed order at the end (deterministic).  Copy geometry
+// and layout-specialised fragment loads are v3's.
+template <int TM, int TN, bool CPLX, int NW = 4, int ST_ = 3>
+struct Seg4Cfg {
+  using B = Seg2Cfg<TM, TN, CPLX, 8, ST_, 1, 1>;
+  static constexpr int NT = 32 * NW;
+  static constexpr int CH = B::STAGE;       // doubles per chunk slot
+  static constexpr int STG = NW * CH;       // doubles per stage
+  static constexpr int PIPE = ST_ * STG;
+  static constexpr int RED = NW * TM * TN * B::W;
+  static constexpr int SMEM = (PIPE > RED ? PIPE : RED) * 8;
+};
+
+template <int TM, int TN, bool CPLX, int NW = 4, int ST_ = 3>
+__global__ void __launch_bounds__(32 * NW) seg_gemm4_kernel(const SegParams p) {
+  using Q = Seg4Cfg<TM, TN, CPLX, NW, ST_>;
+  using C = typename Q::B;
+  constexpr int NT = Q::NT, ST = ST_;
+  constexpr int KC = C::KC, W = C::W;
+  constexpr int EPS = CPLX ? 1 : 2;  // elements per 16-byte copy
+  constexpr int LSEG = TM * KC / EPS, RSEG = TN * KC / EPS;
+  constexpr int LPT = (LSEG + NT - 1) / NT, RPT = (RSEG + NT - 1) / NT;
+  constexpr int FM = TM / 8, FN = TN / 8;
+  extern __shared__ __align__(16) double smem[];
+
+  const int t = blockIdx.x;
+  int m0, n0;
+  if (p.sym) {
+    const int y = blockIdx.y;
+    int tm = (int)((sqrt(8.0 * y + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= y) ++tm;
+    while (tm * (tm + 1) / 2 > y) --tm;
+    m0 = tm * TM;
+    n0 = (y - tm * (tm + 1) / 2) * TN;
+  } else {
+    const int tilesM = (p.M + TM - 1) / TM;
+    m0 = (blockIdx.y % tilesM) * TM;
+    n0 = (blockIdx.y / tilesM) * TN;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  double acc[FM][FN][2];
+  double acci[CPLX ? FM : 1][CPLX ? FN : 1][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if constexpr (CPLX) {
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) acci[i][j][0] = acci[i][j][1] = 0.0;
+  }
+
+  // ---- producer state (v3's) ----------------------------------------------
+  int ig = 0, ie = 0, ie1 = 0, ikc = 0, inkc = 1;
+  bool iv = false;
+  const double* lsrc[LPT];
+  const double* rsrc[RPT];
+  int ldst[LPT], rdst[RPT], loff[LPT], roff[RPT];
+  bool lok[LPT], rok[RPT];
+  long long lstep = 0, rstep = 0;
+  auto range = [&](int g, int& e0, int& e1) {
+    const int* ptr = p.g[g].ptr;
+    if (ptr) {
+      e0 = ptr[t];
+      e1 = ptr[t + 1];
+    } else {
+      e0 = 0;
+      e1 = 1;
+    }
+  };
+  auto setup_group = [&](int g) {
+    const SegGroup& G = p.g[g];
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int sgi = tid + j * NT;
+      int m, k;
+      if (!lt) {
+        k = sgi / (TM / EPS);
+        m = (sgi % (TM / EPS)) * EPS;
+      } else {
+        m = sgi / (KC / EPS);
+        k = (sgi % (KC / EPS)) * EPS;
+      }
+      lok[j] = sgi < LSEG && m0 + m < p.M;
+      loff[j] = lt ? (k + (m0 + m) * G.Lld) : (m0 + m + k * G.Lld);
+      ldst[j] = (lt ? m * (KC + 4) + k : k * (TM + 4) + m) * W;
+    }
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int sgi = tid + j * NT;
+      int n, k;
+      if (rt) {
+        k = sgi / (TN / EPS);
+        n = (sgi % (TN / EPS)) * EPS;
+      } else {
+        n = sgi / (KC / EPS);
+        k = (sgi % (KC / EPS)) * EPS;
+      }
+      rok[j] = sgi < RSEG && n0 + n < p.N;
+      roff[j] = rt ? (n0 + n + k * G.Rld) : (k + (n0 + n) * G.Rld);
+      rdst[j] = (rt ? k * (TN + 4) + n : n * (KC + 4) + k) * W;
+    }
+    lstep = (lt ? (long long)KC : (long long)KC * G.Lld) * W;
+    rstep = (rt ? (long long)KC * G.Rld : (long long)KC) * W;
+    inkc = G.K / KC;
+  };
+  auto setup_entry = [&]() {
+    const SegGroup& G = p.g[ig];
+    int l, r;
+    if (G.ptr) {
+      l = G.li[ie];
+      r = G.ri[ie];
+    } else {
+      l = G.li ? G.li[t] : t;
+      r = G.ri ? G.ri[t] : t;
+    }
+    const double* Lp = G.L + (G.Ls * l + G.Loff) * W;
+    const double* Rp = G.R + (G.Rs * r + G.Roff) * W;
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) lsrc[j] = Lp + (long long)loff[j] * W;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) rsrc[j] = Rp + (long long)roff[j] * W;
+    ikc = 0;
+  };
+  auto next_group = [&](int g) {
+    for (; g < p.ngroups; ++g) {
+      range(g, ie, ie1);
+      if (ie < ie1) {
+        ig = g;
+        setup_group(g);
+        setup_entry();
+        return true;
+      }
+    }
+    return false;
+  };
+  // one stage = up to NW consecutive chunks of ONE group (a group's first chunk always
+  // opens a fresh stage, so producer and consumer partition every group identically)
+  auto issue = [&](int stage) {
+    if (iv) {
+      const int g0 = ig;
+#pragma unroll 1
+      for (int q = 0; q < NW; ++q) {
+        if (!iv || ig != g0) break;
+        double* Ls = smem + stage * Q::STG + q * Q::CH;
+        double* Rs = Ls + C::LSZ;
+#pragma unroll
+        for (int j = 0; j < LPT; ++j) {
+          if (lok[j]) cp_async16(Ls + ldst[j], lsrc[j], true);
+          lsrc[j] += lstep;
+        }
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          if (rok[j]) cp_async16(Rs + rdst[j], rsrc[j], true);
+          rsrc[j] += rstep;
+        }
+        if (++ikc == inkc) {
+          if (++ie < ie1) setup_entry();
+          else iv = next_group(ig + 1);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+  iv = next_group(0);
+#pragma unroll 1
+  for (int s = 0; s < ST - 1; ++s) issue(s);
+
+  int stage = 0, istage = ST - 1;
+  auto run = [&](auto LT, auto RT, int nch, double cl, double cr) {
+    constexpr bool lt = decltype(LT)::value, rt = decltype(RT)::value;
+    const int abase = (lt ? gq * (KC + 4) + tq : tq * (TM + 4) + gq) * W;
+    const int bbase = (rt ? tq * (TN + 4) + gq : gq * (KC + 4) + tq) * W;
+    const int nst = (nch + NW - 1) / NW;
+#pragma unroll 1
+    for (int c = 0; c < nst; ++c) {
+      cp_async_wait<ST - 2>();
+      __syncthreads();
+      issue(istage);
+      istage = istage + 1 == ST ? 0 : istage + 1;
+      if (c * NW + warp < nch) {
+        const double* Ls = smem + stage * Q::STG + warp * Q::CH + abase;
+        const double* Rs = smem + stage * Q::STG + warp * Q::CH + C::LSZ + bbase;
+#pragma unroll
+        for (int kk = 0; kk < KC; kk += 4) {
+          constexpr int ami = (lt ? 8 * (KC + 4) : 8) * W, amk = (lt ? 1 : TM + 4) * W;
+          constexpr int bnj = (rt ? 8 : 8 * (KC + 4)) * W, bnk = (rt ? TN + 4 : 1) * W;
+          if constexpr (CPLX) {
+            double a[FM], ai[FM], b[FN], bi[FN];
+#pragma unroll
+            for (int i = 0; i < FM; ++i) {
+              const double2 v = *reinterpret_cast<const double2*>(Ls + i * ami + kk * amk);
+              a[i] = v.x;
+              ai[i] = cl * v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < FN; ++j) {
+              const double2 v = *reinterpret_cast<const double2*>(Rs + j * bnj + kk * bnk);
+              b[j] = v.x;
+              bi[j] = cr * v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+              for (int j = 0; j < FN; ++j) {
+                dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+                dmma(acc[i][j][0], acc[i][j][1], -ai[i], bi[j]);
+                dmma(acci[i][j][0], acci[i][j][1], a[i], bi[j]);
+                dmma(acci[i][j][0], acci[i][j][1], ai[i], b[j]);
+              }
+          } else {
+            double a[FM], b[FN];
+#pragma unroll
+            for (int i = 0; i < FM; ++i) a[i] = Ls[i * ami + kk * amk];
+#pragma unroll
+            for (int j = 0; j < FN; ++j) b[j] = Rs[j * bnj + kk * bnk];
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+              for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+          }
+        }
+      }
+      stage = stage + 1 == ST ? 0 : stage + 1;
+    }
+  };
+  using F_ = std::false_type;
+  using T_ = std::true_type;
+#pragma unroll 1
+  for (int g = 0; g < p.ngroups; ++g) {
+    int e0, e1;
+    range(g, e0, e1);
+    if (e0 >= e1) continue;
+    const SegGroup& G = p.g[g];
+    const int nch = (e1 - e0) * (G.K / KC);
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+    const double cl = (G.opL == OP_H || G.opL == OP_C) ? -1.0 : 1.0;
+    const double cr = (G.opR == OP_H || G.opR == OP_C) ? -1.0 : 1.0;
+    if (lt) {
+      if (rt) run(T_{}, T_{}, nch, cl, cr);
+      else run(T_{}, F_{}, nch, cl, cr);
+    } else {
+      if (rt) run(F_{}, T_{}, nch, cl, cr);
+      else run(F_{}, F_{}, nch, cl, cr);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // the pipeline buffers become the reduction buffer
+
+  // ---- fixed-order reduction of the NW partial tiles, then the v3 epilogue ----
+  double* red = smem + warp * TM * TN * W;
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int x = (8 * i + gq) + (8 * j + 2 * tq + q) * TM;
+        red[x * W] = acc[i][j][q];
+        if constexpr (CPLX) red[x * W + 1] = acci[i][j][q];
+      }
+  __syncthreads();
+  double* Op = p.out + seg_out_offset(p, t) * W;
+  const bool mirror = p.sym && m0 != n0;
+  for (int x = tid; x < TM * TN; x += NT) {
+    const int m = m0 + x % TM, n = n0 + x / TM;
+    if (m >= p.M || n >= p.N) continue;
+    double re = 0.0, im = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      re += smem[(w * TM * TN + x) * W];
+      if constexpr (CPLX) im += smem[(w * TM * TN + x) * W + 1];
+    }
+    const long long off = m + (long long)n * p.Old;
+    const long long offt = n + (long long)m * p.Old;
+    if constexpr (CPLX) {
+      if (p.accumulate) {
+        re += Op[2 * off];
+        im += Op[2 * off + 1];
+      }
+      Op[2 * off] = re;
+      Op[2 * off + 1] = im;
+      if (mirror) {
+        Op[2 * offt] = re;
+        Op[2 * offt + 1] = -im;
+      }
+    } else {
+      if (p.accumulate) re += Op[off];
+      Op[off] = re;
+      if (mirror) Op[offt] = re;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // seg_add: out_t = sum_{e in seg(t)} in[idx_e]   (elements = matrix size in doubles)
 __global__ void seg_add_kernel(double* out, long long Os, const double* in, long long Is,
                                const int* ptr, const int* idx, long long elems, int accumulate) {
