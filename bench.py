@@ -51,13 +51,13 @@ CONFIGS = {
                                   "tree/structure; eps 1e-6"),
     "cfg5": (1048576, 64, 0, 1e-4, "Helmholtz exp(-i k r)/(4 pi r), k = 2 pi, complex128, N = 2^20 Fibonacci-sphere "
                                    "points (seeded rotation, seed 3), diameter 16 wavelengths, leaf 64, eta 1, "
-                                   "Chebyshev order per level clamp(ceil(2.5 + 1.2 k h_l), 4, 7) recompressed at "
+                                   "Chebyshev order per level clamp(ceil(1 + 1.2 k h_l), 3, 5) recompressed at "
                                    "1e-4; C = A*A, eps 1e-4"),
     # configs[4]'s construction at a quarter of the points on a sphere of half the radius (same
     # points per wavelength)
     "cfg5s": (262144, 64, 0, 1e-4, "configs[4] construction at N = 2^18 on a sphere of diameter 8 wavelengths "
                                    "(same points per wavelength): Helmholtz k = 2 pi, complex128, leaf 64, orders "
-                                   "clamp(ceil(2.5 + 1.2 k h_l), 4, 7), recompressed at 1e-4; C = A*A, eps 1e-4"),
+                                   "clamp(ceil(1 + 1.2 k h_l), 3, 5), recompressed at 1e-4; C = A*A, eps 1e-4"),
     "cfg4s": (110592, 64, 4, 1e-6, "configs[3] construction on the 48^3 grid (h = 1/49): C = A*B, A = 7-point FD "
                                    "Laplacian, B = Laplace Chebyshev order 4 (k=64), leaf 64, eta 1, eps 1e-6"),
 }

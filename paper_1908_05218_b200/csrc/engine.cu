@@ -915,8 +915,32 @@ struct EngineRun {
   }
   // 8-wide tile classes (v3 only): outputs with a padded dimension of 8, e.g.
   // the rank-1 (padded 8) FD operand of cfg4, would waste half a 16-wide tile
+  // v5 (v3 with a grid-stride loop over outputs) for small tiles: H2B_SEG_V5=1 enables
+  const bool seg_v5 = std::getenv("H2B_SEG_V5") != nullptr;
+  template <int TM, int TN, bool CX, int WM = 2, int WN = 2>
+  void launch_v5_cfg(const SegParams& sp, int tiles) {
+    constexpr int sm = Seg2Cfg<TM, TN, CX, 8, 4, WM, WN>::SMEM;
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(seg_gemm5_kernel<TM, TN, CX, 8, 4, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              sm));
+      attr = true;
+    }
+    const int gx = std::max(1, std::min(sp.n_out, (148 * 16) / std::max(1, tiles)));
+    seg_gemm5_kernel<TM, TN, CX, 8, 4, WM, WN><<<dim3(gx, tiles), 32 * WM * WN, sm, s>>>(sp);
+  }
+  bool use_v5(int TM, int TN) const { return seg_v5 && TM <= 32 && TN <= 32; }
   template <int TM, int TN, int WM, int WN>
   void launch_seg8(const SegParams& sp, int tiles) {
+    if constexpr (TM <= 32 && TN <= 32) {
+      if (use_v5(TM, TN)) {
+        if (cplx) launch_v5_cfg<TM, TN, true, WM, WN>(sp, tiles);
+        else launch_v5_cfg<TM, TN, false, WM, WN>(sp, tiles);
+        CK(cudaGetLastError());
+        launches++;
+        return;
+      }
+    }
     dim3 grid(sp.n_out, tiles);
     if (cplx) launch_v3_cfg<TM, TN, true, 8, 4, WM, WN>(sp, grid);
     else launch_v3_cfg<TM, TN, false, 8, 4, WM, WN>(sp, grid);
@@ -929,8 +953,20 @@ struct EngineRun {
     bool v3 = !seg_v1 && !seg_v2;
     for (int g = 0; g < sp.ngroups; ++g) v3 = v3 && sp.g[g].K % 8 == 0;
     if (v3) {
-      if (cplx) launch_v3_cfg<TM, TN, true, 8, 4>(sp, grid);
-      else launch_v3_cfg<TM, TN, false, 8, 4>(sp, grid);
+      bool v5 = false;
+      if constexpr (TM <= 32 && TN <= 32) {
+        if (use_v5(TM, TN)) {
+          v5 = true;
+          if (cplx) launch_v5_cfg<TM, TN, true>(sp, tiles);
+          else launch_v5_cfg<TM, TN, false>(sp, tiles);
+        }
+      }
+      if (v5) {
+      } else if (cplx) {
+        launch_v3_cfg<TM, TN, true, 8, 4>(sp, grid);
+      } else {
+        launch_v3_cfg<TM, TN, false, 8, 4>(sp, grid);
+      }
       CK(cudaGetLastError());
       launches++;
       return;

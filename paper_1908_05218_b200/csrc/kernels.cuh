@@ -906,6 +906,296 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
 }
 
 // ---------------------------------------------------------------------------
+// seg_gemm v5 = v3 with several outputs per CTA (grid-stride over outputs): the copy
+// pipeline runs on across output boundaries, so the next output's operand chunks are in
+// flight while the current output finishes and is written.  For many small outputs with
+// a few short entries each (e.g. 24 x 24 targets from 1-3 entries of K = 8), where v3's
+// one-output CTAs are dominated by their prologue / epilogue.
+template <int TM, int TN, bool CPLX, int KC_ = 8, int ST_ = 4, int WM_ = 2, int WN_ = 2>
+__global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm5_kernel(const SegParams p) {
+  using C = Seg2Cfg<TM, TN, CPLX, KC_, ST_, WM_, WN_>;
+  constexpr int NT = C::NT;
+  constexpr int KC = C::KC, W = C::W, ST = C::STAGES;
+  constexpr int EPS = CPLX ? 1 : 2;  // elements per 16-byte copy
+  constexpr int LSEG = TM * KC / EPS, RSEG = TN * KC / EPS;
+  constexpr int LPT = (LSEG + NT - 1) / NT, RPT = (RSEG + NT - 1) / NT;
+  extern __shared__ __align__(16) double smem[];
+
+  int t = blockIdx.x, tp = blockIdx.x;  // consumer / producer output
+  const int tstride = gridDim.x;
+  int m0, n0;
+  if (p.sym) {
+    const int y = blockIdx.y;
+    int tm = (int)((sqrt(8.0 * y + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= y) ++tm;
+    while (tm * (tm + 1) / 2 > y) --tm;
+    m0 = tm * TM;
+    n0 = (y - tm * (tm + 1) / 2) * TN;
+  } else {
+    const int tilesM = (p.M + TM - 1) / TM;
+    m0 = (blockIdx.y % tilesM) * TM;
+    n0 = (blockIdx.y / tilesM) * TN;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = (warp % C::WM) * (TM / C::WM), wn = (warp / C::WM) * (TN / C::WN);
+
+  double acc[C::FM][C::FN][2];
+  double acci[CPLX ? C::FM : 1][CPLX ? C::FN : 1][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if constexpr (CPLX) {
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) acci[i][j][0] = acci[i][j][1] = 0.0;
+  }
+
+  // ---- copy (producer) state: one chunk ahead of the consumer by ST-1 -------
+  int ig = 0, ie = 0, ie1 = 0, ikc = 0, inkc = 1;
+  bool iv = false;
+  const double* lsrc[LPT];
+  const double* rsrc[RPT];
+  int ldst[LPT], rdst[RPT], loff[LPT], roff[RPT];
+  bool lok[LPT], rok[RPT];
+  long long lstep = 0, rstep = 0;
+  auto range = [&](int g, int tt, int& e0, int& e1) {
+    const int* ptr = p.g[g].ptr;
+    if (ptr) {
+      e0 = ptr[tt];
+      e1 = ptr[tt + 1];
+    } else {
+      e0 = 0;
+      e1 = 1;
+    }
+  };
+  auto setup_group = [&](int g) {  // per-thread copy geometry of group g
+    const SegGroup& G = p.g[g];
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int sgi = tid + j * NT;
+      int m, k;
+      if (!lt) {
+        k = sgi / (TM / EPS);
+        m = (sgi % (TM / EPS)) * EPS;
+      } else {
+        m = sgi / (KC / EPS);
+        k = (sgi % (KC / EPS)) * EPS;
+      }
+      lok[j] = sgi < LSEG && m0 + m < p.M;
+      loff[j] = lt ? (k + (m0 + m) * G.Lld) : (m0 + m + k * G.Lld);
+      ldst[j] = (lt ? m * (KC + 4) + k : k * (TM + 4) + m) * W;
+    }
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int sgi = tid + j * NT;
+      int n, k;
+      if (rt) {
+        k = sgi / (TN / EPS);
+        n = (sgi % (TN / EPS)) * EPS;
+      } else {
+        n = sgi / (KC / EPS);
+        k = (sgi % (KC / EPS)) * EPS;
+      }
+      rok[j] = sgi < RSEG && n0 + n < p.N;
+      roff[j] = rt ? (n0 + n + k * G.Rld) : (k + (n0 + n) * G.Rld);
+      rdst[j] = (rt ? k * (TN + 4) + n : n * (KC + 4) + k) * W;
+    }
+    lstep = (lt ? (long long)KC : (long long)KC * G.Lld) * W;
+    rstep = (rt ? (long long)KC * G.Rld : (long long)KC) * W;
+    inkc = G.K / KC;
+  };
+  auto setup_entry = [&]() {  // source pointers of entry ie of group ig
+    const SegGroup& G = p.g[ig];
+    int l, r;
+    if (G.ptr) {
+      l = G.li[ie];
+      r = G.ri[ie];
+    } else {
+      l = G.li ? G.li[tp] : tp;
+      r = G.ri ? G.ri[tp] : tp;
+    }
+    const double* Lp = G.L + (G.Ls * l + G.Loff) * W;
+    const double* Rp = G.R + (G.Rs * r + G.Roff) * W;
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) lsrc[j] = Lp + (long long)loff[j] * W;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) rsrc[j] = Rp + (long long)roff[j] * W;
+    ikc = 0;
+  };
+  auto next_group = [&](int g) {  // first group >= g with entries, this output or the next ones
+    for (;;) {
+      for (; g < p.ngroups; ++g) {
+        range(g, tp, ie, ie1);
+        if (ie < ie1) {
+          ig = g;
+          setup_group(g);
+          setup_entry();
+          return true;
+        }
+      }
+      tp += tstride;
+      if (tp >= p.n_out) return false;
+      g = 0;
+    }
+  };
+  auto issue = [&](int stage) {
+    if (iv) {
+      double* Ls = smem + stage * C::STAGE;
+      double* Rs = Ls + C::LSZ;
+#pragma unroll
+      for (int j = 0; j < LPT; ++j) {
+        if (lok[j]) cp_async16(Ls + ldst[j], lsrc[j], true);
+        lsrc[j] += lstep;
+      }
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        if (rok[j]) cp_async16(Rs + rdst[j], rsrc[j], true);
+        rsrc[j] += rstep;
+      }
+      if (++ikc == inkc) {
+        if (++ie < ie1) setup_entry();
+        else iv = next_group(ig + 1);
+      }
+    }
+    cp_async_commit();
+  };
+
+  iv = next_group(0);
+#pragma unroll 1
+  for (int s = 0; s < ST - 1; ++s) issue(s);
+
+  // ---- consumer: groups in order, a layout-specialised body per group -------
+  int stage = 0, istage = ST - 1;
+  auto run = [&](auto LT, auto RT, int nch, double cl, double cr) {
+    constexpr bool lt = decltype(LT)::value, rt = decltype(RT)::value;
+    const int abase = (lt ? (wm + gq) * (KC + 4) + tq : tq * (TM + 4) + wm + gq) * W;
+    const int bbase = (rt ? tq * (TN + 4) + wn + gq : (wn + gq) * (KC + 4) + tq) * W;
+#pragma unroll 1
+    for (int c = 0; c < nch; ++c) {
+      cp_async_wait<ST - 2>();
+      __syncthreads();
+      issue(istage);
+      istage = istage + 1 == ST ? 0 : istage + 1;
+      const double* Ls = smem + stage * C::STAGE + abase;
+      const double* Rs = smem + stage * C::STAGE + C::LSZ + bbase;
+#pragma unroll
+      for (int kk = 0; kk < KC; kk += 4) {
+        constexpr int ami = (lt ? 8 * (KC + 4) : 8) * W, amk = (lt ? 1 : TM + 4) * W;
+        constexpr int bnj = (rt ? 8 : 8 * (KC + 4)) * W, bnk = (rt ? TN + 4 : 1) * W;
+        if constexpr (CPLX) {
+          double a[C::FM], ai[C::FM], b[C::FN], bi[C::FN];
+#pragma unroll
+          for (int i = 0; i < C::FM; ++i) {
+            const double2 v = *reinterpret_cast<const double2*>(Ls + i * ami + kk * amk);
+            a[i] = v.x;
+            ai[i] = cl * v.y;
+          }
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) {
+            const double2 v = *reinterpret_cast<const double2*>(Rs + j * bnj + kk * bnk);
+            b[j] = v.x;
+            bi[j] = cr * v.y;
+          }
+#pragma unroll
+          for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+            for (int j = 0; j < C::FN; ++j) {
+              dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+              dmma(acc[i][j][0], acc[i][j][1], -ai[i], bi[j]);
+              dmma(acci[i][j][0], acci[i][j][1], a[i], bi[j]);
+              dmma(acci[i][j][0], acci[i][j][1], ai[i], b[j]);
+            }
+        } else {
+          double a[C::FM], b[C::FN];
+#pragma unroll
+          for (int i = 0; i < C::FM; ++i) a[i] = Ls[i * ami + kk * amk];
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) b[j] = Rs[j * bnj + kk * bnk];
+#pragma unroll
+          for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+            for (int j = 0; j < C::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+      }
+      stage = stage + 1 == ST ? 0 : stage + 1;
+    }
+  };
+  using F_ = std::false_type;
+  using T_ = std::true_type;
+#pragma unroll 1
+  for (; t < p.n_out; t += tstride) {
+#pragma unroll 1
+  for (int g = 0; g < p.ngroups; ++g) {
+    int e0, e1;
+    range(g, t, e0, e1);
+    if (e0 >= e1) continue;
+    const SegGroup& G = p.g[g];
+    const int nch = (e1 - e0) * (G.K / KC);
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+    const double cl = (G.opL == OP_H || G.opL == OP_C) ? -1.0 : 1.0;
+    const double cr = (G.opR == OP_H || G.opR == OP_C) ? -1.0 : 1.0;
+    if (lt) {
+      if (rt) run(T_{}, T_{}, nch, cl, cr);
+      else run(T_{}, F_{}, nch, cl, cr);
+    } else {
+      if (rt) run(F_{}, T_{}, nch, cl, cr);
+      else run(F_{}, F_{}, nch, cl, cr);
+    }
+  }
+  {
+  double* Op = p.out + seg_out_offset(p, t) * W;
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int m = m0 + wm + 8 * i + gq;
+        const int n = n0 + wn + 8 * j + 2 * tq + q;
+        if (m < p.M && n < p.N) {
+          const long long off = m + (long long)n * p.Old;
+          const long long offt = n + (long long)m * p.Old;
+          const bool mirror = p.sym && m0 != n0;
+          if constexpr (CPLX) {
+            double re = acc[i][j][q], im = acci[i][j][q];
+            if (p.accumulate) {
+              re += Op[2 * off];
+              im += Op[2 * off + 1];
+            }
+            Op[2 * off] = re;
+            Op[2 * off + 1] = im;
+            if (mirror) {
+              Op[2 * offt] = re;
+              Op[2 * offt + 1] = -im;
+            }
+          } else {
+            double v = acc[i][j][q];
+            if (p.accumulate) v += Op[off];
+            Op[off] = v;
+            if (mirror) Op[offt] = v;
+          }
+        }
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) {
+      acc[i][j][0] = acc[i][j][1] = 0.0;
+      if constexpr (CPLX) acci[i][j][0] = acci[i][j][1] = 0.0;
+    }
+  }
+  cp_async_wait<0>();
+}
+
+
+// ---------------------------------------------------------------------------
 // seg_gemm v4 (small output tiles, TM, TN <= 32): the NW warps of the CTA split the
 // k-CHUNKS of the segment instead of the output tile.  A pipeline stage holds NW
 // consecutive chunks of one group; warp w multiplies chunk w of the stage into its own

@@ -272,18 +272,20 @@ def test_deterministic_products(ctx):
     assert np.array_equal(r1.product.values, r2.product.values)
 
 
+@pytest.mark.parametrize("knob", ["H2B_SEG_V4", "H2B_SEG_V5"])
 @pytest.mark.parametrize("name", ["cfg3", "cfg5"])
-def test_seg_v4_small_tiles_match_oracle(ctx, name, monkeypatch):
-    """seg_gemm v4 (warps split the chunks of small output tiles, fixed-order reduction) on the
-    small-rank bench constructions: oracle parity and bit-identical repeats."""
+def test_small_tile_kernels_match_oracle(ctx, name, knob, monkeypatch):
+    """seg_gemm v4 (warps split the chunks of small output tiles, fixed-order reduction) and v5
+    (grid-stride over outputs) on the small-rank bench constructions: oracle parity and
+    bit-identical repeats."""
     import bench
     _, _, _, A, B = bench.build_operands(name, 4096)
     eps = bench.CONFIGS[name][3]
-    monkeypatch.setenv("H2B_SEG_V4", "1")
+    monkeypatch.setenv(knob, "1")
     got, ref, cg, co = check_against_oracle(A, B, eps, ctx)
     again = P.mmp(A, B, eps, ctx)
     assert np.array_equal(again.product.values, got.product.values)
-    monkeypatch.delenv("H2B_SEG_V4")
+    monkeypatch.delenv(knob)
     base = P.mmp(A, B, eps, ctx)
     assert np.array_equal(base.product.row_rank, got.product.row_rank)
     assert rel(O.h2_to_dense(base.product), cg) <= 1e-12
