@@ -1111,11 +1111,25 @@ struct EngineRun {
     CK(cudaGetLastError());
     launches++;
   }
+  // Hermitian (Gram) outputs cannot be cut into strips; their square tile is chosen by
+  // lower-triangle tile area / relative tile efficiency (64: 1, 32: 0.75): e.g. an 80 x 80 Gram
+  // takes 6 tiles of 32 (6,144 padded elements) instead of 3 of 64 (12,288, 26 % useful).
+  // H2B_SYM_T64=1 restores the plain rule.
+  const bool sym_t64 = std::getenv("H2B_SYM_T64") != nullptr;
+  static int sym_tile(int M) {
+    if (M <= 32) return M <= 16 ? 16 : 32;
+    auto cost = [&](int T, double eff) {
+      const double t = (M + T - 1) / T;
+      return t * (t + 1) / 2 * T * T / eff;
+    };
+    return cost(32, 0.75) < cost(64, 1.0) ? 32 : 64;
+  }
   void launch_tiles(const SegParams& sp) {
     const int M = sp.M, N = sp.N;
     const bool v3 = !seg_v1 && !seg_v2;
-    const int TM = (M <= 8 && v3) ? 8 : M <= 16 ? 16 : (M <= 32 ? 32 : 64);
-    const int TN = (N <= 8 && v3) ? 8 : N <= 16 ? 16 : (N <= 32 ? 32 : 64);
+    int TM = (M <= 8 && v3) ? 8 : M <= 16 ? 16 : (M <= 32 ? 32 : 64);
+    int TN = (N <= 8 && v3) ? 8 : N <= 16 ? 16 : (N <= 32 ? 32 : 64);
+    if (sp.sym && v3 && !sym_t64 && M > 32) TM = TN = sym_tile(M);
     const int tm_ = (M + TM - 1) / TM;
     const int tiles = sp.sym ? tm_ * (tm_ + 1) / 2 : tm_ * ((N + TN - 1) / TN);
     if (seg_v4 && v3 && TM <= 32 && TN <= 32) {
