@@ -905,6 +905,18 @@ struct EngineRun {
   template <int TM, int TN, bool CX, int KC, int ST, int WM = 2, int WN = 2>
   void launch_v3_cfg(const SegParams& sp, dim3 grid) {
     constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST, WM, WN>::SMEM;
+    if constexpr (CX) {
+      if (cplx3m) {
+        static bool attr3 = false;
+        if (!attr3) {
+          CK(cudaFuncSetAttribute(seg_gemm3_kernel<TM, TN, CX, KC, ST, WM, WN, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          attr3 = true;
+        }
+        seg_gemm3_kernel<TM, TN, CX, KC, ST, WM, WN, true><<<grid, 32 * WM * WN, sm, s>>>(sp);
+        return;
+      }
+    }
     static bool attr = false;
     if (!attr) {
       CK(cudaFuncSetAttribute(seg_gemm3_kernel<TM, TN, CX, KC, ST, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -913,6 +925,8 @@ struct EngineRun {
     }
     seg_gemm3_kernel<TM, TN, CX, KC, ST, WM, WN><<<grid, 32 * WM * WN, sm, s>>>(sp);
   }
+  // complex products with 3 real DMMAs per complex MAC (Gauss): H2B_CPLX3M=1 enables
+  const bool cplx3m = std::getenv("H2B_CPLX3M") != nullptr;
   // 8-wide tile classes (v3 only): outputs with a padded dimension of 8, e.g.
   // the rank-1 (padded 8) FD operand of cfg4, would waste half a 16-wide tile
   // v5 (v3 with a grid-stride loop over outputs) for small tiles: H2B_SEG_V5=1 enables

@@ -638,7 +638,10 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm2_kernel(const SegPara
 //    a constant per chunk;
 //  * the fragment loads run in a body specialised per operand layout (N/C vs
 //    T/H on each side), selected once per group, with immediate smem offsets.
-template <int TM, int TN, bool CPLX, int KC_ = 8, int ST_ = 4, int WM_ = 2, int WN_ = 2>
+// G3 (complex only): 3 real products per complex MAC (Gauss): with s_a = a + i-part, d_b = bi - b,
+// s_b = b + bi: P = sum s_a b, R = sum a d_b, Q = sum ai s_b; Re = P - Q, Im = P + R
+// (3 DMMAs instead of 4, one more accumulator set).
+template <int TM, int TN, bool CPLX, int KC_ = 8, int ST_ = 4, int WM_ = 2, int WN_ = 2, bool G3 = false>
 __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegParams p) {
   using C = Seg2Cfg<TM, TN, CPLX, KC_, ST_, WM_, WN_>;
   constexpr int NT = C::NT;
@@ -668,6 +671,13 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
 
   double acc[C::FM][C::FN][2];
   double acci[CPLX ? C::FM : 1][CPLX ? C::FN : 1][2];
+  double accq[(CPLX && G3) ? C::FM : 1][(CPLX && G3) ? C::FN : 1][2];
+  if constexpr (CPLX && G3) {
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) accq[i][j][0] = accq[i][j][1] = 0.0;
+  }
 #pragma unroll
   for (int i = 0; i < C::FM; ++i)
 #pragma unroll
@@ -823,15 +833,34 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
             b[j] = v.x;
             bi[j] = cr * v.y;
           }
+          if constexpr (G3) {
+            double sa[C::FM], db[C::FN], sb[C::FN];
 #pragma unroll
-          for (int i = 0; i < C::FM; ++i)
+            for (int i = 0; i < C::FM; ++i) sa[i] = a[i] + ai[i];
 #pragma unroll
             for (int j = 0; j < C::FN; ++j) {
-              dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-              dmma(acc[i][j][0], acc[i][j][1], -ai[i], bi[j]);
-              dmma(acci[i][j][0], acci[i][j][1], a[i], bi[j]);
-              dmma(acci[i][j][0], acci[i][j][1], ai[i], b[j]);
+              db[j] = bi[j] - b[j];
+              sb[j] = b[j] + bi[j];
             }
+#pragma unroll
+            for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+              for (int j = 0; j < C::FN; ++j) {
+                dmma(acc[i][j][0], acc[i][j][1], sa[i], b[j]);     // P
+                dmma(acci[i][j][0], acci[i][j][1], a[i], db[j]);   // R
+                dmma(accq[i][j][0], accq[i][j][1], ai[i], sb[j]);  // Q
+              }
+          } else {
+#pragma unroll
+            for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+              for (int j = 0; j < C::FN; ++j) {
+                dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+                dmma(acc[i][j][0], acc[i][j][1], -ai[i], bi[j]);
+                dmma(acci[i][j][0], acci[i][j][1], a[i], bi[j]);
+                dmma(acci[i][j][0], acci[i][j][1], ai[i], b[j]);
+              }
+          }
         } else {
           double a[C::FM], b[C::FN];
 #pragma unroll
@@ -885,6 +914,10 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
           const bool mirror = p.sym && m0 != n0;
           if constexpr (CPLX) {
             double re = acc[i][j][q], im = acci[i][j][q];
+            if constexpr (G3) {
+              re = acc[i][j][q] - accq[i][j][q];
+              im = acc[i][j][q] + acci[i][j][q];
+            }
             if (p.accumulate) {
               re += Op[2 * off];
               im += Op[2 * off + 1];

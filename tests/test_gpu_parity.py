@@ -272,7 +272,7 @@ def test_deterministic_products(ctx):
     assert np.array_equal(r1.product.values, r2.product.values)
 
 
-@pytest.mark.parametrize("knob", ["H2B_SEG_V4", "H2B_SEG_V5"])
+@pytest.mark.parametrize("knob", ["H2B_SEG_V4", "H2B_SEG_V5", "H2B_CPLX3M"])
 @pytest.mark.parametrize("name", ["cfg3", "cfg5"])
 def test_small_tile_kernels_match_oracle(ctx, name, knob, monkeypatch):
     """seg_gemm v4 (warps split the chunks of small output tiles, fixed-order reduction) and v5
