@@ -333,8 +333,10 @@ def run_b200(args) -> None:
     if dist:
         dist.barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, "cuda")
-    # F_alg: 2 flops per real MAC, 8 per complex MAC
+    # F_alg: 2 flops per real MAC, 8 per complex MAC; the tensor pipe
+    # executes 3 real MACs per complex MAC (Gauss form, unless H2B_CPLX4M=1): 6 executed flops
     fpm = 8.0 if A.scalar == P.H2C_COMPLEX else 2.0
+    fpm_exec = (8.0 if os.environ.get("H2B_CPLX4M") else 6.0) if A.scalar == P.H2C_COMPLEX else 2.0
     flops = fpm * rep.flops
     value = job_throughput(flops, world, ms * 1e-3)
 
@@ -350,16 +352,17 @@ def run_b200(args) -> None:
     prof_ms = sum(e["ms"] for e in prof) if prof else 0.0
     roofline = None
     if dom:
-        ach = fpm * dom["macs"] / (dom["ms"] * 1e-3) / 1e12
+        ach = fpm_exec * dom["macs"] / (dom["ms"] * 1e-3) / 1e12
         traffic, traffic_src = measured_traffic(f"{args.config}:{dom['name']}")
         roofline = {"bound": "tensor", "kernel": dom["name"], "launches": dom["launches"],
                     "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                     "traffic": traffic, "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
-                    "flops_per_launch": fpm * dom["macs"] / dom["launches"],
+                    "flops_per_launch": fpm_exec * dom["macs"] / dom["launches"],
+                    "flops_per_mac_exec": fpm_exec,
                     "peak_source": peak_src,
                     "share_of_step": round(dom["ms"] / prof_ms, 4) if prof_ms else None,
-                    "pipeline_exec_tflops": round(fpm * rep.flops_exec / (ms * 1e-3) / 1e12, 3),
-                    "pipeline_frac": round(fpm * rep.flops_exec / (ms * 1e-3) / 1e12 / peak, 4)}
+                    "pipeline_exec_tflops": round(fpm_exec * rep.flops_exec / (ms * 1e-3) / 1e12, 3),
+                    "pipeline_frac": round(fpm_exec * rep.flops_exec / (ms * 1e-3) / 1e12 / peak, 4)}
 
     # end-to-end through the drop-in C-ABI call with pinned host buffers
     del dA, dB
@@ -406,7 +409,7 @@ def run_b200(args) -> None:
             "dtype": "c128" if A.scalar == P.H2C_COMPLEX else "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": W["desc"], "N": W["n"], "eps": eps,
                        "macs_per_step": int(rep.flops), "macs_exec_per_step": int(rep.flops_exec),
-                       "flops_per_mac": fpm, "eps_rel": eps_rel,
+                       "flops_per_mac": fpm, "eps_rel": eps_rel, "build_seconds": round(W["build_seconds"], 1),
                        "max_rank": rep.max_rank(), "l2": "inputs (%.1f GB) >> 126 MB L2" % ((A.values.nbytes + (0 if B is A else B.values.nbytes)) / 1e9),
                        "parallelism": f"replicas{world}"},
             "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),

@@ -24,7 +24,7 @@ CUDA_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-
                      "-Xptxas", "-v"]
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-pthread", "-I/usr/local/cuda/include"]
 
-CU_SOURCES = ["engine.cu"]
+CU_SOURCES = ["engine.cu", "construct_dev.cu"]
 CPP_SOURCES = ["plan.cpp", "counters.cpp", "structure.cpp", "construct.cpp", "capi.cpp"]
 
 
@@ -80,7 +80,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
             _run(["g++", *CXX_FLAGS, "-c", str(s), "-o", str(o)])
         objs.append(o)
     if force or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-lcusolver", *_host_blas(),
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-lcusolver", "-lcublas", *_host_blas(),
               "-Xcompiler", "-pthread"])
     return LIB
 

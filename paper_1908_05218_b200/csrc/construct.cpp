@@ -12,6 +12,7 @@
 //    zero admissible blocks with the degenerate e_1 bases build_h2 produces for
 //    a zero far field, truncation.cpp:16-23).
 #include <atomic>
+#include <memory>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -22,6 +23,7 @@
 #include <type_traits>
 #include <algorithm>
 
+#include "construct_dev.hpp"
 #include "structure.hpp"
 
 namespace h2b {
@@ -435,6 +437,45 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
   };
   scipy_openblas_set_num_threads(1);  // parallel over clusters / blocks instead
 
+  // Device path for the two coupling passes (construct_dev.cu): kernel evaluation + batched
+  // GEMMs on the GPU when one is present (H2B_CONSTRUCT_HOST=1 keeps everything on the host).
+  const bool use_dev = cdev_available() && std::getenv("H2B_CONSTRUCT_HOST") == nullptr;
+  std::unique_ptr<CouplingDev, void (*)(CouplingDev*)> dev(use_dev ? cdev_create(cplx, kappa) : nullptr, cdev_destroy);
+  std::vector<int> pos_in_level(nc, -1);
+  for (int l = 0; l <= D; ++l)
+    for (size_t i = 0; i < levels[l].size(); ++i) pos_in_level[levels[l][i]] = static_cast<int>(i);
+  std::vector<std::vector<int64_t>> adm_level(D + 1);  // per level, sorted by row position (stable)
+  for (int64_t q : adm) adm_level[t.level[b.row[q]]].push_back(q);
+  for (auto& v : adm_level)
+    std::stable_sort(v.begin(), v.end(), [&](int64_t x, int64_t y) {
+      return pos_in_level[b.row[x]] < pos_in_level[b.row[y]];
+    });
+  auto dev_level = [&](int l) {
+    const auto& ids = levels[l];
+    std::vector<double> boxes(6 * ids.size());
+    std::vector<const double*> R(ids.size());
+    std::vector<int> r(ids.size());
+    for (size_t i = 0; i < ids.size(); ++i) {
+      const Cheb& X = cb[ids[i]];
+      for (int d2 = 0; d2 < 3; ++d2) {
+        boxes[6 * i + d2] = X.box.c[d2];
+        boxes[6 * i + 3 + d2] = X.box.h[d2];
+      }
+      R[i] = Rb[ids[i]].d.data();
+      r[i] = Rb[ids[i]].r;
+    }
+    cdev_level(dev.get(), static_cast<int>(ids.size()), boxes.data(), ids.empty() ? 1 : cb[ids[0]].m, R.data(),
+               r.data());
+  };
+  auto level_blocks = [&](int l, std::vector<int>& br, std::vector<int>& bc) {
+    br.clear();
+    bc.clear();
+    for (int64_t q : adm_level[l]) {
+      br.push_back(pos_in_level[b.row[q]]);
+      bc.push_back(pos_in_level[b.col[q]]);
+    }
+  };
+
   // 3. optional recompression (the reference's build_h2 rule, h2_matrix.cpp:83-121, applied to the
   //    interpolation operand): the row Gram of cluster t over its far field (own admissible
   //    partners plus those inherited from its ancestors, far_partners h2_matrix.cpp:22-46) is
@@ -451,13 +492,32 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
     std::vector<M<S>> Z(nc);
     for (int l = lmin; l <= D; ++l) {
       const auto& ids = levels[l];
+      std::vector<M<S>> zown;
+      if (dev) {  // sum_s S_ts S_ts^H of the level on the device
+        zown.resize(ids.size());
+        std::vector<double*> zp(ids.size());
+        for (size_t i = 0; i < ids.size(); ++i) {
+          zown[i] = M<S>(Qb[ids[i]].c, Qb[ids[i]].c);
+          zp[i] = reinterpret_cast<double*>(zown[i].d.data());
+        }
+        std::vector<int> br, bc;
+        level_blocks(l, br, bc);
+        if (!br.empty()) {
+          dev_level(l);
+          cdev_grams(dev.get(), static_cast<int>(br.size()), br.data(), bc.data(), zp.data());
+        }
+      }
       pfor(static_cast<int64_t>(ids.size()), threads, [&](int64_t qi) {
         const int c = ids[qi];
         const int rk = Qb[c].c;
         M<S> z(rk, rk);
-        for (int64_t q : by_row[c]) {
-          const M<S> Sq = coupling_raw(q);
-          gemm(kN, kC, Sq, Sq, z, true);
+        if (dev) {
+          z = std::move(zown[qi]);
+        } else {
+          for (int64_t q : by_row[c]) {
+            const M<S> Sq = coupling_raw(q);
+            gemm(kN, kC, Sq, Sq, z, true);
+          }
         }
         const int p = t.parent[c];
         if (p >= 0 && t.level[p] >= lmin && Z[p].r > 0) {
@@ -552,16 +612,36 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
     if (out->row_off[c] < 0) continue;
     std::copy(basis[c].d.begin(), basis[c].d.end(), V + out->row_off[c]);
   }
-  pfor(static_cast<int64_t>(adm.size()), threads, [&](int64_t a) {
-    const int64_t q = adm[a];
-    M<S> Sq = coupling_raw(q);
-    if (rc) {
-      M<S> PS;
-      gemm(kN, kN, P[b.row[q]], Sq, PS);
-      gemm(kN, kT, PS, P[b.col[q]], Sq);
+  if (dev) {
+    for (int l = lmin; l <= D; ++l) {
+      std::vector<int> br, bc;
+      level_blocks(l, br, bc);
+      if (br.empty()) continue;
+      dev_level(l);
+      const auto& ids = levels[l];
+      std::vector<const double*> pp(ids.size());
+      std::vector<int> kp(ids.size());
+      for (size_t i = 0; i < ids.size(); ++i) {
+        pp[i] = rc ? reinterpret_cast<const double*>(P[ids[i]].d.data()) : nullptr;
+        kp[i] = rc ? P[ids[i]].r : Qb[ids[i]].c;
+      }
+      std::vector<double*> dst(br.size());
+      for (size_t i = 0; i < br.size(); ++i) dst[i] = reinterpret_cast<double*>(V + out->block_off[adm_level[l][i]]);
+      cdev_project(dev.get(), rc ? pp.data() : nullptr, kp.data(), static_cast<int>(br.size()), br.data(), bc.data(),
+                   dst.data());
     }
-    std::copy(Sq.d.begin(), Sq.d.end(), V + out->block_off[q]);
-  });
+  } else {
+    pfor(static_cast<int64_t>(adm.size()), threads, [&](int64_t a) {
+      const int64_t q = adm[a];
+      M<S> Sq = coupling_raw(q);
+      if (rc) {
+        M<S> PS;
+        gemm(kN, kN, P[b.row[q]], Sq, PS);
+        gemm(kN, kT, PS, P[b.col[q]], Sq);
+      }
+      std::copy(Sq.d.begin(), Sq.d.end(), V + out->block_off[q]);
+    });
+  }
   tick("couplings");
   pfor(b.n_blocks, threads, [&](int64_t q) {
     if (b.kind[q] != H2C_INADMISSIBLE_LEAF) return;

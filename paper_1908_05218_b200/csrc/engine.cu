@@ -925,8 +925,9 @@ struct EngineRun {
     }
     seg_gemm3_kernel<TM, TN, CX, KC, ST, WM, WN><<<grid, 32 * WM * WN, sm, s>>>(sp);
   }
-  // complex products with 3 real DMMAs per complex MAC (Gauss): H2B_CPLX3M=1 enables
-  const bool cplx3m = std::getenv("H2B_CPLX3M") != nullptr;
+  // complex products with 3 real DMMAs per complex MAC (Gauss; cfg5s 0.416 -> 0.377 s,
+  // profiles/r01/ab_3m_cfg5s.txt); H2B_CPLX4M=1 restores the 4-product form
+  const bool cplx3m = std::getenv("H2B_CPLX4M") == nullptr;
   // 8-wide tile classes (v3 only): outputs with a padded dimension of 8, e.g.
   // the rank-1 (padded 8) FD operand of cfg4, would waste half a 16-wide tile
   // v5 (v3 with a grid-stride loop over outputs) for small tiles: H2B_SEG_V5=1 enables

@@ -272,7 +272,22 @@ def test_deterministic_products(ctx):
     assert np.array_equal(r1.product.values, r2.product.values)
 
 
-@pytest.mark.parametrize("knob", ["H2B_SEG_V4", "H2B_SEG_V5", "H2B_CPLX3M"])
+@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def test_device_constructor_matches_host(name, monkeypatch):
+    """The Chebyshev constructor's coupling passes on the device (kernel evaluation + batched
+    GEMMs, construct_dev.cu) give the host constructor's operand: equal ranks, dense difference
+    at round-off."""
+    import bench
+    _, _, _, Ad, Bd = bench.build_operands(name, 4096)
+    monkeypatch.setenv("H2B_CONSTRUCT_HOST", "1")
+    _, _, _, Ah, Bh = bench.build_operands(name, 4096)
+    for d, h in ((Ad, Ah), (Bd, Bh)):
+        assert np.array_equal(d.row_rank, h.row_rank) and np.array_equal(d.col_rank, h.col_rank)
+        dd, dh = O.h2_to_dense(d), O.h2_to_dense(h)
+        assert rel(dd, dh) <= 1e-11, rel(dd, dh)
+
+
+@pytest.mark.parametrize("knob", ["H2B_SEG_V4", "H2B_SEG_V5", "H2B_CPLX4M"])
 @pytest.mark.parametrize("name", ["cfg3", "cfg5"])
 def test_small_tile_kernels_match_oracle(ctx, name, knob, monkeypatch):
     """seg_gemm v4 (warps split the chunks of small output tiles, fixed-order reduction) and v5
