@@ -647,6 +647,11 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
   constexpr int NT = C::NT;
   constexpr int KC = C::KC, W = C::W, ST = C::STAGES;
   constexpr int EPS = CPLX ? 1 : 2;  // elements per 16-byte copy
+  // row pads (elements) of the [k][m] / [k][n] and [m][k] / [n][k] stage layouts: 4 doubles
+  // for 8-byte real fragment loads; for 16-byte complex loads 2 and 0 elements make every
+  // quarter-warp hit 8 distinct 4-bank groups (the +4 pads of the real layout gave 2-way
+  // conflicts: 1.3e10 bank conflicts in one cfg5 leaf launch).  Both fit Seg2Cfg's sizes.
+  constexpr int PM = CPLX ? 2 : 4, PK = CPLX ? 0 : 4;
   constexpr int LSEG = TM * KC / EPS, RSEG = TN * KC / EPS;
   constexpr int LPT = (LSEG + NT - 1) / NT, RPT = (RSEG + NT - 1) / NT;
   extern __shared__ __align__(16) double smem[];
@@ -724,7 +729,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
       }
       lok[j] = sgi < LSEG && m0 + m < p.M;
       loff[j] = lt ? (k + (m0 + m) * G.Lld) : (m0 + m + k * G.Lld);
-      ldst[j] = (lt ? m * (KC + 4) + k : k * (TM + 4) + m) * W;
+      ldst[j] = (lt ? m * (KC + PK) + k : k * (TM + PM) + m) * W;
     }
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
@@ -739,7 +744,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
       }
       rok[j] = sgi < RSEG && n0 + n < p.N;
       roff[j] = rt ? (n0 + n + k * G.Rld) : (k + (n0 + n) * G.Rld);
-      rdst[j] = (rt ? k * (TN + 4) + n : n * (KC + 4) + k) * W;
+      rdst[j] = (rt ? k * (TN + PM) + n : n * (KC + PK) + k) * W;
     }
     lstep = (lt ? (long long)KC : (long long)KC * G.Lld) * W;
     rstep = (rt ? (long long)KC * G.Rld : (long long)KC) * W;
@@ -805,8 +810,8 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
   int stage = 0, istage = ST - 1;
   auto run = [&](auto LT, auto RT, int nch, double cl, double cr) {
     constexpr bool lt = decltype(LT)::value, rt = decltype(RT)::value;
-    const int abase = (lt ? (wm + gq) * (KC + 4) + tq : tq * (TM + 4) + wm + gq) * W;
-    const int bbase = (rt ? tq * (TN + 4) + wn + gq : (wn + gq) * (KC + 4) + tq) * W;
+    const int abase = (lt ? (wm + gq) * (KC + PK) + tq : tq * (TM + PM) + wm + gq) * W;
+    const int bbase = (rt ? tq * (TN + PM) + wn + gq : (wn + gq) * (KC + PK) + tq) * W;
 #pragma unroll 1
     for (int c = 0; c < nch; ++c) {
       cp_async_wait<ST - 2>();
@@ -817,8 +822,8 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
       const double* Rs = smem + stage * C::STAGE + C::LSZ + bbase;
 #pragma unroll
       for (int kk = 0; kk < KC; kk += 4) {
-        constexpr int ami = (lt ? 8 * (KC + 4) : 8) * W, amk = (lt ? 1 : TM + 4) * W;
-        constexpr int bnj = (rt ? 8 : 8 * (KC + 4)) * W, bnk = (rt ? TN + 4 : 1) * W;
+        constexpr int ami = (lt ? 8 * (KC + PK) : 8) * W, amk = (lt ? 1 : TM + PM) * W;
+        constexpr int bnj = (rt ? 8 : 8 * (KC + PK)) * W, bnk = (rt ? TN + PM : 1) * W;
         if constexpr (CPLX) {
           double a[C::FM], ai[C::FM], b[C::FN], bi[C::FN];
 #pragma unroll
