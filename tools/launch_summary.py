@@ -19,9 +19,9 @@ ni = next(i for i, h in enumerate(hdr) if "Push/Pop_Range" in h)
 
 
 def phase(r):
-    m = re.search(r'<default domain>:([^:"]+)', r[ni])
+    m = re.search(r'<default domain>:([^:"]+):([^:"]+)', r[ni])
     if m:
-        return m.group(1).replace("/", ":")
+        return m.group(1) + ":" + m.group(2)
     return "(library) " + re.sub(r"\(.*", "", r[ki])[:60]
 
 
