@@ -503,15 +503,21 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
         std::vector<int> br, bc;
         level_blocks(l, br, bc);
         if (!br.empty()) {
-          dev_level(l);
-          cdev_grams(dev.get(), static_cast<int>(br.size()), br.data(), bc.data(), zp.data());
+          try {
+            dev_level(l);
+            cdev_grams(dev.get(), static_cast<int>(br.size()), br.data(), bc.data(), zp.data());
+          } catch (const std::exception& e) {  // e.g. the HBM is held by a product context: host path
+            if (trace) std::fprintf(stderr, "[construct] device pass failed (%s); host path\n", e.what());
+            dev.reset();
+            zown.clear();
+          }
         }
       }
       pfor(static_cast<int64_t>(ids.size()), threads, [&](int64_t qi) {
         const int c = ids[qi];
         const int rk = Qb[c].c;
         M<S> z(rk, rk);
-        if (dev) {
+        if (!zown.empty()) {
           z = std::move(zown[qi]);
         } else {
           for (int64_t q : by_row[c]) {
@@ -612,7 +618,9 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
     if (out->row_off[c] < 0) continue;
     std::copy(basis[c].d.begin(), basis[c].d.end(), V + out->row_off[c]);
   }
+  bool dev_done = false;
   if (dev) {
+    try {
     for (int l = lmin; l <= D; ++l) {
       std::vector<int> br, bc;
       level_blocks(l, br, bc);
@@ -630,7 +638,13 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
       cdev_project(dev.get(), rc ? pp.data() : nullptr, kp.data(), static_cast<int>(br.size()), br.data(), bc.data(),
                    dst.data());
     }
-  } else {
+    dev_done = true;
+    } catch (const std::exception& e) {  // host path below recomputes every coupling
+      if (trace) std::fprintf(stderr, "[construct] device pass failed (%s); host path\n", e.what());
+      dev.reset();
+    }
+  }
+  if (!dev_done) {
     pfor(static_cast<int64_t>(adm.size()), threads, [&](int64_t a) {
       const int64_t q = adm[a];
       M<S> Sq = coupling_raw(q);

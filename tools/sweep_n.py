@@ -6,6 +6,7 @@ MmpReport.flops; executed flops = 2 / 6 (Gauss complex) x flops_exec; fraction o
 DMMA peak.  Points that do not fit the HBM are recorded as such.
 
 Usage: python tools/sweep_n.py [out.json]"""
+import gc
 import json
 import os
 import statistics
@@ -23,6 +24,8 @@ points = [("cfg2", n) for n in (8192, 16384, 32768, 65536, 131072, 262144)] + \
 rows = []
 for name, n in points:
     rec = {"family": name, "N": n, "eps": bench.CONFIGS[name][3]}
+    ctx = dA = dB = A = B = None
+    gc.collect()  # the previous point's context (and its arena) must be gone
     try:
         t0 = time.perf_counter()
         _, tree, _, A, B = bench.build_operands(name, n)
@@ -39,9 +42,9 @@ for name, n in points:
         rec.update(seconds=round(t, 4), gflops=round(f_alg / t / 1e9, 1), exec_tflops=round(f_exe / t / 1e12, 2),
                    frac_of_dmma_peak=round(f_exe / t / 1e12 / peak, 3), depth=tree.depth, max_rank=rep.max_rank(),
                    macs=int(rep.flops), macs_exec=int(rep.flops_exec))
-        del dA, dB, ctx
     except Exception as e:  # e.g. device memory
         rec["error"] = str(e)[:200]
+    ctx = dA = dB = A = B = None
     rows.append(rec)
     print(json.dumps(rec), flush=True)
     os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
