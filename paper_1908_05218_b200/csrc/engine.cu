@@ -89,19 +89,30 @@ class Arena {
   ~Arena() {
     if (base_) cudaFree(base_);
   }
-  void* alloc(size_t bytes) {
+  // high = long-lived buffer (operands, C's targets / merged blocks / full blocks): taken from the
+  // top of the highest free block that fits, so the short-lived per-level scratch (best fit from
+  // the bottom) does not interleave with it and fragment the arena
+  void* alloc(size_t bytes, bool high = false) {
     bytes = (bytes + 255) & ~size_t(255);
     std::lock_guard<std::mutex> g(mu_);
     reclaim_locked(false);
     auto best = free_.end();
     for (auto it = free_.begin(); it != free_.end(); ++it)
-      if (it->second >= bytes && (best == free_.end() || it->second < best->second)) best = it;
+      if (it->second >= bytes &&
+          (best == free_.end() || (high ? it->first > best->first : it->second < best->second)))
+        best = it;
     if (best == free_.end()) return nullptr;
     const size_t off = best->first, sz = best->second;
     free_.erase(best);
-    if (sz > bytes) free_[off + bytes] = sz - bytes;
-    used_[off] = bytes;
-    return static_cast<char*>(base_) + off;
+    size_t at = off;
+    if (high) {
+      at = off + sz - bytes;
+      if (sz > bytes) free_[off] = sz - bytes;
+    } else if (sz > bytes) {
+      free_[off + bytes] = sz - bytes;
+    }
+    used_[at] = bytes;
+    return static_cast<char*>(base_) + at;
   }
   // (total free bytes, largest free block)
   std::pair<size_t, size_t> stats() {
@@ -183,6 +194,13 @@ class Arena {
 // the arena of the context running on this thread, and its main stream
 thread_local Arena* t_arena = nullptr;
 thread_local cudaStream_t t_arena_stream = nullptr;
+// long-lived allocations (Arena::alloc high) while a HighScope is alive on this thread
+thread_local bool t_arena_high = false;
+struct HighScope {
+  bool prev;
+  explicit HighScope(bool on = true) : prev(t_arena_high) { t_arena_high = on; }
+  ~HighScope() { t_arena_high = prev; }
+};
 // the auxiliary stream of the run on this thread: its buffers also come from the
 // arena and are returned through Arena::free_after
 thread_local cudaStream_t t_aux_stream = nullptr;
@@ -221,12 +239,12 @@ struct DBuf {
     s = st;
     n = std::max<size_t>(doubles, 2);
     if (t_arena && (st == t_arena_stream || (st && st == t_aux_stream)) && n * sizeof(double) >= kArenaMin) {
-      p = static_cast<double*>(t_arena->alloc(n * sizeof(double)));
+      p = static_cast<double*>(t_arena->alloc(n * sizeof(double), t_arena_high));
       if (!p && t_aux_stream && t_arena->has_pending()) {
         // memory pressure: let the deferred work drain, reclaim its blocks, retry
         CK(cudaStreamSynchronize(t_aux_stream));
         t_arena->reclaim(false);
-        p = static_cast<double*>(t_arena->alloc(n * sizeof(double)));
+        p = static_cast<double*>(t_arena->alloc(n * sizeof(double), t_arena_high));
       }
       if (p) {
         arena = t_arena;
@@ -570,6 +588,7 @@ static std::shared_ptr<DevOperand> upload_operand(const Plan& P, const h2c_matri
   }
   const int NL = X->NL;
   const LevelPlan& LL = P.lv[D];
+  HighScope operand_is_long_lived;
   X->Vr.alloc(size_t(LL.n) * NL * X->Kr[D] * W, s, true);
   X->Vc.alloc(size_t(LL.n) * NL * X->Kc[D] * W, s, true);
   X->F.alloc(size_t(LL.nearb.size()) * NL * NL * W, s, true);
@@ -645,6 +664,7 @@ static std::shared_ptr<DevOperand> upload_operand(const Plan& P, const h2c_matri
   auto extent = [](const HJob& j) { return int64_t(j.cols - 1) * j.sld + j.rows; };
   int64_t span_max = 0;
   for (const HJob& j : hj) span_max = std::max(span_max, extent(j));
+  HighScope staging_is_short_lived(false);
   DBuf stage(size_t(std::max(cap, span_max)) * W, s);
   for (size_t i = 0; i < hj.size();) {
     const int64_t o0 = hj[i].off;
@@ -1615,6 +1635,7 @@ struct EngineRun {
     const int na = static_cast<int>(L.adm.size()), np = static_cast<int>(L.pend_row.size());
     const int nl = static_cast<int>(L.nl_block.size());
     const int Kr = KCr[l], Kc = KCc[l];
+    HighScope targets_are_long_lived;
     if (np > 0) {
       const int nm = static_cast<int>(P.lv[l - 1].merged_row.size());
       Mg[l - 1].alloc(sz(nm, 2 * Kr, 2 * Kc), s, true);
@@ -1894,7 +1915,10 @@ struct EngineRun {
     const Ref AF = ref(A.F, NN, NL, OP_N), BF = ref(B.F, NN, NL, OP_N);
     phase = "leaf.full_targets";
     const Ref BS = ref(B.S[l], (long long)KBr * KBc, KBr, OP_N);
-    F.alloc(sz(nn, NL, NL), s);
+    {
+      HighScope full_blocks_are_long_lived;
+      F.alloc(sz(nn, NL, NL), s);
+    }
     // in chunks of full blocks: bounded T2 / T4 / U scratch (kChunkBytes each)
     const size_t per = size_t(W) * sizeof(double) * std::max(size_t(NL) * KBc, size_t(KAr) * std::max(KBc, NL));
     const int step = static_cast<int>(std::max<size_t>(4096, kChunkBytes / per));

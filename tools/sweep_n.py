@@ -5,7 +5,7 @@ complex, eps 1e-4) constructions over a range of N.  Per point: resident operand
 MmpReport.flops; executed flops = 2 / 6 (Gauss complex) x flops_exec; fraction of the measured
 DMMA peak.  Points that do not fit the HBM are recorded as such.
 
-Usage: python tools/sweep_n.py [out.json]"""
+Usage: python tools/sweep_n.py [out.json] [family:N1,N2,...]"""
 import gc
 import json
 import os
@@ -21,6 +21,9 @@ out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/sweep_n.json"
 peak, _ = bench.fp64_peak_tflops()
 points = [("cfg2", n) for n in (8192, 16384, 32768, 65536, 131072, 262144)] + \
          [("cfg5", n) for n in (16384, 65536, 262144, 1048576)]
+if len(sys.argv) > 2:  # e.g. cfg2:65536,131072
+    fam, _, ns = sys.argv[2].partition(":")
+    points = [(fam, int(x)) for x in ns.split(",")]
 rows = []
 for name, n in points:
     rec = {"family": name, "N": n, "eps": bench.CONFIGS[name][3]}
