@@ -964,10 +964,19 @@ struct EngineRun {
     const int gx = std::max(1, std::min(sp.n_out, (148 * 16) / std::max(1, tiles)));
     seg_gemm5_kernel<TM, TN, CX, 8, 4, WM, WN><<<dim3(gx, tiles), 32 * WM * WN, sm, s>>>(sp);
   }
-  bool use_v5(int TM, int TN) const { return seg_v5 && TM <= 32 && TN <= 32; }
+  // v5 also by default for launches of many outputs with little work each (<= 4 k-chunks per
+  // output, e.g. cfg3's 619k level-11 targets of 40 x 40 from 2 entries of K = 8), where v3's
+  // one-output CTAs are dominated by their prologue / epilogue; H2B_NO_V5_AUTO=1 disables
+  const bool no_v5_auto = std::getenv("H2B_NO_V5_AUTO") != nullptr;
+  double last_cpo = 1e30;  // k-chunks per output of the current seg() launch
+  int last_nout = 0;
+  bool use_v5(int TM, int TN) const {
+    if (seg_v5) return TM <= 32 && TN <= 32;
+    return !no_v5_auto && last_cpo <= 4.0 && last_nout >= 4096;
+  }
   template <int TM, int TN, int WM, int WN>
   void launch_seg8(const SegParams& sp, int tiles) {
-    if constexpr (TM <= 32 && TN <= 32) {
+    {
       if (use_v5(TM, TN)) {
         if (cplx) launch_v5_cfg<TM, TN, true, WM, WN>(sp, tiles);
         else launch_v5_cfg<TM, TN, false, WM, WN>(sp, tiles);
@@ -989,7 +998,7 @@ struct EngineRun {
     for (int g = 0; g < sp.ngroups; ++g) v3 = v3 && sp.g[g].K % 8 == 0;
     if (v3) {
       bool v5 = false;
-      if constexpr (TM <= 32 && TN <= 32) {
+      {
         if (use_v5(TM, TN)) {
           v5 = true;
           if (cplx) launch_v5_cfg<TM, TN, true>(sp, tiles);
@@ -1079,6 +1088,12 @@ struct EngineRun {
     int64_t macs = 0;
     for (const Grp& g : gs) macs += (g.csr ? g.csr->entries : n_out) * int64_t(M) * N * g.K;
     if (sym) macs = macs / 2 + macs / (2 * ((M + 63) / 64));
+    {
+      double chunks = 0;
+      for (const Grp& g : gs) chunks += double(g.csr ? g.csr->entries : n_out) * ((g.K + 7) / 8);
+      last_cpo = chunks / std::max(1, n_out);
+      last_nout = n_out;
+    }
     if (profiling && prof_shapes) {
       shape_tag = " [" + std::to_string(M) + "x" + std::to_string(N) + " K";
       int64_t ent = 0;
