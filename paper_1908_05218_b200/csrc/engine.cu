@@ -964,10 +964,10 @@ struct EngineRun {
     const int gx = std::max(1, std::min(sp.n_out, (148 * 16) / std::max(1, tiles)));
     seg_gemm5_kernel<TM, TN, CX, 8, 4, WM, WN><<<dim3(gx, tiles), 32 * WM * WN, sm, s>>>(sp);
   }
-  // v5 also by default for launches of many outputs with little work each (<= 4 k-chunks per
-  // output, e.g. cfg3's 619k level-11 targets of 40 x 40 from 2 entries of K = 8), where v3's
-  // one-output CTAs are dominated by their prologue / epilogue; H2B_NO_V5_AUTO=1 disables
-  const bool no_v5_auto = std::getenv("H2B_NO_V5_AUTO") != nullptr;
+  // H2B_V5_AUTO=1: v5 also for launches of many outputs with little work each (<= 4 k-chunks per
+  // output, e.g. cfg3's 619k level-11 targets of 40 x 40 from 2 entries of K = 8).  Measured
+  // neutral to 1 % slower (profiles/r01/ab_v5auto.txt), so off by default.
+  const bool no_v5_auto = std::getenv("H2B_V5_AUTO") == nullptr;
   double last_cpo = 1e30;  // k-chunks per output of the current seg() launch
   int last_nout = 0;
   bool use_v5(int TM, int TN) const {
