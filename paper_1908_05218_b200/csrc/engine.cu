@@ -1121,12 +1121,17 @@ struct EngineRun {
     // and the remainder strip run as separate launches on shifted views, the
     // strip with a 16/32-wide tile class instead of a mostly-padding 64 tile.
     const int rm = M % 64, rn = N % 64;
-    const bool splitM = !sym && !seg_v1 && !no_strips && M > 64 && rm > 0 && rm <= 32;
-    const bool splitN = !sym && !seg_v1 && !no_strips && N > 64 && rn > 0 && rn <= 32;
+    // H2B_STRIPS_SMALL=1: also outputs of 33..56 rows / columns as a 32-strip + a remainder strip
+    // (e.g. 40 = 32 + 8) instead of one mostly-padding 64 tile
+    const bool smM = strips_small && !sym && !seg_v1 && M > 32 && M < 64 && M - 32 <= 24;
+    const bool smN = strips_small && !sym && !seg_v1 && N > 32 && N < 64 && N - 32 <= 24;
+    const bool splitM = smM || (!sym && !seg_v1 && !no_strips && M > 64 && rm > 0 && rm <= 32);
+    const bool splitN = smN || (!sym && !seg_v1 && !no_strips && N > 64 && rn > 0 && rn <= 32);
     if (!splitM && !splitN) {
       launch_tiles(sp);
     } else {
-      const int mcuts[3] = {0, splitM ? M - rm : M, M}, ncuts[3] = {0, splitN ? N - rn : N, N};
+      const int cutM = smM ? 32 : M - rm, cutN = smN ? 32 : N - rn;
+      const int mcuts[3] = {0, splitM ? cutM : M, M}, ncuts[3] = {0, splitN ? cutN : N, N};
       for (int a = 0; a < (splitM ? 2 : 1); ++a)
         for (int b = 0; b < (splitN ? 2 : 1); ++b) {
           const int r0 = mcuts[a], r1 = splitM ? mcuts[a + 1] : M;
@@ -1147,6 +1152,7 @@ struct EngineRun {
     post();
   }
   const bool no_strips = std::getenv("H2B_NO_STRIPS") != nullptr;  // A/B: single launch per product
+  const bool strips_small = std::getenv("H2B_STRIPS_SMALL") != nullptr;
   // v4 (warps split the chunks of small output tiles): H2B_SEG_V4=1 enables
   const bool seg_v4 = std::getenv("H2B_SEG_V4") != nullptr;
   template <int TM, int TN>
