@@ -1121,16 +1121,24 @@ struct EngineRun {
     // and the remainder strip run as separate launches on shifted views, the
     // strip with a 16/32-wide tile class instead of a mostly-padding 64 tile.
     const int rm = M % 64, rn = N % 64;
-    // H2B_STRIPS_SMALL=1: also outputs of 33..56 rows / columns as a 32-strip + a remainder strip
-    // (e.g. 40 = 32 + 8) instead of one mostly-padding 64 tile
-    const bool smM = strips_small && !sym && !seg_v1 && M > 32 && M < 64 && M - 32 <= 24;
-    const bool smN = strips_small && !sym && !seg_v1 && N > 32 && N < 64 && N - 32 <= 24;
+    // outputs of 33..56 rows / columns as a 32-strip + a remainder strip (e.g. 40 = 32 + 8) instead
+    // of one mostly-padding 64 tile (cfg3 0.257 -> 0.227 s, cfg5s 0.371 -> 0.354 s, cfg2 neutral:
+    // profiles/r01/ab_strips_small.txt; H2B_NO_STRIPS_SMALL=1 disables); H2B_STRIPS_24=1 also
+    // 17..24 as 16 + remainder
+    auto small_cut = [&](int X) {
+      if (!strips_small || sym || seg_v1) return 0;
+      if (X > 32 && X < 64 && X - 32 <= 24) return 32;
+      if (strips_24 && X > 16 && X < 32 && X - 16 <= 8) return 16;
+      return 0;
+    };
+    const int scM = small_cut(M), scN = small_cut(N);
+    const bool smM = scM > 0, smN = scN > 0;
     const bool splitM = smM || (!sym && !seg_v1 && !no_strips && M > 64 && rm > 0 && rm <= 32);
     const bool splitN = smN || (!sym && !seg_v1 && !no_strips && N > 64 && rn > 0 && rn <= 32);
     if (!splitM && !splitN) {
       launch_tiles(sp);
     } else {
-      const int cutM = smM ? 32 : M - rm, cutN = smN ? 32 : N - rn;
+      const int cutM = smM ? scM : M - rm, cutN = smN ? scN : N - rn;
       const int mcuts[3] = {0, splitM ? cutM : M, M}, ncuts[3] = {0, splitN ? cutN : N, N};
       for (int a = 0; a < (splitM ? 2 : 1); ++a)
         for (int b = 0; b < (splitN ? 2 : 1); ++b) {
@@ -1152,7 +1160,8 @@ struct EngineRun {
     post();
   }
   const bool no_strips = std::getenv("H2B_NO_STRIPS") != nullptr;  // A/B: single launch per product
-  const bool strips_small = std::getenv("H2B_STRIPS_SMALL") != nullptr;
+  const bool strips_small = std::getenv("H2B_NO_STRIPS_SMALL") == nullptr;
+  const bool strips_24 = std::getenv("H2B_STRIPS_24") != nullptr;
   // v4 (warps split the chunks of small output tiles): H2B_SEG_V4=1 enables
   const bool seg_v4 = std::getenv("H2B_SEG_V4") != nullptr;
   template <int TM, int TN>

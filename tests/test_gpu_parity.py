@@ -287,7 +287,7 @@ def test_device_constructor_matches_host(name, monkeypatch):
         assert rel(dd, dh) <= 1e-11, rel(dd, dh)
 
 
-@pytest.mark.parametrize("knob", ["H2B_SEG_V4", "H2B_SEG_V5", "H2B_CPLX4M", "H2B_STRIPS_SMALL"])
+@pytest.mark.parametrize("knob", ["H2B_SEG_V4", "H2B_SEG_V5", "H2B_CPLX4M", "H2B_NO_STRIPS_SMALL", "H2B_STRIPS_24"])
 @pytest.mark.parametrize("name", ["cfg3", "cfg5"])
 def test_small_tile_kernels_match_oracle(ctx, name, knob, monkeypatch):
     """seg_gemm v4 (warps split the chunks of small output tiles, fixed-order reduction) and v5
