@@ -1121,7 +1121,7 @@ struct EngineRun {
     // and the remainder strip run as separate launches on shifted views, the
     // strip with a 16/32-wide tile class instead of a mostly-padding 64 tile.
     const int rm = M % 64, rn = N % 64;
-    // outputs of 33..40 rows / columns as a 32-strip + a remainder strip (40 = 32 + 8) instead of
+    // outputs of 33..48 rows / columns as a 32-strip + a remainder strip (40 = 32 + 8) instead of
     // one mostly-padding 64 tile (profiles/r01/ab_strips_small.txt; H2B_NO_STRIPS_SMALL=1
     // disables, H2B_STRIPS_SMALL_MAX sets the largest remainder); H2B_STRIPS_24=1 also 17..24 as
     // 16 + remainder
@@ -1162,10 +1162,10 @@ struct EngineRun {
   const bool no_strips = std::getenv("H2B_NO_STRIPS") != nullptr;  // A/B: single launch per product
   const bool strips_small = std::getenv("H2B_NO_STRIPS_SMALL") == nullptr;
   const bool strips_24 = std::getenv("H2B_STRIPS_24") != nullptr;
-  // largest remainder split off a 33..63-wide output (H2B_STRIPS_SMALL_MAX, default 8: 40 = 32 + 8)
+  // largest remainder split off a 33..63-wide output (H2B_STRIPS_SMALL_MAX, default 16: 48 = 32 + 16)
   const int strips_small_max = [] {
     const char* e = std::getenv("H2B_STRIPS_SMALL_MAX");
-    return e ? std::atoi(e) : 8;
+    return e ? std::atoi(e) : 16;
   }();
   // v4 (warps split the chunks of small output tiles): H2B_SEG_V4=1 enables
   const bool seg_v4 = std::getenv("H2B_SEG_V4") != nullptr;
