@@ -2,22 +2,28 @@
 """Benchmark of the B200 H^2-MMP on the BASELINE.json workload.
 
 A "step" is one accuracy-controlled product C = A*A (h2mmp::mmp,
-mmp.cpp:688-691) of the configs[1] workload: Laplace 1/(4 pi r) on N=65,536
-seeded uniform points (reference RNG, geometry.cpp:39-52, seed 1), leaf size
-64, eta = 1, nested tensor-Chebyshev bases of order 4 (k = 64), eps = 1e-8.
+mmp.cpp:688-691) of the largest single-GPU BASELINE configuration, configs[4]
+(default `--config cfg5`): Helmholtz exp(-i kappa r)/(4 pi r), complex128,
+N = 2^20 Fibonacci-sphere points of diameter 16 wavelengths, leaf 64,
+Chebyshev order growing with the box size in wavelengths, recompressed at 1e-4;
+eps = 1e-4.  `--config cfg1..cfg4` run the other BASELINE configurations.
 
-  value : FP64 GFLOP/s = 2 * MmpReport.flops (the reference's MAC counter,
-          mmp.cpp:67-80; identical to the oracle's) / device time per product,
-          operands resident in HBM, CUDA events on the library's stream.
+  value : FP64 GFLOP/s = F_alg / device time per product with F_alg = 2 (real)
+          or 8 (complex) x MmpReport.flops (the reference's MAC counter,
+          mmp.cpp:67-80; identical to the oracle's), operands resident in HBM,
+          CUDA events on the library's stream.
   e2e   : same metric through the drop-in C-ABI call h2c_mmp with pinned host
-          buffers (H2D of A, D2H of C inside the timed region).
+          buffers (H2D of A, D2H of C inside the timed region); the first
+          (cold) call of a fresh context is reported next to it.
 
-`--config cfg4` runs configs[3] instead: C = A*B on the 64^3 grid (N=262,144), A the
-7-point FD Laplacian in H^2 form, B the Laplace Chebyshev operand (k=64), eps 1e-6.
-
-`--impl reference` times the CPU oracle (a C++ restatement of the reference,
-whose Eigen build cannot be compiled here) on a bounded sample of the same
-workload with every host core running an independent product.
+`--impl reference` times the CPU oracle (the C++ restatement of the
+reference's mmp.cpp; the reference itself needs Eigen, absent here) on the SAME
+configuration and N, with every host core (oracle/product_engine.cpp, bit-
+identical to the single-thread restatement): each step is a consecutive
+time slice of one running product (products run back to back), value = the
+reference MACs counted in the timed slices / their wall time.  Its inputs come
+from the CPU-only generator oracle/_build/libh2inputs.so; it never maps the
+B200 library or touches the GPU.
 """
 from __future__ import annotations
 
@@ -61,8 +67,10 @@ CONFIGS = {
     "cfg4s": (110592, 64, 4, 1e-6, "configs[3] construction on the 48^3 grid (h = 1/49): C = A*B, A = 7-point FD "
                                    "Laplacian, B = Laplace Chebyshev order 4 (k=64), leaf 64, eta 1, eps 1e-6"),
 }
-# bounded CPU sample of the same construction (oracle single-thread ~10-30 s)
-CPU_SAMPLE = {"cfg1": 4096, "cfg2": 4096, "cfg3": 4096, "cfg4": 4096, "cfg4s": 4096, "cfg5": 4096, "cfg5s": 4096}
+DEFAULT_CONFIG = "cfg5"
+# CPU baseline of the B200 arm: one warm-up slice + CPU_SLICES slices of CPU_SLICE_S seconds of
+# the all-cores oracle product on the same workload (~20 s of CPU work)
+CPU_WARM_S, CPU_SLICE_S, CPU_SLICES = 2.0, 5.0, 4
 KAPPA = 2.0 * np.pi  # cfg5: wavelength 1
 
 
@@ -217,61 +225,69 @@ def measured_traffic(kernel: str):
         return None, None
 
 
-def cpu_sample(name: str, threads_note: int = 1) -> dict:
-    """Single-thread oracle on the bounded sample; returns GFLOP/s and details."""
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def sliced_oracle(A, B, eps, warm: list[float], timed: list[float], threads: int) -> dict:
+    """Consecutive slices of the all-cores oracle product C = A*B (oracle/pyoracle.SlicedProduct):
+    untimed warm-up slices, then timed slices; GFLOP/s = F_alg of the MACs counted in the timed
+    slices / their wall time."""
     from oracle import pyoracle as O
-    import paper_1908_05218_b200 as P
-    n_full, leaf, order, eps, _ = CONFIGS[name]
-    n = CPU_SAMPLE[name]
-    _, _, _, A, B = build_operands(name, n)
+    import paper_1908_05218_b200.h2c as H
+    fpm = 8.0 if A.scalar == H.H2C_COMPLEX else 2.0
     t0 = time.perf_counter()
-    r = O.mmp(A, B, eps)
-    dt = time.perf_counter() - t0
-    fpm = 8.0 if A.scalar == P.H2C_COMPLEX else 2.0
-    return {"gflops": fpm * r.report.flops / dt / 1e9, "fpm": fpm, "seconds": dt, "flops": r.report.flops, "n": n,
-            "wall_seconds_report": r.report.wall_seconds}
-
-
-def _cpu_worker(name, q):
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    q.put(cpu_sample(name))
+    S = O.SlicedProduct(A, B, eps, threads)
+    setup = time.perf_counter() - t0
+    try:
+        for w in warm:
+            S.step(w)
+        secs, macs, per = 0.0, 0, []
+        prods = 0
+        for t in timed:
+            el, m, prods = S.step(t)
+            secs += el
+            macs += m
+            per.append(el)
+    finally:
+        S.close()
+    return {"gflops": fpm * macs / secs / 1e9, "seconds": secs, "macs": macs, "fpm": fpm, "products_done": prods,
+            "slice_seconds": per, "setup_seconds": setup}
 
 
 def run_reference(args) -> None:
+    """Reference arm: the CPU oracle on the same config, all host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import multiprocessing as mp
-    cores = os.cpu_count() or 1
+    from paper_1908_05218_b200 import h2c
+    h2c.use_inputs_library()  # CPU-only input generator: this arm never maps the B200 library
     name = args.config
-    ctx = mp.get_context("spawn")
-    times = []
-    total_flops = 0
-    # warmup (untimed) then K steps, each step = `cores` independent single-thread oracle products
-    for step in range(args.warmup + args.steps):
-        q = ctx.Queue()
-        procs = [ctx.Process(target=_cpu_worker, args=(name, q)) for _ in range(cores)]
-        t0 = time.perf_counter()
-        for p in procs:
-            p.start()
-        res = [q.get() for _ in procs]
-        for p in procs:
-            p.join()
-        dt = time.perf_counter() - t0
-        if step >= args.warmup:
-            times.append(dt)
-            total_flops = sum(r["flops"] * r["fpm"] / 2.0 for r in res)
-    mean = sum(times) / len(times)
-    value = 2.0 * total_flops / mean / 1e9
-    sample = (f"{cores} concurrent single-thread oracle products of the {name} construction at "
-              f"N={CPU_SAMPLE[name]} (leaf {CONFIGS[name][1]}, order {CONFIGS[name][2]}, eps {CONFIGS[name][3]})")
-    line = {"metric": "H2-MMP FP64 GFLOP/s (F_alg = 2 real / 8 complex x MmpReport.flops per product / wall)", "value": value, "unit": "GFLOP/s",
+    W = build_workload(name)
+    cores = host_cores()
+    r = sliced_oracle(W["A"], W["B"], W["eps"], [1.0] * args.warmup, [args.ref_slice] * args.steps, cores)
+    value = r["gflops"]
+    sample = (f"{args.steps} consecutive ~{args.ref_slice:g} s slices (after {args.warmup} x 1 s warm-up slices) of "
+              f"all-cores oracle products (C++ restatement of mmp.cpp, {cores} threads, bit-identical to 1 thread) "
+              f"on the same {name} workload at N={W['n']}; {r['macs']:.3e} reference MACs in {r['seconds']:.1f} s, "
+              f"{r['products_done']} complete products so far; inputs from the CPU-only generator "
+              f"(build {W['build_seconds']:.0f} s, oracle conversion {r['setup_seconds']:.0f} s, untimed)")
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": {"workload": name, "desc": CONFIGS[name][4]},
-            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "ms_per_step": round(1e3 * r["seconds"] / max(1, args.steps), 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128" if r["fpm"] == 8.0 else "f64", "data": "synthetic",
+            "config": {"workload": name, "desc": W["desc"], "N": W["n"], "eps": W["eps"]},
+            "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+METRIC = "H2-MMP FP64 GFLOP/s (F_alg = 2 real / 8 complex x MmpReport.flops per product / wall)"
 
 
 # ---------------------------------------------------------------------------
@@ -288,6 +304,32 @@ def max_over_ranks(x: float, dist, device: str) -> float:
 def job_throughput(flops_per_rank: float, world: int, seconds: float) -> float:
     """Whole-job GFLOP/s: every rank runs one product (replicas, weak scaling)."""
     return world * flops_per_rank / seconds / 1e9
+
+
+def hbm_peak_gbs() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    except Exception:
+        return 7700.0, "fallback: nominal B200 HBM3e"
+
+
+def kernel_roofline(e: dict, fpm_exec: float, peak_tf: float, peak_gbs: float) -> dict:
+    """Roofline of one profiled (phase, kernel) entry: FP64 tensor bound when its arithmetic
+    intensity (executed flops / algorithmic bytes) is above the ridge, HBM bound below."""
+    fl = fpm_exec * e["macs"]
+    by = e.get("bytes", 0) or 0
+    s = e["ms"] * 1e-3
+    ridge = peak_tf * 1e12 / (peak_gbs * 1e9)
+    ai = fl / by if by else float("inf")
+    if ai >= ridge:
+        ach = fl / s / 1e12
+        return {"bound": "tensor", "achieved": round(ach, 3), "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": round(ach / peak_tf, 4), "intensity": round(ai, 2)}
+    ach = by / s / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
+            "frac": round(ach / peak_gbs, 4), "intensity": round(ai, 2)}
 
 
 def run_b200(args) -> None:
@@ -309,6 +351,19 @@ def run_b200(args) -> None:
     W = build_workload(args.config)
     A, B, eps = W["A"], W["B"], W["eps"]
     ctx = P.Context(local)
+
+    # cold drop-in call on the fresh context: structure plan, arena, upload, product, download
+    Ap, _pin = P.pin_matrix(A)
+    Bp, _pinb = (Ap, None) if B is A else P.pin_matrix(B)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = P.mmp(Ap, Bp, eps, ctx)
+    torch.cuda.synchronize()
+    cold_s = time.perf_counter() - t0
+    plan_s = res.report.plan_seconds
+    del res
+    gc.collect()
+
     dA = P.ResidentOperand(A, ctx)
     dB = dA if B is A else P.ResidentOperand(B, ctx)
 
@@ -340,7 +395,7 @@ def run_b200(args) -> None:
     flops = fpm * rep.flops
     value = job_throughput(flops, world, ms * 1e-3)
 
-    # roofline of the dominant kernel: one profiled (untimed) product
+    # roofline of the dominant kernel (and of the next ones): one profiled (untimed, serialised) product
     ctx.set_profile(True)
     P.mmp_resident(dA, dB, eps)
     prof_all = ctx.profile()
@@ -348,27 +403,30 @@ def run_b200(args) -> None:
     prof = [e for e in prof_all if not e["name"].startswith(("wall:", "host:"))]
     walls = [e for e in prof_all if e["name"].startswith("wall:")]
     peak, peak_src = fp64_peak_tflops()
-    dom = max(prof, key=lambda e: e["ms"]) if prof else None
+    hbm, hbm_src = hbm_peak_gbs()
     prof_ms = sum(e["ms"] for e in prof) if prof else 0.0
     roofline = None
-    if dom:
-        ach = fpm_exec * dom["macs"] / (dom["ms"] * 1e-3) / 1e12
+    kernels = []
+    if prof:
+        top = sorted(prof, key=lambda e: -e["ms"])
+        dom = top[0]
+        rl = kernel_roofline(dom, fpm_exec, peak, hbm)
         traffic, traffic_src = measured_traffic(f"{args.config}:{dom['name']}")
-        roofline = {"bound": "tensor", "kernel": dom["name"], "launches": dom["launches"],
-                    "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+        roofline = {**rl, "kernel": dom["name"], "launches": dom["launches"],
                     "traffic": traffic, "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
                     "flops_per_launch": fpm_exec * dom["macs"] / dom["launches"],
+                    "alg_bytes_per_launch": (dom.get("bytes", 0) or 0) / dom["launches"],
                     "flops_per_mac_exec": fpm_exec,
-                    "peak_source": peak_src,
+                    "peak_source": peak_src if rl["bound"] == "tensor" else hbm_src,
                     "share_of_step": round(dom["ms"] / prof_ms, 4) if prof_ms else None,
                     "pipeline_exec_tflops": round(fpm_exec * rep.flops_exec / (ms * 1e-3) / 1e12, 3),
                     "pipeline_frac": round(fpm_exec * rep.flops_exec / (ms * 1e-3) / 1e12 / peak, 4)}
+        for e in top[:10]:
+            kernels.append({"kernel": e["name"], "ms": round(e["ms"], 2), "share": round(e["ms"] / prof_ms, 4),
+                            **kernel_roofline(e, fpm_exec, peak, hbm)})
 
-    # end-to-end through the drop-in C-ABI call with pinned host buffers
+    # end-to-end through the drop-in C-ABI call with pinned host buffers (warm context)
     del dA, dB
-    Ap, _pin = P.pin_matrix(A)
-    Bp, _pinb = (Ap, None) if B is A else P.pin_matrix(B)
-    P.mmp(Ap, Bp, eps, ctx)  # warm (plan cached, pool warm)
     gc.collect()
     e2e_times = []
     h2d = d2h = 0
@@ -392,32 +450,44 @@ def run_b200(args) -> None:
     # reference's seeded random_vector (metrics.cpp:37-55), exact H^2 MVPs on the device (untimed)
     eps_rel = P.relative_error(A, B, last.product, 1, ctx)
     del last
+    gc.collect()
     e2e_value = job_throughput(flops, world, e2e_s)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        c = cpu_sample(args.config)
-        cpu = {"value": round(c["gflops"], 3), "unit": "GFLOP/s", "cores": 1, "kind": "port",
-               "sample": f"single-thread oracle (C++ restatement + OpenBLAS, 1 thread) on the {args.config} "
-                         f"construction at N={c['n']}: {c['seconds']:.1f} s"}
+        ctx.close()
+        del ctx, Ap, Bp, _pin, _pinb
+        gc.collect()
+        cores = host_cores()
+        c = sliced_oracle(A, B, eps, [CPU_WARM_S], [CPU_SLICE_S] * CPU_SLICES, cores)
+        cpu = {"value": round(c["gflops"], 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
+               "sample": f"{CPU_SLICES} consecutive ~{CPU_SLICE_S:g} s slices (after a {CPU_WARM_S:g} s warm-up "
+                         f"slice) of the all-cores oracle product (C++ restatement of mmp.cpp, {cores} threads) "
+                         f"on the same {args.config} workload at N={W['n']}, from the start of the product: "
+                         f"{c['macs']:.3e} reference MACs in {c['seconds']:.1f} s"}
 
     if rank == 0:
         line = {
-            "metric": "H2-MMP FP64 GFLOP/s (F_alg = 2 real / 8 complex x MmpReport.flops per product / wall)", "value": round(value, 3),
+            "metric": METRIC, "value": round(value, 3),
             "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128" if A.scalar == P.H2C_COMPLEX else "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": W["desc"], "N": W["n"], "eps": eps,
                        "macs_per_step": int(rep.flops), "macs_exec_per_step": int(rep.flops_exec),
                        "flops_per_mac": fpm, "eps_rel": eps_rel, "build_seconds": round(W["build_seconds"], 1),
-                       "max_rank": rep.max_rank(), "l2": "inputs (%.1f GB) >> 126 MB L2" % ((A.values.nbytes + (0 if B is A else B.values.nbytes)) / 1e9),
+                       "max_rank": rep.max_rank(),
+                       "max_rank_per_level": [int(max(a, b)) for a, b in zip(rep.max_row_rank, rep.max_col_rank)],
+                       "l2": "inputs (%.1f GB) >> 126 MB L2" % ((A.values.nbytes + (0 if B is A else B.values.nbytes)) / 1e9),
                        "parallelism": f"replicas{world}"},
             "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "seconds": round(e2e_s, 4),
-                    "device_seconds_inside": round(sum(dev_s) / len(dev_s), 4)},
+                    "device_seconds_inside": round(sum(dev_s) / len(dev_s), 4),
+                    "cold_seconds": round(cold_s, 3), "plan_seconds": round(plan_s, 3),
+                    "cold_value": round(job_throughput(flops, world, cold_s), 3)},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "roofline": roofline,
+            "kernels": kernels,
             "cpu_baseline": cpu,
         }
         if args.profile:
@@ -430,16 +500,30 @@ def run_b200(args) -> None:
         dist.destroy_process_group()
 
 
+def spawn_replicas(args) -> int:
+    """`--gpus N` without a launcher: run N replicas (one process per GPU) under torchrun."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-slice", type=float, default=6.0, help="seconds per reference-arm step (oracle slice)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_replicas(args))
     if args.impl == "reference":
         run_reference(args)
     else:

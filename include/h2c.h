@@ -41,6 +41,9 @@ void h2c_set_profile(h2c_context* ctx, int on);
 int h2c_profile_count(const h2c_context* ctx);
 int h2c_profile_get(const h2c_context* ctx, int i, char* name, int cap, int64_t* launches, double* ms,
                     int64_t* macs);
+/* algorithmic HBM bytes of entry i (operands read once per product entry, outputs
+ * written or read+written when accumulating): the roofline's byte count */
+int64_t h2c_profile_bytes(const h2c_context* ctx, int i);
 
 /* ---- structure (host logic) ------------------------------------------
  * build_cluster_tree (cluster_tree.hpp:43, cluster_tree.cpp:66-93) followed by

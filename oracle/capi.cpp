@@ -3,8 +3,13 @@
 // Flat C-ABI over the oracle (oracle/h2o.h): converts the shared descriptors of
 // include/h2c_types.h to the reference-shaped C++ model and back.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 
 #include "h2o.h"
 #include "linalg.hpp"
@@ -14,6 +19,7 @@ using namespace h2o;
 
 namespace {
 thread_local std::string g_err;
+int g_mmp_threads = 1;  // h2o_set_mmp_threads
 
 int fail(const std::exception& e, int code) {
   g_err = e.what();
@@ -232,6 +238,7 @@ void fill_desc(const h2o_matrix& m, h2c_matrix* d) {
 
 const char* h2o_last_error(void) { return g_err.c_str(); }
 void h2o_set_threads(int n) { set_blas_threads(n); }
+void h2o_set_mmp_threads(int n) { g_mmp_threads = n < 1 ? 1 : n; }
 
 int64_t h2o_geometry_count(int family, uint64_t seed, int n, int bc, int spm, int sw, int st, int ae,
                            int cp) {
@@ -421,6 +428,7 @@ void run_mmp(const h2c_matrix* a, const h2c_matrix* b, double eps, int adaptive,
   const H2Matrix<S> hb = matrix_from<S>(*b, cs);
   MmpOptions opt;
   opt.ff_cache_bytes = cache;
+  opt.threads = g_mmp_threads;
   MmpResult<S> res = adaptive ? mmp<S>(ha, hb, eps, opt) : formatted_mmp<S>(ha, hb, opt);
   matrix_to(res.product, a->tree, a->blocks, r->m);
   r->rep = res.report;
@@ -585,3 +593,153 @@ int h2o_relative_error(const h2c_matrix* a, const h2c_matrix* b, const h2c_matri
   });
 }
 
+
+// ---- multi-vector exact MVP (one conversion for nv vectors) -------------------
+int h2o_mvp_multi(const h2c_matrix* m, const double* x, int nv, double* y) {
+  return guarded([&] {
+    const Converted cs = convert_structure(m->tree, m->blocks);
+    const int n = m->tree->n_points;
+    if (m->scalar == H2C_REAL) {
+      const H2Matrix<Real> h = matrix_from<Real>(*m, cs);
+      for (int v = 0; v < nv; ++v) {
+        const auto r = mvp(h, vec_in<Real>(x + size_t(v) * n, n));
+        std::memcpy(y + size_t(v) * n, r.data(), sizeof(double) * n);
+      }
+    } else {
+      const H2Matrix<Complex> h = matrix_from<Complex>(*m, cs);
+      for (int v = 0; v < nv; ++v) {
+        const auto r = mvp(h, vec_in<Complex>(x + 2 * size_t(v) * n, n));
+        std::memcpy(y + 2 * size_t(v) * n, r.data(), sizeof(Complex) * n);
+      }
+    }
+  });
+}
+
+// ---- sliced all-cores product (bench.py CPU baseline) ----------------------
+// One engine thread runs complete products back to back (mmp with
+// MmpOptions::threads); its slice points block once the granted slice time has
+// elapsed, so the caller measures consecutive slices of the very same product.
+namespace {
+struct Stopped {};
+struct SlicedBase {
+  virtual ~SlicedBase() = default;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool paused = true, stop = false, failed = false;
+  double slice_s = 0;
+  std::chrono::steady_clock::time_point slice_t0;
+  int64_t macs_now = 0, products = 0;
+  std::string err;
+  std::thread th;
+  void gate(int64_t macs) {
+    std::unique_lock<std::mutex> lk(mu);
+    macs_now = macs;
+    if (stop) throw Stopped{};
+    if (paused || std::chrono::duration<double>(std::chrono::steady_clock::now() - slice_t0).count() >= slice_s) {
+      paused = true;
+      cv.notify_all();
+      cv.wait(lk, [&] { return !paused || stop; });
+      if (stop) throw Stopped{};
+    }
+  }
+};
+template <class S>
+struct Sliced : SlicedBase {
+  Converted cs;
+  H2Matrix<S> a, b;
+  bool same = false;
+  double eps = 0;
+  int adaptive = 1, threads = 1;
+  void loop() {
+    try {
+      gate(0);  // wait for the first slice
+      int64_t base = 0;
+      for (;;) {
+        MmpOptions opt;
+        opt.threads = threads;
+        opt.gate = [this, &base](int64_t c) { gate(base + c); };
+        const H2Matrix<S>& bb = same ? a : b;
+        const int64_t f = adaptive ? mmp<S>(a, bb, eps, opt).report.flops : formatted_mmp<S>(a, bb, opt).report.flops;
+        base += f;
+        std::lock_guard<std::mutex> g(mu);
+        ++products;
+      }
+    } catch (const Stopped&) {
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> g(mu);
+      err = e.what();
+      failed = true;
+      paused = true;
+      cv.notify_all();
+    }
+  }
+};
+}  // namespace
+
+struct h2o_sliced {
+  std::unique_ptr<SlicedBase> s;
+};
+
+h2o_sliced* h2o_sliced_start(const h2c_matrix* a, const h2c_matrix* b, double eps, int adaptive, int threads) {
+  try {
+    if (a->tree != b->tree || a->blocks != b->blocks)
+      throw ConfigError("mmp: operands must share cluster trees and block structure");
+    auto* h = new h2o_sliced;
+    auto start = [&](auto* x) {
+      using T = std::remove_pointer_t<decltype(x)>;
+      using S = std::remove_reference_t<decltype(x->a.row_basis.leaf[0](0, 0))>;
+      x->cs = convert_structure(a->tree, a->blocks);
+      x->a = matrix_from<S>(*a, x->cs);
+      x->same = (a == b || a->values == b->values);
+      if (!x->same) x->b = matrix_from<S>(*b, x->cs);
+      x->eps = eps;
+      x->adaptive = adaptive;
+      x->threads = threads < 1 ? 1 : threads;
+      (void)sizeof(T);
+      h->s.reset(x);
+      x->th = std::thread([x] { x->loop(); });
+    };
+    if (a->scalar == H2C_REAL) start(new Sliced<Real>);
+    else start(new Sliced<Complex>);
+    return h;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+int h2o_sliced_step(h2o_sliced* h, double seconds, double* elapsed, int64_t* macs, int64_t* products) {
+  SlicedBase& s = *h->s;
+  std::unique_lock<std::mutex> lk(s.mu);
+  if (s.failed) {
+    g_err = s.err;
+    return H2C_ERR_INVARIANT;
+  }
+  const int64_t m0 = s.macs_now;
+  const auto t0 = std::chrono::steady_clock::now();
+  s.slice_s = seconds;
+  s.slice_t0 = t0;
+  s.paused = false;
+  s.cv.notify_all();
+  s.cv.wait(lk, [&] { return s.paused; });
+  *elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *macs = s.macs_now - m0;
+  *products = s.products;
+  if (s.failed) {
+    g_err = s.err;
+    return H2C_ERR_INVARIANT;
+  }
+  return H2C_OK;
+}
+
+void h2o_sliced_stop(h2o_sliced* h) {
+  if (!h) return;
+  {
+    std::lock_guard<std::mutex> g(h->s->mu);
+    h->s->stop = true;
+    h->s->paused = false;
+    h->s->cv.notify_all();
+  }
+  if (h->s->th.joinable()) h->s->th.join();
+  delete h;
+}

@@ -21,6 +21,9 @@ typedef struct h2o_result h2o_result;
 
 const char* h2o_last_error(void);
 void h2o_set_threads(int n); /* OpenBLAS threads (reference: single-threaded) */
+/* threads of the parallel restatement of the product (default 1; results are
+ * bit-identical for any count, see oracle/product_engine.cpp) */
+void h2o_set_mmp_threads(int n);
 
 /* geometry.cpp:141-181; family: 0 random_cloud, 1 bus, 2 slab, 3 cube_array */
 int64_t h2o_geometry_count(int family, uint64_t seed, int n, int bus_count, int samples_per_meter,
@@ -73,6 +76,20 @@ int64_t h2o_memory_footprint(const h2c_matrix* m);
 int h2o_random_vector(int n, uint64_t seed, int scalar, double* out);
 int h2o_relative_error(const h2c_matrix* a, const h2c_matrix* b, const h2c_matrix* c,
                        uint64_t seed, double* value, int* reference_was_zero);
+
+/* y[:, v] = A x[:, v] for nv vectors (N x nv column-major, complex interleaved) */
+int h2o_mvp_multi(const h2c_matrix* m, const double* x, int nv, double* y);
+
+/* Sliced all-cores product (bench.py CPU baseline): an engine thread runs
+ * complete products C = A*B back to back with `threads` threads; each step
+ * lets it run for `seconds` and returns at its next slice point with the wall
+ * time, the reference MACs counted in the slice and the products completed. */
+typedef struct h2o_sliced h2o_sliced;
+h2o_sliced* h2o_sliced_start(const h2c_matrix* a, const h2c_matrix* b, double eps, int adaptive,
+                             int threads);
+int h2o_sliced_step(h2o_sliced* s, double seconds, double* elapsed, int64_t* macs,
+                    int64_t* products);
+void h2o_sliced_stop(h2o_sliced* s);
 
 #ifdef __cplusplus
 }

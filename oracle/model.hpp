@@ -5,6 +5,7 @@
 #pragma once
 
 #include <array>
+#include <functional>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -206,6 +207,11 @@ struct MmpOptions {
   // oracle recomputes products instead of caching (identical values and
   // counters)
   std::int64_t ff_cache_bytes = std::int64_t(8) << 30;
+  // threads of the parallel restatement (1 = the reference's single thread;
+  // results are bit-identical for any count, oracle/product_engine.cpp)
+  int threads = 1;
+  // slice point callback (counted MACs so far); may block or throw
+  std::function<void(std::int64_t)> gate;
 };
 
 template <class S>

@@ -74,6 +74,14 @@ def lib() -> C.CDLL:
         L.h2o_relative_error.restype = C.c_int
         L.h2o_relative_error.argtypes = [C.POINTER(h2c_matrix)] * 3 + [C.c_uint64, C.POINTER(C.c_double),
                                                                         C.POINTER(C.c_int)]
+        L.h2o_set_mmp_threads.argtypes = [C.c_int]
+        L.h2o_mvp_multi.restype = C.c_int
+        L.h2o_mvp_multi.argtypes = [C.POINTER(h2c_matrix), P_f64, C.c_int, P_f64]
+        L.h2o_sliced_start.restype = C.c_void_p
+        L.h2o_sliced_start.argtypes = [C.POINTER(h2c_matrix), C.POINTER(h2c_matrix), C.c_double, C.c_int, C.c_int]
+        L.h2o_sliced_step.restype = C.c_int
+        L.h2o_sliced_step.argtypes = [C.c_void_p, C.c_double, C.POINTER(C.c_double), P_i64, P_i64]
+        L.h2o_sliced_stop.argtypes = [C.c_void_p]
         L.h2o_set_threads(1)
         _lib = L
     return _lib
@@ -183,9 +191,11 @@ def svd_truncate_gram(gram: np.ndarray, eps: float):
 
 
 def mmp(a: H2Matrix, b: H2Matrix, eps: float, adaptive: bool = True, ff_cache_bytes: int = 8 << 30,
-        with_margin: bool = False):
-    """mmp / formatted_mmp of the CPU oracle (mmp.cpp:688-719)."""
+        with_margin: bool = False, threads: int = 1):
+    """mmp / formatted_mmp of the CPU oracle (mmp.cpp:688-719).  threads > 1 runs the
+    parallel restatement (bit-identical result, oracle/product_engine.cpp)."""
     out = C.c_void_p()
+    lib().h2o_set_mmp_threads(int(threads))
     _check(lib().h2o_mmp(C.byref(a.desc()), C.byref(b.desc()), eps, int(adaptive), ff_cache_bytes, C.byref(out)))
     try:
         d = h2c_matrix()
@@ -232,6 +242,42 @@ def mvp(m: H2Matrix, x: np.ndarray) -> np.ndarray:
     y = np.zeros_like(xx)
     _check(lib().h2o_mvp(C.byref(m.desc()), xx.ctypes.data_as(P_f64), y.ctypes.data_as(P_f64)))
     return y
+
+
+def mvp_multi(m: H2Matrix, x: np.ndarray) -> np.ndarray:
+    """Y = A X for the columns of X (N x nv)."""
+    xx = np.asfortranarray(x, dtype=m.dtype)
+    if xx.ndim == 1:
+        xx = xx.reshape(-1, 1, order="F")
+    y = np.zeros_like(xx)
+    _check(lib().h2o_mvp_multi(C.byref(m.desc()), xx.ctypes.data_as(P_f64), xx.shape[1], y.ctypes.data_as(P_f64)))
+    return y
+
+
+class SlicedProduct:
+    """Consecutive slices of all-cores oracle products C = A*B (bench.py's CPU
+    baseline): step(seconds) lets the engine run that long, returns at its next
+    slice point with (wall seconds, reference MACs counted in the slice, products
+    completed so far).  Products run back to back while steps are requested."""
+
+    def __init__(self, a: H2Matrix, b: H2Matrix, eps: float, threads: int, adaptive: bool = True):
+        self._a, self._b = a, b  # the descriptors must outlive the engine
+        self._h = lib().h2o_sliced_start(C.byref(a.desc()), C.byref(b.desc()), eps, int(adaptive), int(threads))
+        if not self._h:
+            raise ConfigError(_err())
+
+    def step(self, seconds: float):
+        el, macs, prods = C.c_double(), C.c_int64(), C.c_int64()
+        _check(lib().h2o_sliced_step(self._h, seconds, C.byref(el), C.byref(macs), C.byref(prods)))
+        return el.value, int(macs.value), int(prods.value)
+
+    def close(self) -> None:
+        if self._h:
+            lib().h2o_sliced_stop(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def memory_footprint(m: H2Matrix) -> int:

@@ -54,7 +54,8 @@ class Context:
             name = C.create_string_buffer(128)
             n, ms, macs = C.c_int64(), C.c_double(), C.c_int64()
             L.h2c_profile_get(self._h, i, name, 128, C.byref(n), C.byref(ms), C.byref(macs))
-            out.append({"name": name.value.decode(), "launches": n.value, "ms": ms.value, "macs": macs.value})
+            out.append({"name": name.value.decode(), "launches": n.value, "ms": ms.value, "macs": macs.value,
+                        "bytes": int(L.h2c_profile_bytes(self._h, i))})
         return out
 
     def close(self):

@@ -25,7 +25,10 @@ CUDA_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-pthread", "-I/usr/local/cuda/include"]
 
 CU_SOURCES = ["engine.cu", "construct_dev.cu"]
-CPP_SOURCES = ["plan.cpp", "counters.cpp", "structure.cpp", "construct.cpp", "capi.cpp"]
+CPP_SOURCES = ["plan.cpp", "counters.cpp", "structure.cpp", "construct.cpp", "capi_inputs.cpp", "capi.cpp"]
+# CPU-only input generator (structure + synthetic BASELINE operands) for bench.py's reference arm
+INPUT_SOURCES = ["structure.cpp", "construct.cpp", "capi_inputs.cpp", "construct_dev_stub.cpp"]
+INPUTS_LIB = ROOT / "oracle" / "_build" / "libh2inputs.so"
 
 
 def _host_blas() -> list[str]:
@@ -85,6 +88,18 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_inputs_library(force: bool = False) -> Path:
+    """oracle/_build/libh2inputs.so: the host-only entry points of include/h2c.h that build the
+    structure and the synthetic inputs (no CUDA), so bench.py's reference arm never maps
+    libh2mmp_b200.so."""
+    INPUTS_LIB.parent.mkdir(parents=True, exist_ok=True)
+    srcs = [CSRC / s for s in INPUT_SOURCES]
+    if force or _stale(INPUTS_LIB, srcs + _headers()):
+        _run(["g++", *CXX_FLAGS, "-DH2C_INPUTS_ONLY", "-shared", "-o", str(INPUTS_LIB), *map(str, srcs),
+              *[("-Wl," + a) if a.startswith("-rpath") else a for a in _host_blas() if a != "-Xlinker"]])
+    return INPUTS_LIB
+
+
 def build_oracle(force: bool = False) -> Path | None:
     """The CPU oracle (test infrastructure) — built here so it travels with the snapshot."""
     odir = ROOT / "oracle"
@@ -101,3 +116,4 @@ if __name__ == "__main__":
     force = "--force" in sys.argv
     print(build_library(force=force, verbose=True))
     print(build_oracle(force=force))
+    print(build_inputs_library(force=force))

@@ -18,18 +18,13 @@
 #include "counters.hpp"
 #include "engine.hpp"
 #include "structure.hpp"
+#include "capi_inputs.hpp"
 
 using namespace h2b;
 
 struct h2c_context {
   std::unique_ptr<Context> ctx;
   std::string err;
-};
-struct h2c_structure {
-  std::unique_ptr<Structure> s;
-};
-struct h2c_h2 {
-  std::unique_ptr<HostH2> m;
 };
 struct h2c_result {
   HostResult r;
@@ -41,7 +36,7 @@ struct h2c_operand {
 };
 
 namespace {
-thread_local std::string g_err;
+#define g_err (h2b::capi_error())
 
 int code_of(const std::exception& e) {
   if (dynamic_cast<const std::invalid_argument*>(&e)) return H2C_ERR_CONFIG;
@@ -90,6 +85,10 @@ void h2c_set_profile(h2c_context* ctx, int on) {
   if (ctx) ctx->ctx->profile = on != 0;
 }
 int h2c_profile_count(const h2c_context* ctx) { return ctx ? static_cast<int>(ctx->ctx->last_profile.size()) : 0; }
+int64_t h2c_profile_bytes(const h2c_context* ctx, int i) {
+  if (!ctx || i < 0 || i >= static_cast<int>(ctx->ctx->last_profile.size())) return -1;
+  return ctx->ctx->last_profile[i].bytes;
+}
 int h2c_profile_get(const h2c_context* ctx, int i, char* name, int cap, int64_t* launches, double* ms,
                     int64_t* macs) {
   if (!ctx || i < 0 || i >= static_cast<int>(ctx->ctx->last_profile.size())) return H2C_ERR_CONFIG;
@@ -103,80 +102,6 @@ int h2c_profile_get(const h2c_context* ctx, int i, char* name, int cap, int64_t*
   if (macs) *macs = e.macs;
   return H2C_OK;
 }
-
-h2c_structure* h2c_build_structure(const double* xyz, int n, int leafsize, double eta) {
-  try {
-    auto* s = new h2c_structure;
-    s->s = build_structure(xyz, n, leafsize, eta);
-    return s;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return nullptr;
-  }
-}
-void h2c_structure_tree(const h2c_structure* s, h2c_tree* out) { s->s->tree_desc(out); }
-void h2c_structure_blocks(const h2c_structure* s, h2c_blocks* out) { s->s->blocks_desc(out); }
-void h2c_structure_free(h2c_structure* s) { delete s; }
-
-int h2c_target_status(const h2c_tree* tree, const h2c_blocks* blocks, int t, int s) {
-  try {
-    return target_status(*tree, *blocks, t, s);
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return -1;
-  }
-}
-
-int h2c_random_cloud(int n, uint64_t seed, double* xyz) {
-  if (n < 1) {
-    g_err = "random_cloud: n must be positive";
-    return H2C_ERR_CONFIG;
-  }
-  std::mt19937_64 eng(seed);
-  for (int64_t i = 0; i < 3 * int64_t(n); ++i) xyz[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
-  return H2C_OK;
-}
-
-h2c_h2* h2c_build_chebyshev(const h2c_tree* tree, const h2c_blocks* blocks, const double* xyz, int kernel,
-                            double kappa, double diagonal, int order, double eps_recompress, int threads) {
-  try {
-    if (order < 1) throw std::invalid_argument("chebyshev order must be >= 1");
-    const std::vector<int> orders(tree->depth + 1, order);
-    return h2c_build_chebyshev_orders(tree, blocks, xyz, kernel, kappa, diagonal, orders.data(), eps_recompress,
-                                      threads);
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return nullptr;
-  }
-}
-
-h2c_h2* h2c_build_chebyshev_orders(const h2c_tree* tree, const h2c_blocks* blocks, const double* xyz, int kernel,
-                                   double kappa, double diagonal, const int* orders, double eps_recompress,
-                                   int threads) {
-  try {
-    auto m = std::make_unique<h2c_h2>();
-    m->m = build_chebyshev(*tree, *blocks, xyz, kernel, kappa, diagonal, orders, eps_recompress,
-                           threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency())));
-    return m.release();
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return nullptr;
-  }
-}
-
-h2c_h2* h2c_build_fd_laplacian(const h2c_tree* tree, const h2c_blocks* blocks, const double* xyz, double h) {
-  try {
-    auto* m = new h2c_h2;
-    m->m = build_fd_laplacian(*tree, *blocks, xyz, h);
-    return m;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return nullptr;
-  }
-}
-
-void h2c_h2_desc(const h2c_h2* m, h2c_matrix* out) { m->m->desc(out); }
-void h2c_h2_free(h2c_h2* m) { delete m; }
 
 static int run_mmp(h2c_context* ctx, const h2c_matrix* a, const h2c_matrix* b, double eps, int adaptive,
                    h2c_result** out) {
@@ -364,17 +289,6 @@ int h2c_to_dense(h2c_context* ctx, const h2c_matrix* a, double* out) {
     auto op = ctx->ctx->upload(*a);
     ctx->ctx->to_dense(op, out);
   });
-}
-
-int h2c_random_vector(int n, uint64_t seed, int scalar, double* out) {
-  if (n < 0) {
-    g_err = "random_vector: negative length";
-    return H2C_ERR_CONFIG;
-  }
-  std::mt19937_64 eng(seed);
-  auto u = [&eng] { return 2.0 * (static_cast<double>(eng() >> 11) * 0x1.0p-53) - 1.0; };
-  for (int64_t i = 0; i < int64_t(n) * (scalar == H2C_COMPLEX ? 2 : 1); ++i) out[i] = u();
-  return H2C_OK;
 }
 
 int h2c_truncate_gram(h2c_context* ctx, int scalar, const double* gram, int n, double eps, double* basis, int* rank,

@@ -720,6 +720,7 @@ struct EngineRun {
     std::string phase;
     const char* kernel;
     int64_t macs;
+    int64_t bytes;
     cudaEvent_t a, b;
   };
   bool profiling = false;
@@ -732,13 +733,13 @@ struct EngineRun {
   // launches of one phase (ncu --nvtx --nvtx-include "L9.targets:seg_gemm]")
   const bool nvtx = std::getenv("H2B_NVTX") != nullptr;
   int nvtx_depth = 0;
-  void pre(const char* kernel, int64_t macs) {
+  void pre(const char* kernel, int64_t macs, int64_t bytes = 0) {
     if (nvtx) {
       nvtxRangePushA((phase + ":" + kernel).c_str());
       ++nvtx_depth;
     }
     if (!profiling) return;
-    ProfRec r{phase + shape_tag, kernel, macs, nullptr, nullptr};
+    ProfRec r{phase + shape_tag, kernel, macs, bytes, nullptr, nullptr};
     shape_tag.clear();
     CK(cudaEventCreate(&r.a));
     CK(cudaEventCreate(&r.b));
@@ -1103,7 +1104,12 @@ struct EngineRun {
       }
       shape_tag += " e/out " + std::to_string(ent / std::max(1, n_out)) + " out " + std::to_string(n_out) + "]";
     }
-    pre("seg_gemm", macs);
+    int64_t bytes = int64_t(n_out) * M * N * 8 * W * (acc ? 2 : 1);
+    for (const Grp& g : gs) {
+      const int64_t ent = g.csr ? g.csr->entries : n_out;
+      bytes += ent * (int64_t(M) * g.K + int64_t(g.K) * N) * 8 * W;
+    }
+    pre("seg_gemm", macs, bytes);
     if (seg_wide && !seg_v1 && !sym && (M > 64 || N > 64)) {
       const int tm = M > 64 ? 128 : 64, tn = N > 64 ? 128 : 64;
       const int tiles = ((M + tm - 1) / tm) * ((N + tn - 1) / tn);
@@ -1255,7 +1261,7 @@ struct EngineRun {
   void seg_add(double* out, long long Os, const double* in, long long Is, const DevCsr& c, long long elems) {
     if (c.n_out <= 0) return;
     const int chunks = static_cast<int>(std::min<long long>(8, (elems / 2 + 255) / 256));
-    pre("seg_add", 0);
+    pre("seg_add", 0, (c.entries + c.n_out) * elems * 8 * W);
     seg_add_kernel<<<dim3(c.n_out, std::max(1, chunks)), 256, 0, s>>>(out, Os * W, in, Is * W, c.ptr, c.li,
                                                                       elems * W, 0);
     CK(cudaGetLastError());
@@ -1276,7 +1282,7 @@ struct EngineRun {
     Trunc t;
     DBuf G(sz(count, n, n), s);
     t.degen.alloc(count, s);
-    pre("gram_combine", 0);
+    pre("gram_combine", 0, 4LL * count * n * n * 8 * W);
     // few large Grams (upper levels): spread each over P CTAs (two passes)
     const int P = static_cast<int>(std::min<long long>(std::max(1, 1184 / std::max(count, 1)),
                                                        std::max<long long>(1, (long long)n * n * W / 4096)));
@@ -1581,7 +1587,7 @@ struct EngineRun {
   void gather(DBuf& out, int count, const double* src, long long Ss, int R, int Cc, const int* idx) {
     out.alloc(sz(count, 2 * R, 2 * Cc), s);
     if (count <= 0) return;
-    pre("gather_quad", 0);
+    pre("gather_quad", 0, 2LL * count * 4 * R * Cc * 8 * W);
     gather_quad_kernel<<<count, 256, 0, s>>>(out, src, Ss, R, Cc, idx, nullptr, W);
     CK(cudaGetLastError());
     post();
@@ -2294,13 +2300,14 @@ struct EngineRun {
       auto it = at.find(key);
       if (it == at.end()) {
         at[key] = out.size();
-        out.push_back({key, 0, 0.0, 0});
+        out.push_back({key, 0, 0.0, 0, 0});
         it = at.find(key);
       }
       ProfileEntry& e = out[it->second];
       e.launches++;
       e.ms += ms;
       e.macs += r.macs;
+      e.bytes += r.bytes;
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
     }
@@ -2314,10 +2321,10 @@ struct EngineRun {
       for (size_t i = 0; i < marks.size(); ++i) {
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, marks[i].second, i + 1 < marks.size() ? marks[i + 1].second : end));
-        out.push_back({"wall:" + marks[i].first, 1, ms, 0});
+        out.push_back({"wall:" + marks[i].first, 1, ms, 0, 0});
       }
       for (size_t i = 0; i + 1 < host_marks.size(); ++i)
-        out.push_back({"host:" + host_marks[i].first, 1, host_marks[i + 1].second - host_marks[i].second, 0});
+        out.push_back({"host:" + host_marks[i].first, 1, host_marks[i + 1].second - host_marks[i].second, 0, 0});
       host_marks.clear();
       for (auto& m : marks) cudaEventDestroy(m.second);
       cudaEventDestroy(end);

@@ -19,6 +19,7 @@ struct ProfileEntry {
   int64_t launches = 0;
   double ms = 0;
   int64_t macs = 0;
+  int64_t bytes = 0;  // algorithmic HBM bytes (operands read once per entry, outputs written / accumulated)
 };
 
 // Reusable pinned host buffers for product downloads (pinning tens of GB per

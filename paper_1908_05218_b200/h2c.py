@@ -358,81 +358,108 @@ class MmpResult:
 _lib = None
 
 
+# CPU-only input generator (structure + synthetic operands, no MMP entry points):
+# oracle/_build/libh2inputs.so, built from this package's host sources
+INPUTS_LIBPATH = PKG.parent / "oracle" / "_build" / "libh2inputs.so"
+_lib_path = LIBPATH
+
+
+def use_inputs_library() -> None:
+    """Bind the host-only input generator instead of the B200 library (bench.py's
+    reference arm builds its operands without mapping libh2mmp_b200.so).  Must be
+    called before the first lib(); the MMP entry points are then unavailable."""
+    global _lib_path
+    if _lib is not None and _lib_path != INPUTS_LIBPATH:
+        raise RuntimeError("the B200 library is already loaded")
+    _lib_path = INPUTS_LIBPATH
+
+
+def _sig(L, name: str, attr: str, value) -> None:
+    f = getattr(L, name, None)
+    if f is None:
+        if _lib_path == INPUTS_LIBPATH:
+            return  # not part of the input generator
+        raise ImportError(f"{name} missing from {_lib_path}")
+    setattr(f, attr, value)
+
+
 def lib() -> C.CDLL:
     """The B200 library; raises if it is missing (there is no fallback)."""
     global _lib
     if _lib is None:
-        if not LIBPATH.exists():
-            raise ImportError(f"{LIBPATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
-        L = C.CDLL(str(LIBPATH))
-        L.h2c_version.restype = C.c_int
-        L.h2c_last_error.restype = C.c_char_p
-        L.h2c_last_error.argtypes = [C.c_void_p]
-        L.h2c_create.restype = C.c_void_p
-        L.h2c_create.argtypes = [C.c_int]
-        L.h2c_destroy.argtypes = [C.c_void_p]
-        L.h2c_kernel_launches.restype = C.c_int64
-        L.h2c_kernel_launches.argtypes = [C.c_void_p]
-        L.h2c_stream.restype = C.c_void_p
-        L.h2c_stream.argtypes = [C.c_void_p]
-        L.h2c_set_profile.argtypes = [C.c_void_p, C.c_int]
-        L.h2c_profile_count.restype = C.c_int
-        L.h2c_profile_count.argtypes = [C.c_void_p]
-        L.h2c_profile_get.restype = C.c_int
-        L.h2c_profile_get.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int, P_i64, C.POINTER(C.c_double), P_i64]
-        L.h2c_build_structure.restype = C.c_void_p
-        L.h2c_build_structure.argtypes = [P_f64, C.c_int, C.c_int, C.c_double]
-        L.h2c_structure_tree.argtypes = [C.c_void_p, C.POINTER(h2c_tree)]
-        L.h2c_structure_blocks.argtypes = [C.c_void_p, C.POINTER(h2c_blocks)]
-        L.h2c_structure_free.argtypes = [C.c_void_p]
-        L.h2c_target_status.restype = C.c_int
-        L.h2c_target_status.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), C.c_int, C.c_int]
-        L.h2c_random_cloud.restype = C.c_int
-        L.h2c_random_cloud.argtypes = [C.c_int, C.c_uint64, P_f64]
-        L.h2c_build_chebyshev.restype = C.c_void_p
-        L.h2c_build_chebyshev.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_int, C.c_double,
-                                          C.c_double, C.c_int, C.c_double, C.c_int]
-        L.h2c_build_chebyshev_orders.restype = C.c_void_p
-        L.h2c_build_chebyshev_orders.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_int,
-                                                 C.c_double, C.c_double, C.POINTER(C.c_int32), C.c_double, C.c_int]
-        L.h2c_build_fd_laplacian.restype = C.c_void_p
-        L.h2c_build_fd_laplacian.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_double]
-        L.h2c_h2_desc.argtypes = [C.c_void_p, C.POINTER(h2c_matrix)]
-        L.h2c_h2_free.argtypes = [C.c_void_p]
-        for f in ("h2c_mmp",):
-            getattr(L, f).restype = C.c_int
-            getattr(L, f).argtypes = [C.c_void_p, C.POINTER(h2c_matrix), C.POINTER(h2c_matrix), C.c_double,
-                                      C.POINTER(C.c_void_p)]
-        L.h2c_formatted_mmp.restype = C.c_int
-        L.h2c_formatted_mmp.argtypes = [C.c_void_p, C.POINTER(h2c_matrix), C.POINTER(h2c_matrix),
-                                        C.POINTER(C.c_void_p)]
-        L.h2c_result_matrix.argtypes = [C.c_void_p, C.POINTER(h2c_matrix)]
-        L.h2c_result_report.argtypes = [C.c_void_p, C.POINTER(h2c_report)]
-        L.h2c_result_free.argtypes = [C.c_void_p]
-        L.h2c_upload.restype = C.c_int
-        L.h2c_upload.argtypes = [C.c_void_p, C.POINTER(h2c_matrix), C.POINTER(C.c_void_p)]
-        L.h2c_operand_free.argtypes = [C.c_void_p]
-        L.h2c_mmp_resident.restype = C.c_int
-        L.h2c_mmp_resident.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
-                                       C.POINTER(C.c_double), C.POINTER(C.c_void_p)]
-        L.h2c_count_report.restype = C.c_int
-        L.h2c_count_report.argtypes = [C.POINTER(h2c_matrix)] * 3 + [C.c_int, C.c_double, C.POINTER(C.c_void_p)]
-        L.h2c_mvp.restype = C.c_int
-        L.h2c_mvp.argtypes = [C.c_void_p, C.POINTER(h2c_matrix), P_f64, C.c_int, P_f64]
-        L.h2c_to_dense.restype = C.c_int
-        L.h2c_to_dense.argtypes = [C.c_void_p, C.POINTER(h2c_matrix), P_f64]
-        L.h2c_mvp_resident.restype = C.c_int
-        L.h2c_mvp_resident.argtypes = [C.c_void_p, C.c_void_p, P_f64, C.c_int, P_f64]
-        L.h2c_random_vector.restype = C.c_int
-        L.h2c_random_vector.argtypes = [C.c_int, C.c_uint64, C.c_int, P_f64]
-        L.h2c_truncate_gram.restype = C.c_int
-        L.h2c_truncate_gram.argtypes = [C.c_void_p, C.c_int, P_f64, C.c_int, C.c_double, P_f64, C.POINTER(C.c_int),
-                                        C.POINTER(C.c_int)]
-        L.h2c_plan_stats.restype = C.c_int
-        L.h2c_plan_stats.argtypes = [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_i64, C.c_int]
-        L.h2c_host_alloc.restype = C.c_void_p
-        L.h2c_host_alloc.argtypes = [C.c_size_t]
-        L.h2c_host_free.argtypes = [C.c_void_p]
+        path = _lib_path
+        if not path.exists():
+            raise ImportError(f"{path} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(str(path))
+        _sig(L, "h2c_version", "restype", C.c_int)
+        _sig(L, "h2c_last_error", "restype", C.c_char_p)
+        _sig(L, "h2c_last_error", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_create", "restype", C.c_void_p)
+        _sig(L, "h2c_create", "argtypes", [C.c_int])
+        _sig(L, "h2c_destroy", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_kernel_launches", "restype", C.c_int64)
+        _sig(L, "h2c_kernel_launches", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_stream", "restype", C.c_void_p)
+        _sig(L, "h2c_stream", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_set_profile", "argtypes", [C.c_void_p, C.c_int])
+        _sig(L, "h2c_profile_count", "restype", C.c_int)
+        _sig(L, "h2c_profile_count", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_profile_get", "restype", C.c_int)
+        _sig(L, "h2c_profile_bytes", "restype", C.c_int64)
+        _sig(L, "h2c_profile_bytes", "argtypes", [C.c_void_p, C.c_int])
+        _sig(L, "h2c_profile_get", "argtypes", [C.c_void_p, C.c_int, C.c_char_p, C.c_int, P_i64, C.POINTER(C.c_double), P_i64])
+        _sig(L, "h2c_build_structure", "restype", C.c_void_p)
+        _sig(L, "h2c_build_structure", "argtypes", [P_f64, C.c_int, C.c_int, C.c_double])
+        _sig(L, "h2c_structure_tree", "argtypes", [C.c_void_p, C.POINTER(h2c_tree)])
+        _sig(L, "h2c_structure_blocks", "argtypes", [C.c_void_p, C.POINTER(h2c_blocks)])
+        _sig(L, "h2c_structure_free", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_target_status", "restype", C.c_int)
+        _sig(L, "h2c_target_status", "argtypes", [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), C.c_int, C.c_int])
+        _sig(L, "h2c_random_cloud", "restype", C.c_int)
+        _sig(L, "h2c_random_cloud", "argtypes", [C.c_int, C.c_uint64, P_f64])
+        _sig(L, "h2c_build_chebyshev", "restype", C.c_void_p)
+        _sig(L, "h2c_build_chebyshev", "argtypes", [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_int, C.c_double,
+                                          C.c_double, C.c_int, C.c_double, C.c_int])
+        _sig(L, "h2c_build_chebyshev_orders", "restype", C.c_void_p)
+        _sig(L, "h2c_build_chebyshev_orders", "argtypes", [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_int,
+                                                 C.c_double, C.c_double, C.POINTER(C.c_int32), C.c_double, C.c_int])
+        _sig(L, "h2c_build_fd_laplacian", "restype", C.c_void_p)
+        _sig(L, "h2c_build_fd_laplacian", "argtypes", [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_f64, C.c_double])
+        _sig(L, "h2c_h2_desc", "argtypes", [C.c_void_p, C.POINTER(h2c_matrix)])
+        _sig(L, "h2c_h2_free", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_mmp", "restype", C.c_int)
+        _sig(L, "h2c_mmp", "argtypes", [C.c_void_p, C.POINTER(h2c_matrix), C.POINTER(h2c_matrix), C.c_double,
+                                       C.POINTER(C.c_void_p)])
+        _sig(L, "h2c_formatted_mmp", "restype", C.c_int)
+        _sig(L, "h2c_formatted_mmp", "argtypes", [C.c_void_p, C.POINTER(h2c_matrix), C.POINTER(h2c_matrix),
+                                        C.POINTER(C.c_void_p)])
+        _sig(L, "h2c_result_matrix", "argtypes", [C.c_void_p, C.POINTER(h2c_matrix)])
+        _sig(L, "h2c_result_report", "argtypes", [C.c_void_p, C.POINTER(h2c_report)])
+        _sig(L, "h2c_result_free", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_upload", "restype", C.c_int)
+        _sig(L, "h2c_upload", "argtypes", [C.c_void_p, C.POINTER(h2c_matrix), C.POINTER(C.c_void_p)])
+        _sig(L, "h2c_operand_free", "argtypes", [C.c_void_p])
+        _sig(L, "h2c_mmp_resident", "restype", C.c_int)
+        _sig(L, "h2c_mmp_resident", "argtypes", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_void_p)])
+        _sig(L, "h2c_count_report", "restype", C.c_int)
+        _sig(L, "h2c_count_report", "argtypes", [C.POINTER(h2c_matrix)] * 3 + [C.c_int, C.c_double, C.POINTER(C.c_void_p)])
+        _sig(L, "h2c_mvp", "restype", C.c_int)
+        _sig(L, "h2c_mvp", "argtypes", [C.c_void_p, C.POINTER(h2c_matrix), P_f64, C.c_int, P_f64])
+        _sig(L, "h2c_to_dense", "restype", C.c_int)
+        _sig(L, "h2c_to_dense", "argtypes", [C.c_void_p, C.POINTER(h2c_matrix), P_f64])
+        _sig(L, "h2c_mvp_resident", "restype", C.c_int)
+        _sig(L, "h2c_mvp_resident", "argtypes", [C.c_void_p, C.c_void_p, P_f64, C.c_int, P_f64])
+        _sig(L, "h2c_random_vector", "restype", C.c_int)
+        _sig(L, "h2c_random_vector", "argtypes", [C.c_int, C.c_uint64, C.c_int, P_f64])
+        _sig(L, "h2c_truncate_gram", "restype", C.c_int)
+        _sig(L, "h2c_truncate_gram", "argtypes", [C.c_void_p, C.c_int, P_f64, C.c_int, C.c_double, P_f64, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int)])
+        _sig(L, "h2c_plan_stats", "restype", C.c_int)
+        _sig(L, "h2c_plan_stats", "argtypes", [C.POINTER(h2c_tree), C.POINTER(h2c_blocks), P_i64, C.c_int])
+        _sig(L, "h2c_host_alloc", "restype", C.c_void_p)
+        _sig(L, "h2c_host_alloc", "argtypes", [C.c_size_t])
+        _sig(L, "h2c_host_free", "argtypes", [C.c_void_p])
         _lib = L
     return _lib
 
