@@ -476,7 +476,7 @@ def run_b200(args) -> None:
                        "macs_per_step": int(rep.flops), "macs_exec_per_step": int(rep.flops_exec),
                        "flops_per_mac": fpm, "eps_rel": eps_rel, "build_seconds": round(W["build_seconds"], 1),
                        "max_rank": rep.max_rank(),
-                       "max_rank_per_level": [int(max(a, b)) for a, b in zip(rep.max_row_rank, rep.max_col_rank)],
+                       "max_rank_per_level": [int(max(v.max_row_rank, v.max_col_rank)) for v in rep.levels],
                        "l2": "inputs (%.1f GB) >> 126 MB L2" % ((A.values.nbytes + (0 if B is A else B.values.nbytes)) / 1e9),
                        "parallelism": f"replicas{world}"},
             "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),

@@ -41,6 +41,7 @@
 
 #include "counters.hpp"
 #include "engine.hpp"
+#include "heev.cuh"
 #include "kernels.cuh"
 
 namespace h2b {
@@ -48,8 +49,6 @@ namespace h2b {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
-constexpr int kJacobiMaxN = 64;
-constexpr int kJacobiPackedMaxN = 224;
 
 struct ConfigErr : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
@@ -784,13 +783,6 @@ struct EngineRun {
   }
   const bool debug_sync = std::getenv("H2B_DEBUG_SYNC") != nullptr;
   const bool debug_check = std::getenv("H2B_DEBUG_CHECK") != nullptr;
-  // solver selection knobs (A/B): library solver also for n <= 64; packed Jacobi for 64 < n <= 224
-  // batched library solver for every Gram size by default (A/B: 1.75x faster than the CTA-resident
-  // Jacobi on cfg5s's 64 x 64 complex leaf Grams, 2% on cfg2); H2B_EIG_JACOBI=1 selects the Jacobi
-  // kernel for n <= 64
-  const bool force_library = std::getenv("H2B_EIG_JACOBI") == nullptr;
-  const bool jacobi_v_global = std::getenv("H2B_JACOBI_V") != nullptr;
-  const bool use_packed = std::getenv("H2B_EIG_PACKED") != nullptr;
 
   // C
   std::vector<int> KCr, KCc;
@@ -807,7 +799,7 @@ struct EngineRun {
   std::vector<DBuf> Bp, PA, PB, LA, RB;
   // auxiliary stream for the C-independent leaf full targets
   cudaStream_t s_aux = nullptr, prev_aux = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_full = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_full = nullptr, ev_side = nullptr;
   bool joined = true;  // nothing queued on the auxiliary stream yet
   std::vector<DBuf> hold;
   // A main-stream buffer the main stream no longer needs but deferred work on
@@ -847,6 +839,7 @@ struct EngineRun {
     t_aux_stream = prev_aux;
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_full) cudaEventDestroy(ev_full);
+    if (ev_side) cudaEventDestroy(ev_side);
   }
 
   EngineRun(Context& c, const Plan& p, const DevPlan& dp, const DevOperand& a, const DevOperand& b,
@@ -876,53 +869,14 @@ struct EngineRun {
     t_aux_stream = s_aux;
     CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_full, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   }
 
   size_t sz(size_t count, int r, int c) const { return count * size_t(r) * c * W; }
 
   // ---- launchers -----------------------------------------------------------
-  const bool seg_v1 = std::getenv("H2B_SEG_V1") != nullptr;
-  // pipeline shape of seg_gemm v2 (k-chunk x stages); H2B_SEG_CFG=8x4 (default), 16x3, 32x2, 16x4
-  const int seg_cfg = [] {
-    const char* e = std::getenv("H2B_SEG_CFG");
-    if (!e) return 3;  // 8x4: measured best on cfg2 (profiles/r01/seg_cfg_ab.txt)
-    const std::string v(e);
-    return v == "32x2" ? 1 : v == "16x4" ? 2 : v == "16x3" ? 0 : 3;
-  }();
-  template <int TM, int TN, bool CX, int KC, int ST, int WM = 2, int WN = 2>
-  void launch_v2_cfg(const SegParams& sp, dim3 grid) {
-    constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST, WM, WN>::SMEM;
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(seg_gemm2_kernel<TM, TN, CX, KC, ST, WM, WN>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      attr = true;
-    }
-    seg_gemm2_kernel<TM, TN, CX, KC, ST, WM, WN><<<grid, 32 * WM * WN, sm, s>>>(sp);
-  }
-  template <int TM, int TN, bool CX>
-  void launch_v2(const SegParams& sp, dim3 grid) {
-    switch (seg_cfg) {
-      case 1: launch_v2_cfg<TM, TN, CX, 32, 2>(sp, grid); break;
-      case 2: launch_v2_cfg<TM, TN, CX, 16, 4>(sp, grid); break;
-      case 3: launch_v2_cfg<TM, TN, CX, 8, 4>(sp, grid); break;
-      default: launch_v2_cfg<TM, TN, CX, 16, 3>(sp, grid); break;
-    }
-  }
-  // wide CTA tiles (8 or 16 warps of 32x32) for outputs larger than 64 in a dimension
-  // measured slower than 4-warp tiles on cfg2 (profiles/r01/seg_cfg_ab.txt): opt-in only
-  const bool seg_wide = std::getenv("H2B_SEG_WIDE") != nullptr;
-  template <bool CX>
-  void launch_wide(const SegParams& sp, int tm, int tn, dim3 grid) {
-    if (tm == 128 && tn == 128) launch_v2_cfg<128, 128, CX, 8, 4, 4, 4>(sp, grid);
-    else if (tm == 128) launch_v2_cfg<128, 64, CX, 8, 4, 4, 2>(sp, grid);
-    else launch_v2_cfg<64, 128, CX, 8, 4, 2, 4>(sp, grid);
-  }
-
-  // v3 (default): v2's pipeline without the per-chunk integer work; needs every
-  // inner dimension to be a multiple of the k-chunk (8), which the padded layout
-  // guarantees.  H2B_SEG_V2=1 selects v2 for A/B runs.
-  const bool seg_v2 = std::getenv("H2B_SEG_V2") != nullptr;
+  // seg_gemm3 (kernels.cuh): cp.async pipeline of 8-deep k-chunks x 4 stages; every
+  // inner dimension is a multiple of the k-chunk (the padded layout guarantees it)
   template <int TM, int TN, bool CX, int KC, int ST, int WM = 2, int WN = 2>
   void launch_v3_cfg(const SegParams& sp, dim3 grid) {
     constexpr int sm = Seg2Cfg<TM, TN, CX, KC, ST, WM, WN>::SMEM;
@@ -949,43 +903,10 @@ struct EngineRun {
   // complex products with 3 real DMMAs per complex MAC (Gauss; cfg5s 0.416 -> 0.377 s,
   // profiles/r01/ab_3m_cfg5s.txt); H2B_CPLX4M=1 restores the 4-product form
   const bool cplx3m = std::getenv("H2B_CPLX4M") == nullptr;
-  // 8-wide tile classes (v3 only): outputs with a padded dimension of 8, e.g.
-  // the rank-1 (padded 8) FD operand of cfg4, would waste half a 16-wide tile
-  // v5 (v3 with a grid-stride loop over outputs) for small tiles: H2B_SEG_V5=1 enables
-  const bool seg_v5 = std::getenv("H2B_SEG_V5") != nullptr;
-  template <int TM, int TN, bool CX, int WM = 2, int WN = 2>
-  void launch_v5_cfg(const SegParams& sp, int tiles) {
-    constexpr int sm = Seg2Cfg<TM, TN, CX, 8, 4, WM, WN>::SMEM;
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(seg_gemm5_kernel<TM, TN, CX, 8, 4, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              sm));
-      attr = true;
-    }
-    const int gx = std::max(1, std::min(sp.n_out, (148 * 16) / std::max(1, tiles)));
-    seg_gemm5_kernel<TM, TN, CX, 8, 4, WM, WN><<<dim3(gx, tiles), 32 * WM * WN, sm, s>>>(sp);
-  }
-  // H2B_V5_AUTO=1: v5 also for launches of many outputs with little work each (<= 4 k-chunks per
-  // output, e.g. cfg3's 619k level-11 targets of 40 x 40 from 2 entries of K = 8).  Measured
-  // neutral to 1 % slower (profiles/r01/ab_v5auto.txt), so off by default.
-  const bool no_v5_auto = std::getenv("H2B_V5_AUTO") == nullptr;
-  double last_cpo = 1e30;  // k-chunks per output of the current seg() launch
-  int last_nout = 0;
-  bool use_v5(int TM, int TN) const {
-    if (seg_v5) return TM <= 32 && TN <= 32;
-    return !no_v5_auto && last_cpo <= 4.0 && last_nout >= 4096;
-  }
+  // 8-wide tile classes: outputs with a padded dimension of 8, e.g. the rank-1 (padded 8)
+  // FD operand of cfg4, would waste half a 16-wide tile
   template <int TM, int TN, int WM, int WN>
   void launch_seg8(const SegParams& sp, int tiles) {
-    {
-      if (use_v5(TM, TN)) {
-        if (cplx) launch_v5_cfg<TM, TN, true, WM, WN>(sp, tiles);
-        else launch_v5_cfg<TM, TN, false, WM, WN>(sp, tiles);
-        CK(cudaGetLastError());
-        launches++;
-        return;
-      }
-    }
     dim3 grid(sp.n_out, tiles);
     if (cplx) launch_v3_cfg<TM, TN, true, 8, 4, WM, WN>(sp, grid);
     else launch_v3_cfg<TM, TN, false, 8, 4, WM, WN>(sp, grid);
@@ -994,40 +915,11 @@ struct EngineRun {
   }
   template <int TM, int TN>
   void launch_seg(const SegParams& sp, int tiles) {
+    for (int g = 0; g < sp.ngroups; ++g)
+      if (sp.g[g].K % 8 != 0) throw std::logic_error("seg: inner dimension not a multiple of 8");
     dim3 grid(sp.n_out, tiles);
-    bool v3 = !seg_v1 && !seg_v2;
-    for (int g = 0; g < sp.ngroups; ++g) v3 = v3 && sp.g[g].K % 8 == 0;
-    if (v3) {
-      bool v5 = false;
-      {
-        if (use_v5(TM, TN)) {
-          v5 = true;
-          if (cplx) launch_v5_cfg<TM, TN, true>(sp, tiles);
-          else launch_v5_cfg<TM, TN, false>(sp, tiles);
-        }
-      }
-      if (v5) {
-      } else if (cplx) {
-        launch_v3_cfg<TM, TN, true, 8, 4>(sp, grid);
-      } else {
-        launch_v3_cfg<TM, TN, false, 8, 4>(sp, grid);
-      }
-      CK(cudaGetLastError());
-      launches++;
-      return;
-    }
-    if (!seg_v1) {
-      if (cplx) launch_v2<TM, TN, true>(sp, grid);
-      else launch_v2<TM, TN, false>(sp, grid);
-      CK(cudaGetLastError());
-      launches++;
-      return;
-    }
-    if (cplx) {
-      seg_gemm_kernel<TM, TN, true><<<grid, 128, SegCfg<TM, TN, true>::SMEM, s>>>(sp);
-    } else {
-      seg_gemm_kernel<TM, TN, false><<<grid, 128, SegCfg<TM, TN, false>::SMEM, s>>>(sp);
-    }
+    if (cplx) launch_v3_cfg<TM, TN, true, 8, 4>(sp, grid);
+    else launch_v3_cfg<TM, TN, false, 8, 4>(sp, grid);
     CK(cudaGetLastError());
     launches++;
   }
@@ -1089,12 +981,6 @@ struct EngineRun {
     int64_t macs = 0;
     for (const Grp& g : gs) macs += (g.csr ? g.csr->entries : n_out) * int64_t(M) * N * g.K;
     if (sym) macs = macs / 2 + macs / (2 * ((M + 63) / 64));
-    {
-      double chunks = 0;
-      for (const Grp& g : gs) chunks += double(g.csr ? g.csr->entries : n_out) * ((g.K + 7) / 8);
-      last_cpo = chunks / std::max(1, n_out);
-      last_nout = n_out;
-    }
     if (profiling && prof_shapes) {
       shape_tag = " [" + std::to_string(M) + "x" + std::to_string(N) + " K";
       int64_t ent = 0;
@@ -1110,17 +996,6 @@ struct EngineRun {
       bytes += ent * (int64_t(M) * g.K + int64_t(g.K) * N) * 8 * W;
     }
     pre("seg_gemm", macs, bytes);
-    if (seg_wide && !seg_v1 && !sym && (M > 64 || N > 64)) {
-      const int tm = M > 64 ? 128 : 64, tn = N > 64 ? 128 : 64;
-      const int tiles = ((M + tm - 1) / tm) * ((N + tn - 1) / tn);
-      dim3 grid(sp.n_out, tiles);
-      if (cplx) launch_wide<true>(sp, tm, tn, grid);
-      else launch_wide<false>(sp, tm, tn, grid);
-      CK(cudaGetLastError());
-      launches++;
-      post();
-      return;
-    }
     if (sym && (M != N || acc)) throw std::logic_error("seg: symmetric launch needs a square, fresh output");
     // Outputs wider than one 64 tile whose last tile row / column would be at
     // most half full (e.g. a padded rank of 208 = 3*64 + 16): the full 64-tiles
@@ -1132,15 +1007,15 @@ struct EngineRun {
     // disables, H2B_STRIPS_SMALL_MAX sets the largest remainder); H2B_STRIPS_24=1 also 17..24 as
     // 16 + remainder
     auto small_cut = [&](int X) {
-      if (!strips_small || sym || seg_v1) return 0;
+      if (!strips_small || sym) return 0;
       if (X > 32 && X - 32 <= strips_small_max) return 32;
       if (strips_24 && X > 16 && X < 32 && X - 16 <= 8) return 16;
       return 0;
     };
     const int scM = small_cut(M), scN = small_cut(N);
     const bool smM = scM > 0, smN = scN > 0;
-    const bool splitM = smM || (!sym && !seg_v1 && !no_strips && M > 64 && rm > 0 && rm <= 32);
-    const bool splitN = smN || (!sym && !seg_v1 && !no_strips && N > 64 && rn > 0 && rn <= 32);
+    const bool splitM = smM || (!sym && !no_strips && M > 64 && rm > 0 && rm <= 32);
+    const bool splitN = smN || (!sym && !no_strips && N > 64 && rn > 0 && rn <= 32);
     if (!splitM && !splitN) {
       launch_tiles(sp);
     } else {
@@ -1173,20 +1048,6 @@ struct EngineRun {
     const char* e = std::getenv("H2B_STRIPS_SMALL_MAX");
     return e ? std::atoi(e) : 16;
   }();
-  // v4 (warps split the chunks of small output tiles): H2B_SEG_V4=1 enables
-  const bool seg_v4 = std::getenv("H2B_SEG_V4") != nullptr;
-  template <int TM, int TN>
-  void launch_seg4(const SegParams& sp, int tiles) {
-    dim3 grid(sp.n_out, tiles);
-    auto go = [&](auto kern, int sm) {
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      kern<<<grid, 128, sm, s>>>(sp);
-    };
-    if (cplx) go(seg_gemm4_kernel<TM, TN, true>, Seg4Cfg<TM, TN, true>::SMEM);
-    else go(seg_gemm4_kernel<TM, TN, false>, Seg4Cfg<TM, TN, false>::SMEM);
-    CK(cudaGetLastError());
-    launches++;
-  }
   // Hermitian (Gram) outputs cannot be cut into strips; their square tile is chosen by
   // lower-triangle tile area / relative tile efficiency (64: 1, 32: 0.75): e.g. an 80 x 80 Gram
   // takes 6 tiles of 32 (6,144 padded elements) instead of 3 of 64 (12,288, 26 % useful).
@@ -1202,29 +1063,11 @@ struct EngineRun {
   }
   void launch_tiles(const SegParams& sp) {
     const int M = sp.M, N = sp.N;
-    const bool v3 = !seg_v1 && !seg_v2;
-    int TM = (M <= 8 && v3) ? 8 : M <= 16 ? 16 : (M <= 32 ? 32 : 64);
-    int TN = (N <= 8 && v3) ? 8 : N <= 16 ? 16 : (N <= 32 ? 32 : 64);
-    if (sp.sym && v3 && !sym_t64 && M > 32) TM = TN = sym_tile(M);
+    int TM = M <= 8 ? 8 : M <= 16 ? 16 : (M <= 32 ? 32 : 64);
+    int TN = N <= 8 ? 8 : N <= 16 ? 16 : (N <= 32 ? 32 : 64);
+    if (sp.sym && !sym_t64 && M > 32) TM = TN = sym_tile(M);
     const int tm_ = (M + TM - 1) / TM;
     const int tiles = sp.sym ? tm_ * (tm_ + 1) / 2 : tm_ * ((N + TN - 1) / TN);
-    if (seg_v4 && v3 && TM <= 32 && TN <= 32) {
-      bool k8 = true;
-      for (int g = 0; g < sp.ngroups; ++g) k8 = k8 && sp.g[g].K % 8 == 0;
-      if (k8) {
-        switch (TM * 100 + TN) {
-          case 808: launch_seg4<8, 8>(sp, tiles); return;
-          case 816: launch_seg4<8, 16>(sp, tiles); return;
-          case 832: launch_seg4<8, 32>(sp, tiles); return;
-          case 1608: launch_seg4<16, 8>(sp, tiles); return;
-          case 1616: launch_seg4<16, 16>(sp, tiles); return;
-          case 1632: launch_seg4<16, 32>(sp, tiles); return;
-          case 3208: launch_seg4<32, 8>(sp, tiles); return;
-          case 3216: launch_seg4<32, 16>(sp, tiles); return;
-          default: launch_seg4<32, 32>(sp, tiles); return;
-        }
-      }
-    }
     if (TM == 8 || TN == 8) {
       if (TM == 8 && TN == 8) launch_seg8<8, 8, 1, 1>(sp, tiles);
       else if (TM == 8 && TN == 16) launch_seg8<8, 16, 1, 2>(sp, tiles);
@@ -1275,7 +1118,10 @@ struct EngineRun {
     DBuf vec, val;
     DVec<int32_t> rank;
     DVec<uint8_t> degen;
-    DBuf G;  // deferred library eigensolve input
+    DBuf G;  // eigensolve input (deferred library solve / kept until the solve is joined)
+    DBuf hV, hZ, hSlab;  // heev workspaces
+    DVec<int> fail;      // heev: a QL iteration did not converge
+    bool side = false;   // solved on side stream 1 (joined in finish_async)
     int n = 0, count = 0;
   };
   Trunc truncate(DBuf& g1, DBuf& g2, DBuf& g3, int count, int n, const DVec<uint8_t>& opdeg, bool defer = false) {
@@ -1313,110 +1159,107 @@ struct EngineRun {
     t.vec.alloc(sz(count, n, n), s);
     t.val.alloc(size_t(count) * n, s);
     t.rank.alloc(count, s);
-    JacobiParams jp{};
-    jp.G = G;
-    jp.vec_out = t.vec;
-    jp.val_out = t.val;
-    jp.rank_out = t.rank.p;
-    jp.degen_io = t.degen.p;
-    jp.n = n;
-    jp.eps = adaptive ? eps : 0.5;
-    jp.max_sweeps = 40;
-    const size_t smem = size_t(2) * n * (n + 1) * W * sizeof(double);
-    if (n <= kJacobiMaxN && !force_library) {
-      pre("jacobi_eig", 0);
-      // H2B_JACOBI_V=global: eigenvectors in a global (L2-resident) scratch, halving the shared
-      // memory per CTA (more CTAs per SM)
-      DBuf vscr;
-      if (jacobi_v_global) {
-        vscr.alloc(size_t(count) * n * (n + 1) * W, s);
-        jp.scratch = vscr.p;
-        const size_t sm1 = smem / 2;
-        if (cplx) {
-          CK(cudaFuncSetAttribute(jacobi_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
-          jacobi_kernel<true, 2><<<count, 256, sm1, s>>>(jp);
-        } else {
-          CK(cudaFuncSetAttribute(jacobi_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
-          jacobi_kernel<false, 2><<<count, 256, sm1, s>>>(jp);
-        }
-      } else if (cplx) {
-        CK(cudaFuncSetAttribute(jacobi_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        jacobi_kernel<true, 1><<<count, 256, smem, s>>>(jp);
+    if (use_library) {  // A/B only: cuSOLVER's batched solver + eig_finalize
+      if (defer) {
+        t.G = std::move(G);  // solved later by solve_async (concurrently with the column side)
+        t.n = n;
+        t.count = count;
       } else {
-        CK(cudaFuncSetAttribute(jacobi_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        jacobi_kernel<false, 1><<<count, 256, smem, s>>>(jp);
+        library_eig(G, count, n, t);
       }
-      CK(cudaGetLastError());
-      post();
-      launches++;
-    } else if (!cplx && n <= kJacobiPackedMaxN && use_packed) {
-      packed_jacobi(G, count, n, t);
-    } else if (defer) {
-      t.G = std::move(G);  // solved later by solve_deferred (possibly concurrently)
-      t.n = n;
-      t.count = count;
-    } else {
-      library_eig(G, count, n, t);
+      return t;
     }
+    // the engine's own solver (heev.cuh); a deferred (row-side) solve runs on side stream 1,
+    // concurrently with the column side, and is joined in finish_async
+    cudaStream_t st = s;
+    if (defer) {
+      st = static_cast<cudaStream_t>(ctx.side_stream(1));
+      t.side = true;
+    }
+    heev(G, count, n, t, st);
+    t.G = std::move(G);  // input kept alive until the (possibly deferred) solve is joined
+    t.n = n;
+    t.count = count;
     return t;
   }
 
-  // 64 < n <= 224 (real): packed shared-memory Jacobi + parallel replay of the rotations
-  void packed_jacobi(const DBuf& G, int count, int n, Trunc& t) {
-    constexpr int kSweeps = 30;
-    const int h = n / 2;
-    const bool vsm = n <= 128;  // packed A + V both fit in shared memory
-    DBuf log;
-    if (!vsm) log.alloc(size_t(count) * kSweeps * (n - 1) * h * 3, s);
-    DVec<int> steps, order;
-    steps.alloc(count, s);
-    order.alloc(size_t(count) * n, s);
-    JacobiPackedParams jp{};
-    jp.G = G;
-    jp.log = log.p;
-    jp.steps_out = steps.p;
-    jp.order_out = order.p;
-    jp.val_out = t.val;
-    jp.vec_out = t.vec;
-    jp.rank_out = t.rank.p;
-    jp.degen_io = t.degen.p;
-    jp.n = n;
-    jp.eps = jp_eps();
-    jp.max_sweeps = kSweeps;
-    const int smem = (n * (n + 1) / 2 + (vsm ? n * (n + 1) : 0)) * int(sizeof(double));
-    pre("jacobi_packed", 0);
-    if (vsm) {
-      CK(cudaFuncSetAttribute(jacobi_packed_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      jacobi_packed_kernel<true><<<count, 512, smem, s>>>(jp);
-    } else {
-      CK(cudaFuncSetAttribute(jacobi_packed_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      jacobi_packed_kernel<false><<<count, 512, smem, s>>>(jp);
-    }
-    CK(cudaGetLastError());
-    post();
-    launches++;
-    if (debug_check) {
-      std::vector<int> st(count);
-      CK(cudaMemcpyAsync(st.data(), steps.p, count * sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      long tot = 0;
-      int mx = 0;
-      for (int v : st) {
-        tot += v;
-        mx = std::max(mx, v);
+  // H2B_EIG_LIBRARY=1: cuSOLVER XsyevBatched instead of heev_kernel (A/B runs)
+  const bool use_library = std::getenv("H2B_EIG_LIBRARY") != nullptr;
+
+  // Batched Hermitian eigensolver + truncation rule (heev.cuh).  Two placements, chosen per
+  // launch from tools/heev_bench.cu measurements on the B200 (profiles/r02/heev_bench.txt):
+  //  * few large Grams (one wave of clusters, n > 128): one cluster of CS CTAs per Gram with the
+  //    Gram in the cluster's shared memory (CS the smallest power of two that fits, <= 16);
+  //  * otherwise (the batched levels): one CTA per Gram with the Gram in a global (L2-resident)
+  //    slab and ~20-50 KB of shared memory, so 4-16 Grams share an SM and hide each other's
+  //    latency-bound phases.
+  // Workspaces come from the main-stream arena before the fork.
+  void heev(const DBuf& G, int count, int n, Trunc& t, cudaStream_t st) {
+    constexpr int kMaxSmem = 232448, kSMs = 148;
+    int CS = 0;
+    bool smem = true;
+    for (int cs : {1, 2, 4, 8, 16}) {
+      if (HeevLayout(n, cs, cplx, true).total * 8 <= kMaxSmem) {
+        CS = cs;
+        break;
       }
-      std::fprintf(stderr, "[jacobi_packed] n=%d count=%d sweeps mean %.1f max %.1f\n", n, count,
-                   double(tot) / count / (n - 1), double(mx) / (n - 1));
     }
-    if (vsm) return;
-    const int rows = 32;
-    CK(cudaFuncSetAttribute(jacobi_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(rows * n * sizeof(double))));
-    pre("jacobi_replay", 0);
-    jacobi_replay_kernel<<<dim3((n + rows - 1) / rows, count), 256, rows * n * sizeof(double), s>>>(
-        log, steps.p, order.p, n, kSweeps, rows, t.vec);
+    if (!(CS && n > 128 && (long long)count * CS <= kSMs)) {
+      CS = 1;
+      smem = false;
+    }
+    const HeevLayout L(n, CS, cplx, smem);
+    const int nt = n <= 64 ? 128 : (n <= 192 ? 256 : 512);
+    const size_t bytes = size_t(L.total) * 8;
+    t.hV.alloc(sz(count, n, n), s);
+    t.hZ.alloc(size_t(count) * n * n, s);
+    if (!smem) t.hSlab.alloc(size_t(count) * CS * L.ncl * L.ld * W, s);
+    t.fail.alloc(1, s);
+    CK(cudaMemsetAsync(t.fail.p, 0, sizeof(int), s));
+    if (st != s) {
+      CK(cudaEventRecord(ev_fork, s));
+      CK(cudaStreamWaitEvent(st, ev_fork, 0));
+    }
+    HeevParams hp{};
+    hp.G = G.p;
+    hp.V = t.hV.p;
+    hp.Zs = t.hZ.p;
+    hp.slab = t.hSlab.p;
+    hp.vec_out = t.vec.p;
+    hp.val_out = t.val.p;
+    hp.rank_out = t.rank.p;
+    hp.degen_io = t.degen.p;
+    hp.fail = t.fail.p;
+    hp.n = n;
+    hp.eps = jp_eps();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(count) * CS);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    auto go = [&](auto kern) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      CK(cudaLaunchKernelEx(&cfg, kern, hp));
+    };
+    const bool main = st == s;
+    if (main) pre("heev", 0);
+    if (cplx) {
+      if (smem) go(heev_kernel<true, true>);
+      else go(heev_kernel<true, false>);
+    } else {
+      if (smem) go(heev_kernel<false, true>);
+      else go(heev_kernel<false, false>);
+    }
     CK(cudaGetLastError());
-    post();
+    if (main) post();
     launches++;
   }
 
@@ -1450,7 +1293,7 @@ struct EngineRun {
   // the row and column eigensolves of a level overlap (cuSOLVER's batched
   // solver is launch-latency bound).
   std::thread solve_async(Trunc& t, EigWork& wk, std::exception_ptr& err) {
-    if (!t.G.p) return std::thread();
+    if (!t.G.p || t.side || !use_library) return std::thread();
     cudaStream_t st = static_cast<cudaStream_t>(ctx.side_stream(1));
     cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.side_solver(1));
     prepare_eig(wk, t.count, t.n, h);
@@ -1469,11 +1312,16 @@ struct EngineRun {
   void finish_async(std::thread& th, std::exception_ptr& err, Trunc& t, EigWork& wk) {
     if (th.joinable()) th.join();  // the solve ended with a synchronize of its stream
     if (err) std::rethrow_exception(err);
+    if (t.side) {  // heev on side stream 1: the main stream waits for it
+      CK(cudaEventRecord(ev_side, static_cast<cudaStream_t>(ctx.side_stream(1))));
+      CK(cudaStreamWaitEvent(s, ev_side, 0));
+      t.side = false;
+    }
     t.G.release();
     wk = EigWork{};
   }
 
-  // Gram dimensions beyond the shared-memory Jacobi (upper levels, where C's
+  // A/B only (H2B_EIG_LIBRARY=1): cuSOLVER batched solver (upper levels, where C's
   // ranks grow): batched Hermitian eigensolver from cuSOLVER, then the same
   // truncation rule on the device.
   void library_eig(const DBuf& G, int count, int n, Trunc& t) {
@@ -1556,11 +1404,15 @@ struct EngineRun {
                  count, rmin, rmax, worst, margin);
   }
 
-  // ranks to host, padded width
-  int fetch_ranks(const DVec<int32_t>& r, int count, std::vector<int64_t>& out) {
+  // ranks to host, padded width (and the solver's convergence flag)
+  int fetch_ranks(const Trunc& t, int count, std::vector<int64_t>& out) {
+    const DVec<int32_t>& r = t.rank;
     std::vector<int32_t> h(count);
+    int failed = 0;
     CK(cudaMemcpyAsync(h.data(), r.p, count * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (t.fail.p) CK(cudaMemcpyAsync(&failed, t.fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (failed) throw std::logic_error("svd_truncate_gram: eigendecomposition failed (QL iteration did not converge)");
     out.assign(h.begin(), h.end());
     int64_t mx = 0;
     for (auto v : out) mx = std::max(mx, v);
@@ -1890,8 +1742,8 @@ struct EngineRun {
                 nullptr, nullptr}});
       Trunc tc = truncate(c1, c2, c3, n, NL, B.dgc_d[l]);
       mark("leaf.bases");
-      KCr[l] = fetch_ranks(tr.rank, n, rcr[l]);
-      KCc[l] = fetch_ranks(tc.rank, n, rcc[l]);
+      KCr[l] = fetch_ranks(tr, n, rcr[l]);
+      KCc[l] = fetch_ranks(tc, n, rcc[l]);
       pack(tr, n, NL, Vr, NL, KCr[l]);
       pack(tc, n, NL, Vc, NL, KCc[l]);
       dgr[l] = std::move(tr.degen);
@@ -2082,8 +1934,8 @@ struct EngineRun {
         throw;
       }
       finish_async(row_th, row_err, tr, row_wk);
-      KCr[l] = fetch_ranks(tr.rank, n, rcr[l]);
-      KCc[l] = fetch_ranks(tc.rank, n, rcc[l]);
+      KCr[l] = fetch_ranks(tr, n, rcr[l]);
+      KCc[l] = fetch_ranks(tc, n, rcc[l]);
       pack(tr, n, 2 * Kn, Tr[l], 2 * Kn, KCr[l]);
       pack(tc, n, 2 * Kq, Tc[l], 2 * Kq, KCc[l]);
       dgr[l] = std::move(tr.degen);

@@ -25,8 +25,8 @@ else:
     s = P.build_block_tree(t, t, 1.0)
     A = B = P.build_chebyshev(t, s, pts, order)
     specs = sys.argv[5:]
-KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_SEG_V2", "H2B_EIG_JACOBI", "H2B_EIG_LIBRARY", "H2B_SEG_CFG", "H2B_NO_STRIPS",
-         "H2B_EIG_PACKED", "H2B_JACOBI_V", "H2B_CPLX4M", "H2B_SEG_V4", "H2B_SEG_V5", "H2B_SYM_T64", "H2B_V5_AUTO", "H2B_NO_STRIPS_SMALL", "H2B_STRIPS_24", "H2B_STRIPS_SMALL_MAX")
+KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_EIG_LIBRARY", "H2B_NO_STRIPS", "H2B_CPLX4M", "H2B_SYM_T64",
+         "H2B_NO_STRIPS_SMALL", "H2B_STRIPS_24", "H2B_STRIPS_SMALL_MAX")
 for spec in specs:
     label, _, kv = spec.partition(":")
     for k in KNOBS:
