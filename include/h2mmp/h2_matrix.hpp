@@ -11,6 +11,8 @@
 #include <vector>
 
 #include "h2mmp/block_tree.hpp"
+#include "h2mmp/context.hpp"
+#include "h2mmp/truncation.hpp"
 #include "h2mmp/dense.hpp"
 
 namespace h2mmp {
@@ -201,6 +203,20 @@ DenseMatrix<Scalar> h2_to_dense(const H2Matrix<Scalar>& h) {
   for (int b = 0; b < n; ++b)
     for (int a = 0; a < n; ++a) out(t.perm[a], t.perm[b]) = dt(a, b);
   return out;
+}
+
+/// h2_matrix.cpp:213-278: exact H^2 matrix-vector product (forward transform, coupling
+/// products, backward transform, near field), on the B200 (h2c_mvp), original ordering.
+template <class Scalar>
+DenseVector<Scalar> mvp(const H2Matrix<Scalar>& h, const DenseVector<Scalar>& x) {
+  const int n = h.tree->size();
+  if (x.rows() != n || x.cols() != 1) throw ConfigError("mvp: vector length must match the matrix");
+  const detail::Flat<Scalar> f = detail::flatten(h);
+  DenseVector<Scalar> y(n, 1);
+  h2c_context* ctx = detail::default_context();
+  detail::rethrow(h2c_mvp(ctx, &f.desc, reinterpret_cast<const double*>(x.data()), 1, reinterpret_cast<double*>(y.data())),
+                  ctx);
+  return y;
 }
 
 }  // namespace h2mmp

@@ -8,3 +8,4 @@
 #include "h2mmp/geometry.hpp"
 #include "h2mmp/h2_matrix.hpp"
 #include "h2mmp/mmp.hpp"
+#include "h2mmp/truncation.hpp"

@@ -10,6 +10,7 @@
 #include <memory>
 #include <vector>
 
+#include "h2mmp/context.hpp"
 #include "h2mmp/h2_matrix.hpp"
 
 namespace h2mmp {
@@ -50,36 +51,12 @@ struct MmpResult {
 
 namespace detail {
 
-inline h2c_context* default_context() {
-  struct Holder {
-    h2c_context* c = nullptr;
-    ~Holder() {
-      if (c) h2c_destroy(c);
-    }
-  };
-  thread_local Holder h;
-  if (!h.c) {
-    h.c = h2c_create(0);
-    if (!h.c) throw DeviceError(h2c_last_error(nullptr));
-  }
-  return h.c;
-}
-
-inline void rethrow(int rc, h2c_context* ctx) {
-  const std::string msg = h2c_last_error(ctx);
-  switch (rc) {
-    case H2C_OK: return;
-    case H2C_ERR_CONFIG: throw ConfigError(msg);
-    case H2C_ERR_INVARIANT: throw InvariantError(msg);
-    default: throw DeviceError(msg);
-  }
-}
-
 template <class Scalar>
 MmpResult<Scalar> run(const H2Matrix<Scalar>& a, const H2Matrix<Scalar>& b, double eps, bool adaptive) {
-  // mmp.cpp:58-63 — shared tree and structure objects
+  // mmp.cpp:58-63 — shared tree and structure objects first, then eps (adaptive only)
   if (a.tree != b.tree || a.structure != b.structure)
     throw ConfigError("mmp: operands must share cluster trees and block structure");
+  if (adaptive && !(eps > 0.0 && eps < 1.0)) throw ConfigError("mmp: eps_trunc must be in (0,1)");
   h2c_context* ctx = default_context();
   const Flat<Scalar> fa = flatten(a);
   const Flat<Scalar> fb = (&a == &b) ? Flat<Scalar>{} : flatten(b);
@@ -124,7 +101,6 @@ MmpResult<Scalar> run(const H2Matrix<Scalar>& a, const H2Matrix<Scalar>& b, doub
 /// mmp.cpp:688-691
 template <class Scalar>
 MmpResult<Scalar> mmp(const H2Matrix<Scalar>& a, const H2Matrix<Scalar>& b, double eps_trunc) {
-  if (!(eps_trunc > 0.0 && eps_trunc < 1.0)) throw ConfigError("mmp: eps_trunc must be in (0,1)");
   return detail::run(a, b, eps_trunc, true);
 }
 

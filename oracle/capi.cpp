@@ -690,7 +690,9 @@ h2o_sliced* h2o_sliced_start(const h2c_matrix* a, const h2c_matrix* b, double ep
       using S = std::remove_reference_t<decltype(x->a.row_basis.leaf[0](0, 0))>;
       x->cs = convert_structure(a->tree, a->blocks);
       x->a = matrix_from<S>(*a, x->cs);
-      x->same = (a == b || a->values == b->values);
+      x->same = a == b || (a->values == b->values && a->n_values == b->n_values && a->row_rank == b->row_rank &&
+                           a->col_rank == b->col_rank && a->row_offset == b->row_offset &&
+                           a->col_offset == b->col_offset && a->block_offset == b->block_offset);
       if (!x->same) x->b = matrix_from<S>(*b, x->cs);
       x->eps = eps;
       x->adaptive = adaptive;

@@ -270,7 +270,14 @@ def _result(handle, a: H2Matrix) -> MmpResult:
     nc, nb = a.tree.n_clusters, a.structure.n_blocks
     w = 2 if d.scalar == h2c.H2C_COMPLEX else 1
     n = w * d.n_values
-    vals = np.ctypeslib.as_array(d.values, shape=(max(1, n),))[:n] if n else np.zeros(0)
+    if n:
+        # the array's base chain ends in a ctypes buffer that holds the owner, so any view of
+        # the values (even without the H2Matrix) keeps the library's pinned buffer alive
+        buf = (C.c_double * n).from_address(C.cast(d.values, C.c_void_p).value)
+        buf._owner = owner
+        vals = np.frombuffer(buf, dtype=np.float64)
+    else:
+        vals = np.zeros(0)
     if w == 2:
         vals = vals.view(np.complex128)
     prod = H2Matrix(a.tree, a.structure, d.scalar, h2c._copy(d.row_rank, nc, np.int32),

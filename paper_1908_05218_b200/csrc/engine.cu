@@ -190,6 +190,26 @@ class Arena {
   std::mutex mu_;
 };
 
+// Per-device state shared by every Context of the process: the arena (one cudaMalloc of
+// the free HBM minus a reserve, so it cannot be per context) and the mutex that serialises
+// calls on the device (the arena, the plan caches and the pinned pools are not re-entrant).
+// It lives until process exit, so buffers released after their Context is gone still
+// return to a live arena.
+struct DeviceShared {
+  std::recursive_mutex call_mu;
+  std::mutex init_mu;
+  Arena* arena = nullptr;
+  bool tried = false;
+};
+static DeviceShared& device_shared(int dev) {
+  static std::mutex m;
+  static std::map<int, DeviceShared*> all;
+  std::lock_guard<std::mutex> g(m);
+  DeviceShared*& p = all[dev];
+  if (!p) p = new DeviceShared;  // intentionally never freed (process lifetime)
+  return *p;
+}
+
 // the arena of the context running on this thread, and its main stream
 thread_local Arena* t_arena = nullptr;
 thread_local cudaStream_t t_arena_stream = nullptr;
@@ -1186,13 +1206,15 @@ struct EngineRun {
   // H2B_EIG_LIBRARY=1: cuSOLVER XsyevBatched instead of heev_kernel (A/B runs)
   const bool use_library = std::getenv("H2B_EIG_LIBRARY") != nullptr;
 
-  // Batched Hermitian eigensolver + truncation rule (heev.cuh).  Two placements, chosen per
-  // launch from tools/heev_bench.cu measurements on the B200 (profiles/r02/heev_bench.txt):
-  //  * few large Grams (one wave of clusters, n > 128): one cluster of CS CTAs per Gram with the
-  //    Gram in the cluster's shared memory (CS the smallest power of two that fits, <= 16);
-  //  * otherwise (the batched levels): one CTA per Gram with the Gram in a global (L2-resident)
-  //    slab and ~20-50 KB of shared memory, so 4-16 Grams share an SM and hide each other's
-  //    latency-bound phases.
+  // Batched Hermitian eigensolver + truncation rule (heev.cuh).  Placement per launch, from
+  // tools/heev_bench.cu on the B200 (profiles/r02/heev_bench.txt):
+  //  * n <= 64 (leaf Grams): one CTA per Gram, Gram in shared memory (2-3 CTAs per SM);
+  //  * 64 < n <= 256 with >= 64 Grams (the batched middle levels): one CTA per Gram with the
+  //    Gram in a global (L2-resident) slab and ~20-50 KB of shared memory, so several Grams
+  //    share an SM and hide each other's latency-bound phases;
+  //  * otherwise a cluster of CS CTAs per Gram (CS the smallest power of two whose column
+  //    slabs fit the CTAs' shared memory, <= 16; global slabs beyond), unless that needs more
+  //    than 4 waves of clusters, where the one-CTA global placement is faster.
   // Workspaces come from the main-stream arena before the fork.
   void heev(const DBuf& G, int count, int n, Trunc& t, cudaStream_t st) {
     constexpr int kMaxSmem = 232448, kSMs = 148;
@@ -1204,7 +1226,13 @@ struct EngineRun {
         break;
       }
     }
-    if (!(CS && n > 128 && (long long)count * CS <= kSMs)) {
+    if (!CS) {
+      CS = 16;
+      smem = false;
+    }
+    const bool batched_mid = n > 64 && n <= 256 && count >= 64;
+    const bool many_waves = (long long)count * CS > 4LL * kSMs;
+    if (n > 64 && (batched_mid || many_waves)) {
       CS = 1;
       smem = false;
     }
@@ -2347,6 +2375,10 @@ uint64_t structure_hash(const h2c_tree& t, const h2c_blocks& b) {
   mix(t.begin, sizeof(int32_t) * t.n_clusters);
   mix(t.end, sizeof(int32_t) * t.n_clusters);
   mix(t.level, sizeof(int32_t) * t.n_clusters);
+  if (t.child0) mix(t.child0, sizeof(int32_t) * t.n_clusters);
+  if (t.child1) mix(t.child1, sizeof(int32_t) * t.n_clusters);
+  if (t.bbox) mix(t.bbox, sizeof(double) * 6 * t.n_clusters);
+  if (t.perm) mix(t.perm, sizeof(int32_t) * t.n_points);
   mix(&b.n_blocks, sizeof(int64_t));
   mix(b.row, sizeof(int32_t) * b.n_blocks);
   mix(b.col, sizeof(int32_t) * b.n_blocks);
@@ -2451,7 +2483,6 @@ void* Context::side_solver(int i) {
 
 Context::~Context() {
   if (stream_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
-  delete static_cast<Arena*>(arena_);
   for (void* h : side_solvers_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(h));
   for (void* st : side_streams_) cudaStreamDestroy(static_cast<cudaStream_t>(st));
   if (green_ctx_ && green_destroy_)
@@ -2466,7 +2497,15 @@ Context::~Context() {
 
 const Plan& Context::plan_for(const h2c_tree& t, const h2c_blocks& b, double* build_seconds) {
   const uint64_t key = structure_hash(t, b);
-  if (plan_ && key == plan_key_) {
+  // a hash hit is confirmed against the cached descriptor contents (the permutation is what
+  // mvp / to_dense gather with; the plan itself depends on parent/begin/end/level and the blocks)
+  auto same_desc = [&] {
+    return t.n_points == plan_->n_points && t.n_clusters == static_cast<int>(plan_->n_clusters) &&
+           perm_.size() == size_t(t.n_points) && std::memcmp(perm_.data(), t.perm, sizeof(int32_t) * t.n_points) == 0 &&
+           key_rows_ == std::vector<int32_t>(b.row, b.row + b.n_blocks) &&
+           key_cols_ == std::vector<int32_t>(b.col, b.col + b.n_blocks);
+  };
+  if (plan_ && key == plan_key_ && same_desc()) {
     if (build_seconds) *build_seconds = 0.0;
     return *plan_;
   }
@@ -2474,6 +2513,8 @@ const Plan& Context::plan_for(const h2c_tree& t, const h2c_blocks& b, double* bu
   dplan_.reset();
   plan_ = std::make_unique<Plan>(build_plan(t, b, std::max(1u, std::thread::hardware_concurrency())));
   perm_.assign(t.perm, t.perm + t.n_points);
+  key_rows_.assign(b.row, b.row + b.n_blocks);
+  key_cols_.assign(b.col, b.col + b.n_blocks);
   dplan_ = upload_plan(*plan_, static_cast<cudaStream_t>(stream_));
   plan_key_ = key;
   if (build_seconds) *build_seconds = plan_->build_seconds;
@@ -2495,6 +2536,7 @@ struct ArenaScope {
 };
 
 std::shared_ptr<DevOperand> Context::upload(const h2c_matrix& m) {
+  std::lock_guard<std::recursive_mutex> call_lock(call_mutex());
   double bs = 0;
   const Plan& P = plan_for(*m.tree, *m.blocks, &bs);
   // resident operands live in the context's arena too (it holds nearly all free HBM once created)
@@ -2543,8 +2585,10 @@ static void fill_report(const Plan& P, const DevOperand& A, const DevOperand& B,
 
 
 Arena* Context::arena() {
-  if (!arena_tried_) {
-    arena_tried_ = true;
+  DeviceShared& D = device_shared(device_);
+  std::lock_guard<std::mutex> g(D.init_mu);
+  if (!D.tried) {
+    D.tried = true;
     // return what the stream-ordered pool keeps cached (release threshold is
     // unlimited) so the arena can claim it
     CK(cudaDeviceSynchronize());
@@ -2553,19 +2597,22 @@ Arena* Context::arena() {
     CK(cudaMemPoolTrimTo(pool, 0));
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
-    // outside the arena: cuSOLVER workspaces, index vectors, small buffers
+    // outside the arena: cuSOLVER workspaces (A/B runs), index vectors, small buffers
     const size_t reserve = size_t(4) << 30;
     if (fr > reserve + (size_t(4) << 30)) {
       auto* a = new Arena;
-      if (a->init(fr - reserve)) arena_ = a;
+      if (a->init(fr - reserve)) D.arena = a;
       else delete a;
     }
   }
-  return static_cast<Arena*>(arena_);
+  return D.arena;
 }
+
+std::recursive_mutex& Context::call_mutex() { return device_shared(device_).call_mu; }
 
 double Context::run_resident(const std::shared_ptr<DevOperand>& a, const std::shared_ptr<DevOperand>& b,
                              double eps, int adaptive, HostResult* out) {
+  std::lock_guard<std::recursive_mutex> call_lock(call_mutex());
   ArenaScope scope(arena(), static_cast<cudaStream_t>(stream_));
   if (!plan_ || a->key != plan_key_ || b->key != plan_key_)
     throw ConfigErr("mmp: operands were uploaded for another structure");
@@ -2599,6 +2646,7 @@ double Context::run_resident(const std::shared_ptr<DevOperand>& a, const std::sh
 }
 
 void Context::mvp(const std::shared_ptr<DevOperand>& a, const double* x_host, int nv, double* y_host) {
+  std::lock_guard<std::recursive_mutex> call_lock(call_mutex());
   if (!plan_ || a->key != plan_key_) throw ConfigErr("mvp: operand was uploaded for another structure");
   if (nv < 1) throw ConfigErr("mvp: need at least one vector");
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
@@ -2618,6 +2666,7 @@ void Context::mvp(const std::shared_ptr<DevOperand>& a, const double* x_host, in
 }
 
 void Context::to_dense(const std::shared_ptr<DevOperand>& a, double* out) {
+  std::lock_guard<std::recursive_mutex> call_lock(call_mutex());
   if (!plan_ || a->key != plan_key_) throw ConfigErr("to_dense: operand was uploaded for another structure");
   const int N = plan_->n_points;
   if (N > 32768) throw ConfigErr("to_dense: N > 32768 (use the MVP)");
@@ -2645,6 +2694,7 @@ void Context::to_dense(const std::shared_ptr<DevOperand>& a, double* out) {
 
 void Context::truncate_gram(int scalar, const double* gram, int n, double eps, double* basis, int* rank,
                             int* degenerate) {
+  std::lock_guard<std::recursive_mutex> call_lock(call_mutex());
   if (n < 1) throw ConfigErr("svd_truncate_gram: gram matrix must be square and non-empty");
   if (!(eps > 0.0 && eps < 1.0)) throw ConfigErr("svd_truncate_gram: eps must be in (0,1)");
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
@@ -2660,6 +2710,7 @@ void Context::truncate_gram(int scalar, const double* gram, int n, double eps, d
 }
 
 void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adaptive, HostResult& out) {
+  std::lock_guard<std::recursive_mutex> call_lock(call_mutex());
   const auto t0 = std::chrono::steady_clock::now();
   ArenaScope scope(arena(), static_cast<cudaStream_t>(stream_));
   if (a.tree != b.tree || a.blocks != b.blocks)  // mmp.cpp:58-63
@@ -2676,7 +2727,14 @@ void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adap
   auto secs = [](auto a0, auto a1) { return std::chrono::duration<double>(a1 - a0).count(); };
   const auto tu0 = now();
   auto A = upload_operand(P, a, s, &up_launches);
-  std::shared_ptr<DevOperand> B = (&a == &b || a.values == b.values) ? A : upload_operand(P, b, s, &up_launches);
+  // B shares A's upload only when it is the very same operand (same descriptor or identical
+  // descriptor contents); two operands that merely share a value buffer are uploaded apart
+  const bool same_operand =
+      &a == &b || (a.values == b.values && a.n_values == b.n_values && a.scalar == b.scalar &&
+                   a.row_rank == b.row_rank && a.col_rank == b.col_rank && a.row_offset == b.row_offset &&
+                   a.col_offset == b.col_offset && a.block_offset == b.block_offset &&
+                   a.row_degenerate == b.row_degenerate && a.col_degenerate == b.col_degenerate);
+  std::shared_ptr<DevOperand> B = same_operand ? A : upload_operand(P, b, s, &up_launches);
   const auto tu1 = now();
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));

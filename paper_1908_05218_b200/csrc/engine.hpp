@@ -89,7 +89,8 @@ class Context {
   void* stream() const { return stream_; }
   int device() const { return device_; }
   void* solver();  // cusolverDn handle bound to the stream (lazy)
-  struct Arena* arena();  // large-buffer arena of the main stream (lazy)
+  struct Arena* arena();  // large-buffer arena of the device, shared by every Context (lazy)
+  std::recursive_mutex& call_mutex();  // serialises calls on the device (process-wide)
   // side streams with their own cusolverDn handles.  0: auxiliary stream of
   // the off-critical-path work (leaf full targets, deferred coupling-target
   // sums) at low priority, optionally bound to a green context holding a
@@ -111,8 +112,6 @@ class Context {
   int device_;
   void* stream_ = nullptr;
   void* solver_ = nullptr;
-  void* arena_ = nullptr;
-  bool arena_tried_ = false;
   std::vector<void*> side_streams_, side_solvers_;
   void* green_ctx_ = nullptr;
   void* green_destroy_ = nullptr;
@@ -120,7 +119,7 @@ class Context {
   std::string err_;
   uint64_t plan_key_ = 0;
   std::unique_ptr<Plan> plan_;
-  std::vector<int32_t> perm_;
+  std::vector<int32_t> perm_, key_rows_, key_cols_;  // cached structure (confirms a plan-cache hit)
   std::unique_ptr<DevPlan> dplan_;
   int64_t launches_ = 0;
 };

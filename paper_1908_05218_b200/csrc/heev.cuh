@@ -48,6 +48,7 @@ struct HeevParams {
   uint8_t* degen_io;
   int* fail;         // set when a QL iteration does not converge
   long long* prof;   // optional: clock64() phase stamps of block 0 (tools/heev_bench.cu)
+  int dbg;           // tools/heev_bench.cu only: bit 0 skips the Z updates (times the QL chain alone)
   int n;
   double eps;
 };
@@ -183,10 +184,9 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
   nzf = __syncthreads_or(nzf);
   if (tid == 0) pub[6] = nzf ? 1.0 : 0.0;
   csync();
-  if (tid == 0) {
-    int nz = 0;
-    for (int q = 0; q < CS; ++q) nz |= (*cl.map_shared_rank(pub + 6, q)) != 0.0;
-    misc[38] = nz;
+  if (warp == 0) {
+    const int nz = __any_sync(0xffffffffu, lane < CS && (*cl.map_shared_rank(pub + 6, lane)) != 0.0);
+    if (lane == 0) misc[38] = nz;
   }
   __syncthreads();
   const bool nonzero = misc[38] != 0.0;
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
     const int jl0 = (k + 1 - r + CS - 1) / CS;  // first local column with j > k
     {
       const int act = ncl - jl0;
-      int ts = 1;
+      int ts = SMEM ? 1 : 32;  // global slabs: a full warp per column (coalesced rows)
       while (ts < 32 && act * ts < nt) ts <<= 1;
       const int teams = nt / ts, team = tid / ts, tl = tid % ts;
       for (int base = jl0; base < ncl; base += teams) {
@@ -276,10 +276,11 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       const int q = i % CS;
       yall[i] = q == r ? yown[i] : *cl.map_shared_rank(yown + i, q);
     }
-    if (tid == 0) {
+    if (warp == 0) {  // the CS gamma parts loaded in parallel, summed in rank order (same in every CTA)
+      const double part = lane < CS ? *cl.map_shared_rank(pub + 4, lane) : 0.0;
       double g = 0.0;
-      for (int q = 0; q < CS; ++q) g += *cl.map_shared_rank(pub + 4, q);  // fixed order: same in every CTA
-      misc[36] = g;
+      for (int q = 0; q < CS; ++q) g += __shfl_sync(0xffffffffu, part, q);
+      if (lane == 0) misc[36] = g;
     }
     __syncthreads();
     // rank-2 update of own columns j > k, rows i > k with w = tau y - (|tau|^2 gamma / 2) v:
@@ -335,30 +336,42 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
   // (the Householder reduction already perturbs every eigenvalue by O(eps_mach ||G||); the
   // rank rule compares against eps * lambda_max), so the null-space half of a Gram's spectrum
   // costs no extra sweeps.
+  // Called by all of warp 0 (uniform control flow): the scan for the next negligible
+  // off-diagonal runs 32 positions per step (ballot); the chain itself runs on lane 0.
   auto produce = [&](int q) -> void {
     double* rc = rcb[q];
     double* rs = rsb[q];
     int cnt = 0, mm = l;
-    meta[2 * q + 1] = 0;  // no chain unless one is produced below
+    if (lane == 0) meta[2 * q + 1] = 0;  // no chain unless one is produced below
     for (;;) {
       if (l >= n) {
-        meta[4] = 1;
+        if (lane == 0) meta[4] = 1;
         return;
       }
-      for (mm = l; mm < n - 1; ++mm)
-        if (fabs(e[mm]) <= tol) break;
+      mm = n - 1;
+      for (int b0 = l; b0 < n - 1; b0 += 32) {
+        const int i = b0 + lane;
+        const unsigned hit = __ballot_sync(0xffffffffu, i < n - 1 && fabs(e[i]) <= tol);
+        if (hit) {
+          mm = b0 + __ffs(hit) - 1;
+          break;
+        }
+      }
       if (mm == l) {
         ++l;
         iter = 0;
         continue;
       }
       if (++iter > 60) {
-        meta[5] = 1;
-        meta[4] = 1;
+        if (lane == 0) {
+          meta[5] = 1;
+          meta[4] = 1;
+        }
         return;
       }
       break;
     }
+    if (lane != 0) return;
     double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
     double rr = hypot(g, 1.0);
     g = d[mm] - d[l] + e[l] / (g + copysign(rr, g));
@@ -376,8 +389,14 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
         early = true;
         break;
       }
+#ifdef HEEV_DIV_ROTATION
+      const double rt = sqrt(t2);
+      const double inv = 1.0 / rt;
+      e[i + 1] = rt;
+#else
       const double inv = rsqrt(t2);
       e[i + 1] = t2 * inv;
+#endif
       s = f * inv;
       c = g * inv;
       g = di1 - pp;
@@ -402,14 +421,18 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
     ++sweeps;
     rots += cnt;
   };
-  if (tid == 0) {
-    meta[4] = 0;
-    meta[5] = 0;
+  if (warp == 0) {
     double an = 0.0;
-    for (int i = 0; i < n; ++i) an = fmax(an, fabs(d[i]) + fabs(e[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0));
+    for (int i = lane; i < n; i += 32) an = fmax(an, fabs(d[i]) + fabs(e[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0));
+    for (int of = 16; of > 0; of >>= 1) an = fmax(an, __shfl_xor_sync(0xffffffffu, an, of));
     tol = 2.2204460492503131e-16 * an;
-    meta[0] = 0;
-    meta[1] = 0;
+    if (lane == 0) {
+      meta[4] = 0;
+      meta[5] = 0;
+      meta[0] = 0;
+      meta[1] = 0;
+    }
+    __syncwarp();
     produce(0);
   }
   __syncthreads();
@@ -419,10 +442,11 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
     const bool done = meta[4] != 0;
     __syncthreads();  // everyone has read this sweep's meta before the producer overwrites buffer q^1
     if (done && cnt == 0) break;
-    if (tid == 0) {
+    if (warp == 0) {
       if (!meta[4]) produce(q ^ 1);
-      else meta[2 * (q ^ 1) + 1] = 0;
-    } else if (tid >= 32) {
+      else if (lane == 0) meta[2 * (q ^ 1) + 1] = 0;
+      __syncwarp();
+    } else if (!(p.dbg & 1)) {
       const double* rc = rcb[q];
       const double* rs = rsb[q];
       for (int il = tid - 32; il < nrl; il += nt - 32) {

@@ -5,6 +5,7 @@
 #include <atomic>
 #include <chrono>
 #include <stdexcept>
+#include <string>
 #include <thread>
 
 namespace h2b {
@@ -73,6 +74,9 @@ Status status_of(const std::vector<LevelPlan>& lv, int l, int i, int k) {
 
 void finish_csr(Csr& c, int n_out, const std::vector<int32_t>& owner) {
   // owner[e] = output of entry e; entries already in the wanted per-output order
+  if (owner.size() > size_t(INT32_MAX))  // row pointers are int32 on the device
+    throw std::length_error("structure plan: " + std::to_string(owner.size()) +
+                            " entries in one CSR list exceed the int32 index range");
   c.ptr.assign(n_out + 1, 0);
   for (int32_t o : owner) c.ptr[o + 1]++;
   for (int o = 0; o < n_out; ++o) c.ptr[o + 1] += c.ptr[o];

@@ -2,7 +2,9 @@
 // (tests/test_support.hpp:37-47 -> mmp(), test_mmp.cpp:50-59) compiled against
 // the B200 headers and linked to libh2mmp_b200.so.  Prints one line per check;
 // exit code 0 iff all pass.
+#include <cmath>
 #include <cstdio>
+#include <string>
 #include <memory>
 
 #include "h2mmp/h2mmp.hpp"
@@ -67,6 +69,31 @@ int main() {
     threw = true;
   }
   CHECK(threw);
+  // validation order of mmp.cpp:58-63: different trees are reported even with a bad eps
+  threw = false;
+  try {
+    (void)mmp(a, b, 2.0);
+  } catch (const ConfigError& e) {
+    threw = std::string(e.what()).find("share") != std::string::npos;
+  }
+  CHECK(threw);
+
+  // h2_matrix.hpp:62-66 mvp (device) against the dense matrix
+  DenseVector<Real> x(a.tree->size(), 1);
+  for (Index i = 0; i < x.rows(); ++i) x(i, 0) = std::sin(0.37 * double(i));
+  const DenseVector<Real> y = mvp(a, x);
+  const DenseVector<Real> yd = da * x;
+  CHECK((y - yd).norm() <= 1e-12 * yd.norm());
+
+  // truncation.hpp:7-19 svd_truncate_gram (device eigensolver): test_truncation.cpp's KATs
+  DenseMatrix<Real> g(4, 4);
+  g(0, 0) = 1.0;
+  g(1, 1) = 1e-1;
+  g(2, 2) = 1e-3;
+  const TruncatedBasis<Real> tb = svd_truncate_gram(g, 1e-2);
+  CHECK(tb.basis.cols() == 2 && !tb.degenerate);
+  const TruncatedBasis<Real> tz = svd_truncate_gram(DenseMatrix<Real>(5, 5), 1e-4);
+  CHECK(tz.degenerate && tz.basis.cols() == 1 && tz.basis(0, 0) == 1.0);
   std::printf("%s\n", failures ? "DROPIN FAIL" : "DROPIN OK");
   return failures ? 1 : 0;
 }

@@ -1,8 +1,12 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
-B=tools/heev_bench
 {
-for a in "128 512 0 0 256 1 0" "128 512 0 0 128 1 0" "128 8192 1 0 256 1 0" "128 8192 1 0 128 1 0" "256 512 0 0 256 1 0" "256 512 0 0 512 1 0" "406 256 0 0 256 1 0" "406 256 0 0 512 1 0" "406 256 0 0 512 2 0" "250 256 1 0 256 1 0" "610 2 0 0 512 1 0" "64 4096 1 0 128 1 0"; do
-  timeout 120 $B $a
+for B in tools/heev_bench tools/heev_bench_div; do
+  for dbg in 0 1; do
+    echo "== $B dbg=$dbg"
+    timeout 120 $B 610 2 0 0 512 16 1 $dbg
+    timeout 120 $B 406 16 0 0 512 8 1 $dbg
+    timeout 120 $B 128 64 0 0 256 1 1 $dbg
+  done
 done
-} > gpurun_out/heevb.txt 2>&1
+} > gpurun_out/heevb2.txt 2>&1

@@ -99,7 +99,7 @@ int main(int argc, char** argv) {
   long long* dProf;
   CK(cudaMalloc(&dProf, 8 * sizeof(long long)));
   CK(cudaMemset(dProf, 0, 8 * sizeof(long long)));
-  HeevParams hp{dG, dV, dZ, dSlab, dVec, dVal, dRank, dDeg, dFail, dProf, n, eps};
+  HeevParams hp{dG, dV, dZ, dSlab, dVec, dVal, dRank, dDeg, dFail, dProf, argc > 8 ? std::atoi(argv[8]) : 0, n, eps};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(count) * CS);
   cfg.blockDim = dim3(nt);
