@@ -57,13 +57,13 @@ CONFIGS = {
                                   "tree/structure; eps 1e-6"),
     "cfg5": (1048576, 64, 0, 1e-4, "Helmholtz exp(-i k r)/(4 pi r), k = 2 pi, complex128, N = 2^20 Fibonacci-sphere "
                                    "points (seeded rotation, seed 3), diameter 16 wavelengths, leaf 64, eta 1, "
-                                   "Chebyshev order per level clamp(ceil(1 + 1.2 k h_l), 3, 5) recompressed at "
+                                   "Chebyshev order per level clamp(ceil(1 + 1.2 k h_l), 3, 9) recompressed at "
                                    "1e-4; C = A*A, eps 1e-4"),
     # configs[4]'s construction at a quarter of the points on a sphere of half the radius (same
     # points per wavelength)
     "cfg5s": (262144, 64, 0, 1e-4, "configs[4] construction at N = 2^18 on a sphere of diameter 8 wavelengths "
                                    "(same points per wavelength): Helmholtz k = 2 pi, complex128, leaf 64, orders "
-                                   "clamp(ceil(1 + 1.2 k h_l), 3, 5), recompressed at 1e-4; C = A*A, eps 1e-4"),
+                                   "clamp(ceil(1 + 1.2 k h_l), 3, 9), recompressed at 1e-4; C = A*A, eps 1e-4"),
     "cfg4s": (110592, 64, 4, 1e-6, "configs[3] construction on the 48^3 grid (h = 1/49): C = A*B, A = 7-point FD "
                                    "Laplacian, B = Laplace Chebyshev order 4 (k=64), leaf 64, eta 1, eps 1e-6"),
 }
@@ -97,7 +97,14 @@ def sphere_points(n: int, seed: int = 3) -> np.ndarray:
     return np.ascontiguousarray(x @ q.T)
 
 
-def helmholtz_orders(tree, kappa: float = KAPPA, lo: int = 3, hi: int = 5) -> np.ndarray:
+# Chebyshev order cap of configs[4]: the order grows with the box size as clamp(ceil(1 + 1.2 kappa
+# h_l), 3, HELM_ORDER_CAP); at N = 2^20 the recompressed (1e-4) ranks of the operand saturate by
+# order 9 (max rank per level 46-49 at cap 5, 70-76 at 7, 75-87 at 9: profiles/r02/order_caps_cfg5.txt),
+# so higher orders only add constructor cost
+HELM_ORDER_CAP = 9
+
+
+def helmholtz_orders(tree, kappa: float = KAPPA, lo: int = 3, hi: int = HELM_ORDER_CAP) -> np.ndarray:
     """Chebyshev order per level from the largest box half-width h_l in wavelengths."""
     bb = np.asarray(tree.bbox).reshape(-1, 6)
     out = np.full(tree.depth + 1, lo, dtype=np.int32)

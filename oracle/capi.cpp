@@ -596,22 +596,27 @@ int h2o_relative_error(const h2c_matrix* a, const h2c_matrix* b, const h2c_matri
 
 // ---- multi-vector exact MVP (one conversion for nv vectors) -------------------
 int h2o_mvp_multi(const h2c_matrix* m, const double* x, int nv, double* y) {
+  // one conversion, the nv independent MVPs on the mmp thread count (h2o_set_mmp_threads)
   return guarded([&] {
     const Converted cs = convert_structure(m->tree, m->blocks);
     const int n = m->tree->n_points;
-    if (m->scalar == H2C_REAL) {
-      const H2Matrix<Real> h = matrix_from<Real>(*m, cs);
-      for (int v = 0; v < nv; ++v) {
-        const auto r = mvp(h, vec_in<Real>(x + size_t(v) * n, n));
-        std::memcpy(y + size_t(v) * n, r.data(), sizeof(double) * n);
-      }
-    } else {
-      const H2Matrix<Complex> h = matrix_from<Complex>(*m, cs);
-      for (int v = 0; v < nv; ++v) {
-        const auto r = mvp(h, vec_in<Complex>(x + 2 * size_t(v) * n, n));
-        std::memcpy(y + 2 * size_t(v) * n, r.data(), sizeof(Complex) * n);
-      }
-    }
+    auto run = [&](auto tag) {
+      using S = decltype(tag);
+      const int w = is_complex_v<S> ? 2 : 1;
+      const H2Matrix<S> h = matrix_from<S>(*m, cs);
+      std::atomic<int> next{0};
+      std::vector<std::thread> th;
+      for (int t = 0; t < std::max(1, std::min(g_mmp_threads, nv)); ++t)
+        th.emplace_back([&] {
+          for (int v; (v = next.fetch_add(1)) < nv;) {
+            const auto r = mvp(h, vec_in<S>(x + w * size_t(v) * n, n));
+            std::memcpy(y + w * size_t(v) * n, r.data(), sizeof(S) * n);
+          }
+        });
+      for (auto& t : th) t.join();
+    };
+    if (m->scalar == H2C_REAL) run(Real{});
+    else run(Complex{});
   });
 }
 

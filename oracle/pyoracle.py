@@ -244,12 +244,13 @@ def mvp(m: H2Matrix, x: np.ndarray) -> np.ndarray:
     return y
 
 
-def mvp_multi(m: H2Matrix, x: np.ndarray) -> np.ndarray:
-    """Y = A X for the columns of X (N x nv)."""
+def mvp_multi(m: H2Matrix, x: np.ndarray, threads: int = 1) -> np.ndarray:
+    """Y = A X for the columns of X (N x nv), the columns on `threads` threads."""
     xx = np.asfortranarray(x, dtype=m.dtype)
     if xx.ndim == 1:
         xx = xx.reshape(-1, 1, order="F")
     y = np.zeros_like(xx)
+    lib().h2o_set_mmp_threads(int(threads))
     _check(lib().h2o_mvp_multi(C.byref(m.desc()), xx.ctypes.data_as(P_f64), xx.shape[1], y.ctypes.data_as(P_f64)))
     return y
 

@@ -227,6 +227,8 @@ constexpr size_t kArenaMin = size_t(8) << 20;
 // per-buffer scratch bound of the chunked target / full-block / case-1 loops:
 // one chunk per level at cfg2, bounded scratch at the larger configurations
 constexpr size_t kChunkBytes = size_t(8) << 30;
+// the chunk bound actually used: kChunkBytes, or 1/24 of the arena's free bytes when that is
+// smaller (large configurations near the HBM capacity)
 
 struct DBuf {
   double* p = nullptr;
@@ -1552,46 +1554,64 @@ struct EngineRun {
   // targets, the parent's merged blocks Mg[l-1] (zero where a quadrant has no
   // child).  zero_tg: the targets accumulate onto case-1 values written first.
   void alloc_targets(int l, bool zero_tg) {
+    alloc_tg(l, zero_tg);
+    alloc_parent_merged(l);
+  }
+  void alloc_tg(int l, bool zero_tg) {
     const LevelPlan& L = P.lv[l];
-    const int na = static_cast<int>(L.adm.size()), np = static_cast<int>(L.pend_row.size());
-    const int nl = static_cast<int>(L.nl_block.size());
-    const int Kr = KCr[l], Kc = KCc[l];
-    HighScope targets_are_long_lived;
-    if (np > 0) {
-      const int nm = static_cast<int>(P.lv[l - 1].merged_row.size());
-      Mg[l - 1].alloc(sz(nm, 2 * Kr, 2 * Kc), s, true);
-    }
-    Tg[l].alloc(sz(na + nl, Kr, Kc), s, zero_tg);
+    const int na = static_cast<int>(L.adm.size()), nl = static_cast<int>(L.nl_block.size());
+    // the leaf targets sit with the other long-lived buffers at the top of the arena; an upper
+    // level's targets are allocated from the bottom: the only long-lived buffer created since
+    // this level's merged blocks is then below them, and the hole those leave when released
+    // joins the free middle of the arena (the parent's merged blocks are the largest buffers
+    // of a product: 70 GB at the 64^3 grid of configs[3])
+    HighScope targets_placement(l == D);
+    Tg[l].alloc(sz(na + nl, KCr[l], KCc[l]), s, zero_tg);
+  }
+  void alloc_parent_merged(int l) {
+    if (P.lv[l].pend_row.empty()) return;
+    const int nm = static_cast<int>(P.lv[l - 1].merged_row.size());
+    HighScope merged_blocks_are_long_lived;
+    Mg[l - 1].alloc(sz(nm, 2 * KCr[l], 2 * KCc[l]), s, true);
   }
 
   // case 1 of the upper levels (mmp.cpp:573-585): T^C_i^H M conj(T^C_k) of every
-  // merged block, written into its (admissible or pending) target before the
-  // triple sums accumulate onto it; in chunks (Zc = T^C_i^H M scratch)
-  void merged_into_targets(int l, const DBuf& M) {
+  // merged block, written into its target before the triple sums accumulate onto it; in
+  // chunks (Zc = T^C_i^H M scratch).  pend = false: admissible targets, straight into their
+  // Tg slots; pend = true: pending targets, into the compact store CP[e] (entry e of
+  // mz_pend), which scatter_pending() later copies into the parent's merged quadrants —
+  // so the merged blocks of this level are freed before the parent's are allocated
+  // (at the 64^3 grid, configs[3], the two would not fit next to each other).
+  void merged_into_targets(int l, const DBuf& M, bool pend, DBuf* CP) {
     const DevLevel& Q = DP.lv[l];
     const int Kn = KCr[l + 1], Kq = KCc[l + 1], Kr = KCr[l], Kc = KCc[l];
     const long long MM = 4LL * Kn * Kq;
-    for (int pend = 0; pend < 2; ++pend) {
-      const DevLevel::MZ& z = pend ? Q.mz_pend : Q.mz_adm;
-      if (z.n == 0) continue;
-      const size_t per = sz(1, Kr, 2 * Kq) * sizeof(double);
-      const int step = static_cast<int>(std::max<size_t>(4096, kChunkBytes / per));
-      for (int e0 = 0; e0 < z.n; e0 += step) {
-        const int cnt = std::min(step, z.n - e0);
-        DBuf Zc(sz(cnt, Kr, 2 * Kq), s);
-        segd(Zc, Kr, 2 * Kq, cnt,
-             {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), ref(M, MM, 2 * Kn, OP_N), 2 * Kn, nullptr, z.row + e0,
-                  z.m + e0}});
-        const Grp g{ref(Zc, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, nullptr, nullptr,
-                    z.col + e0};
-        if (pend) {
-          quad = {z.out + e0, Kr, Kc};
-          seg(Mg[l - 1], 4LL * Kr * Kc, 0, 2 * Kr, nullptr, Kr, Kc, cnt, false, {g});
-        } else {
-          seg(Tg[l], (long long)Kr * Kc, 0, Kr, z.out + e0, Kr, Kc, cnt, false, {g});
-        }
-      }
+    const DevLevel::MZ& z = pend ? Q.mz_pend : Q.mz_adm;
+    if (z.n == 0) return;
+    if (pend) CP->alloc(sz(z.n, Kr, Kc), s);
+    const size_t per = sz(1, Kr, 2 * Kq) * sizeof(double);
+    const int step = static_cast<int>(std::max<size_t>(4096, chunk_bytes() / per));
+    for (int e0 = 0; e0 < z.n; e0 += step) {
+      const int cnt = std::min(step, z.n - e0);
+      DBuf Zc(sz(cnt, Kr, 2 * Kq), s);
+      segd(Zc, Kr, 2 * Kq, cnt,
+           {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), ref(M, MM, 2 * Kn, OP_N), 2 * Kn, nullptr, z.row + e0,
+                z.m + e0}});
+      const Grp g{ref(Zc, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, nullptr, nullptr,
+                  z.col + e0};
+      if (pend) seg(CP->p, (long long)Kr * Kc, (long long)e0 * Kr * Kc, Kr, nullptr, Kr, Kc, cnt, false, {g});
+      else seg(Tg[l], (long long)Kr * Kc, 0, Kr, z.out + e0, Kr, Kc, cnt, false, {g});
     }
+  }
+  // the compact pending case-1 values into their quadrants of the parent's merged blocks
+  void scatter_pending(int l, const DBuf& CP) {
+    const DevLevel::MZ& z = DP.lv[l].mz_pend;
+    if (z.n == 0) return;
+    pre("scatter_quad", 0, 2LL * z.n * KCr[l] * KCc[l] * 8 * W);
+    scatter_quad_kernel<<<z.n, 256, 0, s>>>(Mg[l - 1], CP, z.out, KCr[l], KCc[l], W);
+    CK(cudaGetLastError());
+    post();
+    launches++;
   }
 
   // acc: accumulate onto the stores (upper levels, after merged_into_targets)
@@ -1612,12 +1632,17 @@ struct EngineRun {
     else on_aux(phase + "_deferred", rest);
   }
 
-  // target ranges in chunks that bound the per-target scratch (V1, U1, U2) to kChunkBytes each
+  size_t chunk_bytes() const {
+    if (!t_arena) return kChunkBytes;
+    const size_t fr = t_arena->stats().first;
+    return std::max<size_t>(size_t(512) << 20, std::min(kChunkBytes, fr / 24));
+  }
+  // target ranges in chunks that bound the per-target scratch (V1, U1, U2) to chunk_bytes() each
   template <class Fn>
   void chunks(int l, int t0, int cnt, Fn&& fn) {
     const size_t per = size_t(W) * sizeof(double) *
                        std::max({size_t(A.Kr[l]) * B.Kc[l], size_t(KCr[l]) * B.Kc[l], size_t(A.Kr[l]) * KCc[l]});
-    const int step = static_cast<int>(std::max<size_t>(4096, kChunkBytes / std::max<size_t>(per, 1)));
+    const int step = static_cast<int>(std::max<size_t>(4096, chunk_bytes() / std::max<size_t>(per, 1)));
     for (int c = 0; c < cnt; c += step) fn(t0 + c, std::min(step, cnt - c));
   }
 
@@ -1842,7 +1867,7 @@ struct EngineRun {
     }
     // in chunks of full blocks: bounded T2 / T4 / U scratch (kChunkBytes each)
     const size_t per = size_t(W) * sizeof(double) * std::max(size_t(NL) * KBc, size_t(KAr) * std::max(KBc, NL));
-    const int step = static_cast<int>(std::max<size_t>(4096, kChunkBytes / per));
+    const int step = static_cast<int>(std::max<size_t>(4096, chunk_bytes() / per));
     for (int t0 = 0; t0 < nn; t0 += step) {
       const int cnt = std::min(step, nn - t0);
       const DevCsr fr = sub_csr(Q.fr, L.fr, t0, cnt), rr = sub_csr(Q.rr, L.rr, t0, cnt),
@@ -2008,9 +2033,14 @@ struct EngineRun {
     mark("L" + std::to_string(l) + ".targets");
     // case 1 over merged children couplings first (mmp.cpp:573-585), then the
     // triple sums of cases 2-4 accumulate onto the same stores
-    alloc_targets(l, true);
-    merged_into_targets(l, Mg);
+    DBuf CP;
+    merged_into_targets(l, Mg, true, &CP);  // pending targets: compact, while only Mg[l] is live
+    alloc_tg(l, true);
+    merged_into_targets(l, Mg, false, nullptr);
     Mg.release();
+    alloc_parent_merged(l);
+    scatter_pending(l, CP);
+    CP.release();
     targets(l, SB, nullptr, nullptr, true);
     retire(std::move(SB));
   }

@@ -254,8 +254,22 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
         const bool ok = jl < ncl && j < n;
         T acc = N::zero();
         if (ok) {
-          const T* cj = slab + (size_t)jl * ld;
-          for (int i = k + 1 + tl; i < n; i += ts) acc = N::cfma(cj[i], vloc[i], acc);
+          const T* __restrict__ cj = slab + (size_t)jl * ld;
+          if (SMEM) {
+            for (int i = k + 1 + tl; i < n; i += ts) acc = N::cfma(cj[i], vloc[i], acc);
+          } else {  // L2-resident slab: 4 loads in flight per lane
+            T a1 = N::zero(), a2 = N::zero(), a3 = N::zero();
+            int i = k + 1 + tl;
+            for (; i + 3 * ts < n; i += 4 * ts) {
+              const T b0 = cj[i], b1 = cj[i + ts], b2 = cj[i + 2 * ts], b3 = cj[i + 3 * ts];
+              acc = N::cfma(b0, vloc[i], acc);
+              a1 = N::cfma(b1, vloc[i + ts], a1);
+              a2 = N::cfma(b2, vloc[i + 2 * ts], a2);
+              a3 = N::cfma(b3, vloc[i + 3 * ts], a3);
+            }
+            for (; i < n; i += ts) acc = N::cfma(cj[i], vloc[i], acc);
+            acc = N::add(N::add(acc, a1), N::add(a2, a3));
+          }
         }
         for (int of = ts >> 1; of > 0; of >>= 1) acc = N::add(acc, N::shfl_xor(acc, of));
         if (ok && tl == 0) yown[j] = acc;
@@ -289,19 +303,37 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       const double c = 0.5 * N::abs2(tau) * misc[36];
       const int m = n - k - 1;
       const int ncol = ncl - jl0;
-      for (long long x = tid; x < (long long)ncol * m; x += nt) {
-        const int jl = jl0 + static_cast<int>(x / m);
-        const int i = k + 1 + static_cast<int>(x % m);
-        const int j = jl * CS + r;
-        if (j >= n) continue;
-        const T vi = vloc[i], vj = vloc[j];
-        const T wi = N::sub(N::mul(tau, yall[i]), N::scale(vi, c));
-        const T wj = N::sub(N::mul(tau, yall[j]), N::scale(vj, c));
-        T* a = slab + (size_t)jl * ld + i;
-        T v = *a;
-        v = N::sub(v, N::mul(vi, N::conj(wj)));
-        v = N::sub(v, N::mul(wi, N::conj(vj)));
-        *a = v;
+      const long long tot = (long long)ncol * m;
+      constexpr int U = 4;  // elements per thread per batch: loads issued before any store
+      for (long long x0 = tid; x0 < tot; x0 += (long long)U * nt) {
+        T* ap[U];
+        T av[U], vi[U], wi[U], vj[U], wj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const long long x = x0 + (long long)u * nt;
+          ap[u] = nullptr;
+          if (x < tot) {
+            const int jl = jl0 + static_cast<int>(x / m);
+            const int i = k + 1 + static_cast<int>(x % m);
+            const int j = jl * CS + r;
+            if (j < n) {
+              ap[u] = slab + (size_t)jl * ld + i;
+              vi[u] = vloc[i];
+              vj[u] = vloc[j];
+              wi[u] = N::sub(N::mul(tau, yall[i]), N::scale(vi[u], c));
+              wj[u] = N::sub(N::mul(tau, yall[j]), N::scale(vj[u], c));
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ap[u]) av[u] = *ap[u];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ap[u]) {
+            T v = N::sub(av[u], N::mul(vi[u], N::conj(wj[u])));
+            *ap[u] = N::sub(v, N::mul(wi[u], N::conj(vj[u])));
+          }
       }
     }
     __syncthreads();
@@ -450,15 +482,29 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       const double* rc = rcb[q];
       const double* rs = rsb[q];
       for (int il = tid - 32; il < nrl; il += nt - 32) {
-        double carry = Z[(size_t)mm * nrl + il];
-        for (int t = 0; t < cnt; ++t) {
-          const int i = mm - 1 - t;
-          const double zi = Z[(size_t)i * nrl + il];
-          const double c = rc[t], s = rs[t];
-          Z[(size_t)(i + 1) * nrl + il] = fma(s, zi, c * carry);
-          carry = fma(c, zi, -s * carry);
+        double* __restrict__ zc0 = Z + il;
+        double carry = zc0[(size_t)mm * nrl];
+        // the next z values are loaded ahead of the stores (no store-to-load serialisation
+        // when Z lives in a global slab)
+        double nxt[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) nxt[u] = (u < cnt) ? zc0[(size_t)(mm - 1 - u) * nrl] : 0.0;
+        for (int t = 0; t < cnt; t += 4) {
+          double cur[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) nxt[u] = (t + 4 + u < cnt) ? zc0[(size_t)(mm - 5 - t - u) * nrl] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (t + u < cnt) {
+              const int i = mm - 1 - t - u;
+              const double c = rc[t + u], s = rs[t + u];
+              zc0[(size_t)(i + 1) * nrl] = fma(s, cur[u], c * carry);
+              carry = fma(c, cur[u], -s * carry);
+            }
         }
-        if (cnt > 0) Z[(size_t)(mm - cnt) * nrl + il] = carry;
+        if (cnt > 0) zc0[(size_t)(mm - cnt) * nrl] = carry;
       }
     }
     __syncthreads();

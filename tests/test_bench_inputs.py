@@ -31,7 +31,7 @@ def test_helmholtz_orders_grow_toward_the_root():
     t = P.build_cluster_tree(x, 64)
     o = bench.helmholtz_orders(t)
     assert o.shape == (t.depth + 1,)
-    assert (np.diff(o) <= 0).all() and o[-1] == 3 and o.max() == 5
+    assert (np.diff(o) <= 0).all() and o[-1] == 3 and o.max() <= bench.HELM_ORDER_CAP and o.max() > 5
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])

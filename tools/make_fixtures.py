@@ -58,9 +58,9 @@ def make(name: str, threads: int) -> dict:
     t_oracle = time.perf_counter() - t0
     X, Wv = probe_vectors(n, cplx)
     t0 = time.perf_counter()
-    Y = O.mvp_multi(ref.product, X)
-    SA = Wv.conj().T @ O.mvp_multi(A, X)
-    SB = SA if B is A else Wv.conj().T @ O.mvp_multi(B, X)
+    Y = O.mvp_multi(ref.product, X, threads)
+    SA = Wv.conj().T @ O.mvp_multi(A, X, threads)
+    SB = SA if B is A else Wv.conj().T @ O.mvp_multi(B, X, threads)
     t_probe = time.perf_counter() - t0
     rows = probe_rows(n)
     rep = ref.report
