@@ -223,6 +223,13 @@ struct HighScope {
 // the auxiliary stream of the run on this thread: its buffers also come from the
 // arena and are returned through Arena::free_after
 thread_local cudaStream_t t_aux_stream = nullptr;
+// memory-pressure hook of the run on this thread: frees device memory (eviction of buffers the
+// rest of the product does not read) and returns true if it did
+struct Relief {
+  virtual bool relieve() = 0;
+  virtual ~Relief() = default;
+};
+thread_local Relief* t_relief = nullptr;
 constexpr size_t kArenaMin = size_t(8) << 20;
 // per-buffer scratch bound of the chunked target / full-block / case-1 loops:
 // one chunk per level at cfg2, bounded scratch at the larger configurations
@@ -267,6 +274,8 @@ struct DBuf {
         t_arena->reclaim(false);
         p = static_cast<double*>(t_arena->alloc(n * sizeof(double), t_arena_high));
       }
+      while (!p && t_relief && t_relief->relieve())  // evict what the rest of the product does not read
+        p = static_cast<double*>(t_arena->alloc(n * sizeof(double), t_arena_high));
       if (p) {
         arena = t_arena;
         aux = st != t_arena_stream;
@@ -713,6 +722,35 @@ struct Ref {
   long long off;  // view offset (scalars)
   int ld;
   int op;
+  const double* const* ch = nullptr;  // chunked storage (Chunked::table), see SegGroup::Lch
+  int sh = 0;
+};
+
+// A per-level store of many equal blocks kept as power-of-two block chunks of <= 4 GiB
+// (the merged 2x2 blocks: 55-70 GB at the 64^3 grid of configs[3]) so it needs no single
+// contiguous region of the arena; the kernels address block b at table[b >> shift].
+struct Chunked {
+  std::vector<DBuf> parts;
+  DVec<double*> table;
+  int shift = 0;
+  bool empty() const { return parts.empty(); }
+  void alloc(long long nblocks, long long block_doubles, cudaStream_t st, bool zero) {
+    release();
+    const long long cap = (long long)(size_t(4) << 30) / 8;  // doubles per chunk
+    shift = 0;
+    while ((2LL << shift) * block_doubles <= cap && (1LL << shift) < nblocks) ++shift;
+    const long long bpc = 1LL << shift;
+    std::vector<double*> ptrs;
+    for (long long b0 = 0; b0 < std::max<long long>(nblocks, 1); b0 += bpc) {
+      parts.emplace_back(size_t(std::min(bpc, std::max<long long>(nblocks, 1) - b0) * block_doubles), st, zero);
+      ptrs.push_back(parts.back().p);
+    }
+    table.upload(ptrs, st);
+  }
+  void release() {
+    parts.clear();
+    table.release();
+  }
 };
 struct Grp {
   Ref L, R;
@@ -722,7 +760,7 @@ struct Grp {
   const int* ri;
 };
 
-struct EngineRun {
+struct EngineRun : Relief {
   Context& ctx;
   const Plan& P;
   const DevPlan& DP;
@@ -813,7 +851,8 @@ struct EngineRun {
   DBuf Vr, Vc, F;
   // Tg: [adm | NL] coupling targets per level; Mg[l]: merged 2x2 blocks of level l,
   // written directly by level l+1's pending targets (mmp.cpp:344-365)
-  std::vector<DBuf> Tr, Tc, Tg, Mg;
+  std::vector<DBuf> Tr, Tc, Tg;
+  std::vector<Chunked> Mg;
   // H2B_NO_DEFER=1: admissible / NL targets on the main stream (A/B runs)
   const bool no_defer_env = std::getenv("H2B_NO_DEFER") != nullptr;
   bool defer_targets = true;  // set in run(): off when profiling or H2B_NO_DEFER
@@ -855,9 +894,76 @@ struct EngineRun {
     hold.clear();  // frees on the main stream, ordered after the join
     joined = true;
   }
+  // ---- memory pressure (configs[3] at the 64^3 grid): buffers the upper levels do not read
+  // move to pinned host memory and come back when needed: the operands' full blocks once the
+  // leaf phase is done (restored at the end of the product), C's full blocks and leaf targets
+  // once the deferred leaf work has finished (restored for the split).  Off unless an
+  // allocation fails.
+  struct Evicted {
+    DBuf* buf;
+    double* host;
+    size_t bytes, n;
+    bool operand;
+  };
+  std::vector<Evicted> evicted;
+  bool leaf_done = false;
+  Relief* prev_relief = nullptr;
+  bool evict(DBuf& b, bool operand) {
+    if (!b.p) return false;
+    for (auto& e : evicted)
+      if (e.buf == &b) return false;
+    if (!operand) {  // C's stores are written by the deferred (auxiliary-stream) work
+      if (s_aux) CK(cudaStreamSynchronize(s_aux));
+    }
+    CK(cudaStreamSynchronize(s));
+    Evicted e{&b, nullptr, b.n * sizeof(double), b.n, operand};
+    size_t got = 0;
+    e.host = ctx.pinned->take(e.bytes, &got);
+    CK(cudaMemcpyAsync(e.host, b.p, e.bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    e.bytes = got;
+    b.release();
+    if (t_arena) t_arena->reclaim(false);
+    evicted.push_back(e);
+    if (std::getenv("H2B_MEM_TRACE"))
+      std::fprintf(stderr, "[mem] evicted %zu MiB to pinned host memory (%s)\n", (e.n * 8) >> 20,
+                   operand ? "operand full blocks" : "C leaf stores");
+    return true;
+  }
+  bool relieve() override {
+    if (!leaf_done) return false;
+    if (evict(const_cast<DBuf&>(A.F), true)) return true;
+    if (evict(const_cast<DBuf&>(B.F), true)) return true;
+    if (evict(F, false)) return true;
+    if (evict(Tg[D], false)) return true;
+    return false;
+  }
+  void restore(bool operands) {
+    for (size_t i = 0; i < evicted.size();) {
+      Evicted& e = evicted[i];
+      if (e.operand != operands) {
+        ++i;
+        continue;
+      }
+      {
+        HighScope long_lived;
+        e.buf->alloc(e.n, s);
+      }
+      CK(cudaMemcpyAsync(e.buf->p, e.host, e.n * sizeof(double), cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      ctx.pinned->give(e.host, e.bytes);
+      evicted.erase(evicted.begin() + i);
+    }
+  }
   ~EngineRun() {
     // deferred work may still read held buffers (error paths): drain it first
     if (s_aux) cudaStreamSynchronize(s_aux);
+    try {
+      restore(true);  // operands stay resident across calls
+      restore(false);
+    } catch (...) {
+    }
+    t_relief = prev_relief;
     t_aux_stream = prev_aux;
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_full) cudaEventDestroy(ev_full);
@@ -889,6 +995,8 @@ struct EngineRun {
     s_aux = static_cast<cudaStream_t>(c.side_stream(0));
     prev_aux = t_aux_stream;
     t_aux_stream = s_aux;
+    prev_relief = t_relief;
+    t_relief = this;
     CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_full, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
@@ -951,12 +1059,20 @@ struct EngineRun {
     const int* mq = nullptr;
     int qm = 0, qn = 0;
   } quad;
+  // one-shot chunked output store for the next seg() (see SegParams::och)
+  const Chunked* ochunk = nullptr;
   void seg(double* out, long long Os, long long Ooff, int Old, const int* omap, int M, int N, int n_out,
            bool acc, std::initializer_list<Grp> gs, bool sym = false) {
     const Quad qd = quad;
     quad = Quad{};
+    const Chunked* oc = ochunk;
+    ochunk = nullptr;
     if (n_out <= 0) return;
     SegParams sp{};
+    if (oc) {
+      sp.och = oc->table.p;
+      sp.osh = oc->shift;
+    }
     sp.oquad = qd.mq;
     sp.qm = qd.qm;
     sp.qn = qd.qn;
@@ -977,6 +1093,10 @@ struct EngineRun {
       if (ng >= kMaxGroups) throw std::logic_error("seg: too many groups");
       SegGroup& G = sp.g[ng++];
       G.L = g.L.p;
+      G.Lch = g.L.ch;
+      G.Lsh = g.L.sh;
+      G.Rch = g.R.ch;
+      G.Rsh = g.R.sh;
       G.Ls = g.L.s;
       G.Loff = g.L.off;
       G.Lld = g.L.ld;
@@ -1122,6 +1242,9 @@ struct EngineRun {
   static Ref ref(const double* p, long long stride, int ld, int op, long long off = 0) {
     return Ref{p, stride, off, ld, op};
   }
+  static Ref cref(const Chunked& c, long long stride, int ld, int op, long long off = 0) {
+    return Ref{nullptr, stride, off, ld, op, c.table.p, c.shift};
+  }
 
   void seg_add(double* out, long long Os, const double* in, long long Is, const DevCsr& c, long long elems) {
     if (c.n_out <= 0) return;
@@ -1209,17 +1332,16 @@ struct EngineRun {
   const bool use_library = std::getenv("H2B_EIG_LIBRARY") != nullptr;
 
   // Batched Hermitian eigensolver + truncation rule (heev.cuh).  Placement per launch, from
-  // tools/heev_bench.cu on the B200 (profiles/r02/heev_bench.txt):
-  //  * n <= 64 (leaf Grams): one CTA per Gram, Gram in shared memory (2-3 CTAs per SM);
-  //  * 64 < n <= 256 with >= 64 Grams (the batched middle levels): one CTA per Gram with the
-  //    Gram in a global (L2-resident) slab and ~20-50 KB of shared memory, so several Grams
-  //    share an SM and hide each other's latency-bound phases;
-  //  * otherwise a cluster of CS CTAs per Gram (CS the smallest power of two whose column
-  //    slabs fit the CTAs' shared memory, <= 16; global slabs beyond), unless that needs more
-  //    than 4 waves of clusters, where the one-CTA global placement is faster.
+  // tools/heev_bench.cu on the B200 (profiles/r02/heev_*.txt):
+  //  * n <= 96 (leaf Grams): one CTA per Gram, Gram in shared memory (2-3 CTAs per SM);
+  //  * many Grams (>= 64, or >= 32 with n <= 400: the batched middle levels): one CTA per Gram
+  //    with the Gram in a global (L2-resident) slab and ~20-50 KB of shared memory, so several
+  //    Grams share an SM and hide each other's latency-bound phases;
+  //  * few large Grams: a cluster of CS CTAs per Gram (CS the smallest power of two whose
+  //    column slabs fit the CTAs' shared memory, <= 16; global slabs beyond).
   // Workspaces come from the main-stream arena before the fork.
   void heev(const DBuf& G, int count, int n, Trunc& t, cudaStream_t st) {
-    constexpr int kMaxSmem = 232448, kSMs = 148;
+    constexpr int kMaxSmem = 232448;
     int CS = 0;
     bool smem = true;
     for (int cs : {1, 2, 4, 8, 16}) {
@@ -1232,9 +1354,8 @@ struct EngineRun {
       CS = 16;
       smem = false;
     }
-    const bool batched_mid = n > 64 && n <= 256 && count >= 64;
-    const bool many_waves = (long long)count * CS > 4LL * kSMs;
-    if (n > 64 && (batched_mid || many_waves)) {
+    const bool many = count >= 64 || (count >= 32 && n <= 400);
+    if (n > 96 && many) {
       CS = 1;
       smem = false;
     }
@@ -1572,7 +1693,7 @@ struct EngineRun {
     if (P.lv[l].pend_row.empty()) return;
     const int nm = static_cast<int>(P.lv[l - 1].merged_row.size());
     HighScope merged_blocks_are_long_lived;
-    Mg[l - 1].alloc(sz(nm, 2 * KCr[l], 2 * KCc[l]), s, true);
+    Mg[l - 1].alloc(nm, (long long)sz(1, 2 * KCr[l], 2 * KCc[l]), s, true);
   }
 
   // case 1 of the upper levels (mmp.cpp:573-585): T^C_i^H M conj(T^C_k) of every
@@ -1582,7 +1703,7 @@ struct EngineRun {
   // mz_pend), which scatter_pending() later copies into the parent's merged quadrants —
   // so the merged blocks of this level are freed before the parent's are allocated
   // (at the 64^3 grid, configs[3], the two would not fit next to each other).
-  void merged_into_targets(int l, const DBuf& M, bool pend, DBuf* CP) {
+  void merged_into_targets(int l, const Chunked& M, bool pend, DBuf* CP) {
     const DevLevel& Q = DP.lv[l];
     const int Kn = KCr[l + 1], Kq = KCc[l + 1], Kr = KCr[l], Kc = KCc[l];
     const long long MM = 4LL * Kn * Kq;
@@ -1595,7 +1716,7 @@ struct EngineRun {
       const int cnt = std::min(step, z.n - e0);
       DBuf Zc(sz(cnt, Kr, 2 * Kq), s);
       segd(Zc, Kr, 2 * Kq, cnt,
-           {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), ref(M, MM, 2 * Kn, OP_N), 2 * Kn, nullptr, z.row + e0,
+           {Grp{ref(Tr[l], 2LL * Kn * Kr, 2 * Kn, OP_H), cref(M, MM, 2 * Kn, OP_N), 2 * Kn, nullptr, z.row + e0,
                 z.m + e0}});
       const Grp g{ref(Zc, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, nullptr, nullptr,
                   z.col + e0};
@@ -1608,7 +1729,7 @@ struct EngineRun {
     const DevLevel::MZ& z = DP.lv[l].mz_pend;
     if (z.n == 0) return;
     pre("scatter_quad", 0, 2LL * z.n * KCr[l] * KCc[l] * 8 * W);
-    scatter_quad_kernel<<<z.n, 256, 0, s>>>(Mg[l - 1], CP, z.out, KCr[l], KCc[l], W);
+    scatter_quad_kernel<<<z.n, 256, 0, s>>>(Mg[l - 1].table.p, Mg[l - 1].shift, CP, z.out, KCr[l], KCc[l], W);
     CK(cudaGetLastError());
     post();
     launches++;
@@ -1622,7 +1743,7 @@ struct EngineRun {
     const int nl = static_cast<int>(L.nl_block.size());
     if (np > 0)  // pending targets straight into the parent's merged blocks (critical path)
       chunks(l, na, np, [&](int t0, int cnt) {
-        targets_range(l, t0, cnt, Mg[l - 1], 0, SB, WA, WB, acc, Q.pend_mq + (t0 - na));
+        targets_range(l, t0, cnt, nullptr, 0, SB, WA, WB, acc, Q.pend_mq + (t0 - na), &Mg[l - 1]);
       });
     auto rest = [&] {
       chunks(l, 0, na, [&](int t0, int cnt) { targets_range(l, t0, cnt, Tg[l], t0, SB, WA, WB, acc); });
@@ -1694,7 +1815,7 @@ struct EngineRun {
   //   U2 = sum_{A adm, B near} S^A_ij coll_b_jk
   // oq: quadrant scatter of the outputs into merged 2x2 blocks (pending targets), else slots slot0..
   void targets_range(int l, int t0, int cnt, double* out, long long slot0, const DBuf& SB, const DBuf* WA,
-                     const DBuf* WB, bool acc, const int* oq = nullptr) {
+                     const DBuf* WB, bool acc, const int* oq = nullptr, const Chunked* oc = nullptr) {
     if (cnt <= 0) return;
     const LevelPlan& L = P.lv[l];
     const DevLevel& Q = DP.lv[l];
@@ -1721,6 +1842,7 @@ struct EngineRun {
                  trow, nullptr};
     const Grp gB{ref(U1, (long long)Kr * KBc, Kr, OP_N), PBk, KBc, nullptr, nullptr, tcol};
     quad = {oq, Kr, Kc};
+    ochunk = oc;
     if (WA) {
       const DevCsr ww = sub_csr(Q.ww, L.ww, t0, cnt);
       seg(out, os, slot0 * os, old, nullptr, Kr, Kc, cnt, acc,
@@ -1913,7 +2035,7 @@ struct EngineRun {
     mark("L" + std::to_string(l) + ".assemble");
     // merged children couplings and assembled collected blocks (mmp.cpp:344-404)
     DBuf Aa, Ab;
-    DBuf Mg = std::move(this->Mg[l]);  // filled by level l+1's pending targets
+    Chunked Mg = std::move(this->Mg[l]);  // filled by level l+1's pending targets
     (void)Lc;
     (void)nm;
     gather(Aa, ns, LA[l + 1], (long long)Kn * KBr1, Kn, KBr1, Q.sub_child);
@@ -1958,7 +2080,7 @@ struct EngineRun {
       // row transfer Gram (mmp.cpp:406-457)
       DBuf g1(sz(n, 2 * Kn, 2 * Kn), s), g2(sz(n, 2 * Kn, 2 * Kn), s), g3(sz(n, 2 * Kn, 2 * Kn), s);
       segh(g1, 2 * Kn, n,
-           {Grp{ref(Mg, MM, 2 * Kn, OP_N), ref(Mg, MM, 2 * Kn, OP_H), 2 * Kq, &Q.row_merged, nullptr, nullptr}});
+           {Grp{cref(Mg, MM, 2 * Kn, OP_N), cref(Mg, MM, 2 * Kn, OP_H), 2 * Kq, &Q.row_merged, nullptr, nullptr}});
       segh(g2, 2 * Kn, n,
            {Grp{ref(X, 2LL * Kn * KBr, 2 * Kn, OP_N), ref(X, 2LL * Kn * KBr, 2 * Kn, OP_H), KBr, &Q.row_near,
                 nullptr, nullptr}});
@@ -1972,7 +2094,7 @@ struct EngineRun {
       // column transfer Gram (mmp.cpp:459-512)
       DBuf c1(sz(n, 2 * Kq, 2 * Kq), s), c2(sz(n, 2 * Kq, 2 * Kq), s), c3(sz(n, 2 * Kq, 2 * Kq), s);
       segh(c1, 2 * Kq, n,
-           {Grp{ref(Mg, MM, 2 * Kn, OP_T), ref(Mg, MM, 2 * Kn, OP_C), 2 * Kn, &Q.col_merged, nullptr, nullptr}});
+           {Grp{cref(Mg, MM, 2 * Kn, OP_T), cref(Mg, MM, 2 * Kn, OP_C), 2 * Kn, &Q.col_merged, nullptr, nullptr}});
       segh(c2, 2 * Kq, n,
            {Grp{ref(Xc, 2LL * Kq * KAc, 2 * Kq, OP_N), ref(Xc, 2LL * Kq * KAc, 2 * Kq, OP_H), KAc, &Q.col_near,
                 nullptr, nullptr}});
@@ -2048,6 +2170,7 @@ struct EngineRun {
   // ---- top-down split of non-leaf couplings (mmp.cpp:617-659) --------------
   void split() {
     join();
+    restore(false);  // C's evicted leaf stores receive split contributions
     mark("split");
     for (int l = 1; l < D; ++l) {
       const LevelPlan& L = P.lv[l];
@@ -2089,9 +2212,11 @@ struct EngineRun {
     try {
       basis_products();
       leaf_phase();
+      leaf_done = true;
       for (int l = D - 1; l >= 1; --l) upper_level(l);
       split();
       join();
+      restore(true);
     } catch (const CudaError& e) {
       throw CudaError(std::string(e.what()) + " [phase " + phase + "]");
     }

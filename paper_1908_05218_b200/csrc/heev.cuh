@@ -192,6 +192,14 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
   const bool nonzero = misc[38] != 0.0;
 
   // ---- 1. tridiagonalisation ------------------------------------------------
+  long long tprev = stamp ? clock64() : 0;
+  auto lap = [&](int slot) {
+    if (stamp) {
+      const long long t = clock64();
+      p.prof[slot] += t - tprev;
+      tprev = t;
+    }
+  };
   for (int k = 0; k + 1 < n; ++k) {
     const int o = k % CS;
     if (r == o) {
@@ -231,6 +239,7 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       }
       if (tid == 0) Vg[k + (size_t)k * n] = N::make(pub[0], pub[1]);  // tau_k on the diagonal slot
     }
+    lap(8);
     csync();  // (1) v, tau published by the owner
     const double* po = cl.map_shared_rank(pub, o);
     const T tau = N::make(po[0], po[1]);
@@ -241,6 +250,7 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       d[k] = po[3];
     }
     __syncthreads();
+    lap(9);
     // y_j = sum_{i>k} conj(B_ij) v_i for own columns j > k: a team of ts lanes per column
     const int jl0 = (k + 1 - r + CS - 1) / CS;  // first local column with j > k
     {
@@ -276,6 +286,7 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       }
     }
     __syncthreads();
+    lap(10);
     if (warp == 0) {  // gamma part = sum_{own j > k} conj(v_j) y_j, fixed order
       double gp = 0.0;
       for (int jl = jl0 + lane; jl < ncl; jl += 32) {
@@ -297,46 +308,59 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       if (lane == 0) misc[36] = g;
     }
     __syncthreads();
+    lap(11);
     // rank-2 update of own columns j > k, rows i > k with w = tau y - (|tau|^2 gamma / 2) v:
     // B_ij -= v_i conj(w_j) + w_i conj(v_j)
     {
       const double c = 0.5 * N::abs2(tau) * misc[36];
       const int m = n - k - 1;
       const int ncol = ncl - jl0;
-      const long long tot = (long long)ncol * m;
-      constexpr int U = 4;  // elements per thread per batch: loads issued before any store
-      for (long long x0 = tid; x0 < tot; x0 += (long long)U * nt) {
-        T* ap[U];
-        T av[U], vi[U], wi[U], vj[U], wj[U];
+      const int tot = ncol * m;  // <= n^2: fits an int
+      if (SMEM || CPLX || n <= 256) {
+        for (int x = tid; x < tot; x += nt) {
+          const int q = x / m;
+          const int jl = jl0 + q, i = k + 1 + (x - q * m);
+          const int j = jl * CS + r;
+          if (j >= n) continue;
+          const T vi = vloc[i], vj = vloc[j];
+          const T wi = N::sub(N::mul(tau, yall[i]), N::scale(vi, c));
+          const T wj = N::sub(N::mul(tau, yall[j]), N::scale(vj, c));
+          T* a = slab + (size_t)jl * ld + i;
+          *a = N::sub(N::sub(*a, N::mul(vi, N::conj(wj))), N::mul(wi, N::conj(vj)));
+        }
+      } else {  // large real Grams in an L2-resident slab: 4 loads in flight before the stores
+        constexpr int U = 4;
+        for (int x0 = tid; x0 < tot; x0 += U * nt) {
+          int ii[U], jj[U];
+          T av[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const long long x = x0 + (long long)u * nt;
-          ap[u] = nullptr;
-          if (x < tot) {
-            const int jl = jl0 + static_cast<int>(x / m);
-            const int i = k + 1 + static_cast<int>(x % m);
-            const int j = jl * CS + r;
-            if (j < n) {
-              ap[u] = slab + (size_t)jl * ld + i;
-              vi[u] = vloc[i];
-              vj[u] = vloc[j];
-              wi[u] = N::sub(N::mul(tau, yall[i]), N::scale(vi[u], c));
-              wj[u] = N::sub(N::mul(tau, yall[j]), N::scale(vj[u], c));
+          for (int u = 0; u < U; ++u) {
+            const int x = x0 + u * nt;
+            jj[u] = -1;
+            if (x < tot) {
+              const int q = x / m;
+              const int jl = jl0 + q;
+              ii[u] = k + 1 + (x - q * m);
+              if (jl * CS + r < n) jj[u] = jl;
             }
           }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (jj[u] >= 0) av[u] = slab[(size_t)jj[u] * ld + ii[u]];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (jj[u] >= 0) {
+              const int i = ii[u], j = jj[u] * CS + r;
+              const T vi = vloc[i], vj = vloc[j];
+              const T wi = N::sub(N::mul(tau, yall[i]), N::scale(vi, c));
+              const T wj = N::sub(N::mul(tau, yall[j]), N::scale(vj, c));
+              slab[(size_t)jj[u] * ld + i] = N::sub(N::sub(av[u], N::mul(vi, N::conj(wj))), N::mul(wi, N::conj(vj)));
+            }
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (ap[u]) av[u] = *ap[u];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (ap[u]) {
-            T v = N::sub(av[u], N::mul(vi[u], N::conj(wj[u])));
-            *ap[u] = N::sub(v, N::mul(wi[u], N::conj(vj[u])));
-          }
       }
     }
     __syncthreads();
+    lap(12);
   }
   {  // last diagonal entry (owner of column n-1)
     const int o = (n - 1) % CS;
@@ -484,25 +508,35 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       for (int il = tid - 32; il < nrl; il += nt - 32) {
         double* __restrict__ zc0 = Z + il;
         double carry = zc0[(size_t)mm * nrl];
-        // the next z values are loaded ahead of the stores (no store-to-load serialisation
-        // when Z lives in a global slab)
-        double nxt[4];
+        if (SMEM) {
+          for (int t = 0; t < cnt; ++t) {
+            const int i = mm - 1 - t;
+            const double zi = zc0[(size_t)i * nrl];
+            const double c = rc[t], s = rs[t];
+            zc0[(size_t)(i + 1) * nrl] = fma(s, zi, c * carry);
+            carry = fma(c, zi, -s * carry);
+          }
+        } else {
+          // global slab: the next z values are loaded ahead of the stores (no store-to-load
+          // serialisation through L2)
+          double nxt[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) nxt[u] = (u < cnt) ? zc0[(size_t)(mm - 1 - u) * nrl] : 0.0;
-        for (int t = 0; t < cnt; t += 4) {
-          double cur[4];
+          for (int u = 0; u < 4; ++u) nxt[u] = (u < cnt) ? zc0[(size_t)(mm - 1 - u) * nrl] : 0.0;
+          for (int t = 0; t < cnt; t += 4) {
+            double cur[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+            for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) nxt[u] = (t + 4 + u < cnt) ? zc0[(size_t)(mm - 5 - t - u) * nrl] : 0.0;
+            for (int u = 0; u < 4; ++u) nxt[u] = (t + 4 + u < cnt) ? zc0[(size_t)(mm - 5 - t - u) * nrl] : 0.0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (t + u < cnt) {
-              const int i = mm - 1 - t - u;
-              const double c = rc[t + u], s = rs[t + u];
-              zc0[(size_t)(i + 1) * nrl] = fma(s, cur[u], c * carry);
-              carry = fma(c, cur[u], -s * carry);
-            }
+            for (int u = 0; u < 4; ++u)
+              if (t + u < cnt) {
+                const int i = mm - 1 - t - u;
+                const double c = rc[t + u], s = rs[t + u];
+                zc0[(size_t)(i + 1) * nrl] = fma(s, cur[u], c * carry);
+                carry = fma(c, cur[u], -s * carry);
+              }
+          }
         }
         if (cnt > 0) zc0[(size_t)(mm - cnt) * nrl] = carry;
       }

@@ -28,6 +28,11 @@ struct SegGroup {
   const int* ptr;      // CSR over outputs, or nullptr: exactly one entry per output
   const int* li;       // entry (or per-output, if ptr==nullptr) left index; nullptr = output index
   const int* ri;
+  // chunked operand storage (the merged 2x2 blocks of the largest configurations): matrix l
+  // lives at Lch[l >> Lsh] + Ls * (l & (2^Lsh - 1)) instead of L + Ls * l (nullptr: contiguous)
+  const double* const* Lch;
+  const double* const* Rch;
+  int Lsh, Rsh;
 };
 
 constexpr int kMaxGroups = 4;
@@ -47,16 +52,26 @@ struct SegParams {
   // q = oquad[t] & 3 at row offset (q >> 1) * qm and column offset (q & 1) * qn
   const int* oquad;
   int qm, qn;
+  // chunked output storage (see SegGroup::Lch): output block b at och[b >> osh] + Os * (b & mask)
+  double* const* och;
+  int osh;
   SegGroup g[kMaxGroups];
 };
 
-__device__ __forceinline__ long long seg_out_offset(const SegParams& p, int t) {
+// address of output t's block (W = scalars per element)
+__device__ __forceinline__ double* seg_out_ptr(const SegParams& p, int t, int W) {
+  long long blk, extra = 0;
   if (p.oquad) {
     const int v = p.oquad[t];
     const int q = v & 3;
-    return p.Os * (v >> 2) + p.Ooff + (q >> 1) * p.qm + (long long)((q & 1) * p.qn) * p.Old;
+    blk = v >> 2;
+    extra = (q >> 1) * p.qm + (long long)((q & 1) * p.qn) * p.Old;
+  } else {
+    blk = p.omap ? p.omap[t] : t;
   }
-  return p.Os * (p.omap ? p.omap[t] : t) + p.Ooff;
+  if (p.och)
+    return p.och[blk >> p.osh] + (p.Os * (blk & ((1LL << p.osh) - 1)) + p.Ooff + extra) * W;
+  return p.out + (p.Os * blk + p.Ooff + extra) * W;
 }
 
 // ---------------------------------------------------------------------------
@@ -247,8 +262,10 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
       l = G.li ? G.li[t] : t;
       r = G.ri ? G.ri[t] : t;
     }
-    const double* Lp = G.L + (G.Ls * l + G.Loff) * W;
-    const double* Rp = G.R + (G.Rs * r + G.Roff) * W;
+    const double* Lp = G.Lch ? G.Lch[l >> G.Lsh] + (G.Ls * (l & ((1 << G.Lsh) - 1)) + G.Loff) * W
+                             : G.L + (G.Ls * l + G.Loff) * W;
+    const double* Rp = G.Rch ? G.Rch[r >> G.Rsh] + (G.Rs * (r & ((1 << G.Rsh) - 1)) + G.Roff) * W
+                             : G.R + (G.Rs * r + G.Roff) * W;
 #pragma unroll
     for (int j = 0; j < LPT; ++j) lsrc[j] = Lp + (long long)loff[j] * W;
 #pragma unroll
@@ -391,7 +408,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
   }
   cp_async_wait<0>();
 
-  double* Op = p.out + seg_out_offset(p, t) * W;
+  double* Op = seg_out_ptr(p, t, W);
 #pragma unroll
   for (int i = 0; i < C::FM; ++i)
 #pragma unroll
@@ -605,11 +622,14 @@ __global__ void pack_basis_kernel(const double* vec, int n, double* out, int row
 // ---------------------------------------------------------------------------
 // copy compact R x C blocks cp[e] into quadrant oquad[e] & 3 of the 2R x 2C block
 // oquad[e] >> 2 of `out` (the parents' merged blocks, mmp.cpp:344-365)
-__global__ void scatter_quad_kernel(double* out, const double* cp, const int* oquad, int R, int Cc, int W) {
+__global__ void scatter_quad_kernel(double* const* och, int osh, const double* cp, const int* oquad, int R, int Cc,
+                                    int W) {
   const int e = blockIdx.x;
   const int v = oquad[e];
   const int q = v & 3;
-  double* o = out + ((size_t)4 * R * Cc * (v >> 2) + (q >> 1) * R + (size_t)(q & 1) * Cc * 2 * R) * W;
+  const long long blk = v >> 2;
+  double* o = och[blk >> osh] + ((size_t)4 * R * Cc * (blk & ((1LL << osh) - 1)) + (q >> 1) * R +
+                                 (size_t)(q & 1) * Cc * 2 * R) * W;
   const double* c = cp + (size_t)e * R * Cc * W;
   for (int x = threadIdx.x; x < R * Cc * W; x += blockDim.x) {
     const int el = x / W, w = x % W;

@@ -97,8 +97,8 @@ int main(int argc, char** argv) {
   if (!smem) CK(cudaMalloc(&dSlab, size_t(count) * CS * L.ncl * L.ld * W * 8));
   const int nt = argc > 5 ? std::atoi(argv[5]) : (n <= 64 ? 128 : (n <= 192 ? 256 : 512));
   long long* dProf;
-  CK(cudaMalloc(&dProf, 8 * sizeof(long long)));
-  CK(cudaMemset(dProf, 0, 8 * sizeof(long long)));
+  CK(cudaMalloc(&dProf, 16 * sizeof(long long)));
+  CK(cudaMemset(dProf, 0, 16 * sizeof(long long)));
   HeevParams hp{dG, dV, dZ, dSlab, dVec, dVal, dRank, dDeg, dFail, dProf, argc > 8 ? std::atoi(argv[8]) : 0, n, eps};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(count) * CS);
@@ -125,10 +125,12 @@ int main(int argc, char** argv) {
   launch();
   CK(cudaDeviceSynchronize());
   {
-    long long pr[8];
+    long long pr[16];
     CK(cudaMemcpy(pr, dProf, sizeof(pr), cudaMemcpyDeviceToHost));
     std::printf("  block0 cycles: load+tridiag %lld  QL %lld  rank %lld  back %lld  sweeps %lld rotations %lld\n",
                 pr[1] - pr[0], pr[2] - pr[1], pr[3] - pr[2], pr[4] - pr[3], pr[5], pr[6]);
+    std::printf("  tridiag steps: householder %lld  sync1+v %lld  y %lld  gamma+sync2+gather %lld  rank2 %lld\n",
+                pr[8], pr[9], pr[10], pr[11], pr[12]);
   }
   hp.prof = nullptr;
   cudaEvent_t e0, e1;
