@@ -377,6 +377,7 @@ struct DevLevel {
   const int *near_row = nullptr, *near_col = nullptr, *adm_row = nullptr, *adm_col = nullptr;
   const int *nearb = nullptr, *adm = nullptr, *merged_row = nullptr, *merged_quad = nullptr;
   const int *sub_child = nullptr, *nl_col = nullptr;
+  const int* subq[4] = {};  // per quadrant q = 2*ri + ci: sub_child[4 t + q] (child block index)
   const int* pend_mq = nullptr;  // pending target -> 4 * merged idx (level-1) + quadrant
   struct MZ {
     const int *row = nullptr, *col = nullptr, *m = nullptr, *out = nullptr;
@@ -393,6 +394,7 @@ struct DevPlan {
   std::vector<DevLevel> lv;
   const int* even = nullptr;  // p -> 2p
   const int* odd = nullptr;   // p -> 2p+1
+  const int* iota = nullptr;  // e -> e (block indices of chunked outputs written densely)
   DVec<int32_t> blob;
 };
 
@@ -464,6 +466,11 @@ static std::unique_ptr<DevPlan> upload_plan(const Plan& P, cudaStream_t s) {
     put_mz(Q.mz_adm, L.mz_adm);
     put_mz(Q.mz_pend, L.mz_pend);
     put(&Q.sub_child, L.sub_child);
+    for (int q = 0; q < 4; ++q) {
+      std::vector<int32_t> v(L.sub_child.size() / 4);
+      for (size_t t = 0; t < v.size(); ++t) v[t] = L.sub_child[4 * t + q];
+      put(&Q.subq[q], v);
+    }
     put(&Q.nl_col, nlc);
     {
       Csr ar, nr;
@@ -527,6 +534,11 @@ static std::unique_ptr<DevPlan> upload_plan(const Plan& P, cudaStream_t s) {
   }
   put(&D->even, ev);
   put(&D->odd, od);
+  size_t maxz = 1;
+  for (int l = 0; l <= P.depth; ++l) maxz = std::max(maxz, P.lv[l].mz_pend.m.size());
+  std::vector<int32_t> io(maxz);
+  for (size_t e = 0; e < maxz; ++e) io[e] = static_cast<int32_t>(e);
+  put(&D->iota, io);
   D->blob.upload(blob, s);
   for (auto& [dst, off] : fix) *dst = D->blob.p + off;
   return D;
@@ -1328,6 +1340,8 @@ struct EngineRun : Relief {
     return t;
   }
 
+  // the upper levels' row and column truncations run concurrently (side stream 1 + main)
+  bool paired_solves = false;
   // H2B_EIG_LIBRARY=1: cuSOLVER XsyevBatched instead of heev_kernel (A/B runs)
   const bool use_library = std::getenv("H2B_EIG_LIBRARY") != nullptr;
 
@@ -1354,7 +1368,9 @@ struct EngineRun : Relief {
       CS = 16;
       smem = false;
     }
-    const bool many = count >= 64 || (count >= 32 && n <= 400);
+    // the row and column solves of a level run concurrently: size the decision on both
+    const int eff = paired_solves ? 2 * count : count;
+    const bool many = eff >= 64 || (eff >= 32 && n <= 400);
     if (n > 96 && many) {
       CS = 1;
       smem = false;
@@ -1587,16 +1603,6 @@ struct EngineRun : Relief {
     launches++;
   }
 
-  void gather(DBuf& out, int count, const double* src, long long Ss, int R, int Cc, const int* idx) {
-    out.alloc(sz(count, 2 * R, 2 * Cc), s);
-    if (count <= 0) return;
-    pre("gather_quad", 0, 2LL * count * 4 * R * Cc * 8 * W);
-    gather_quad_kernel<<<count, 256, 0, s>>>(out, src, Ss, R, Cc, idx, nullptr, W);
-    CK(cudaGetLastError());
-    post();
-    launches++;
-  }
-
   void copy_dev(DBuf& dst, const DBuf& src) {
     dst.alloc(src.n, s);
     CK(cudaMemcpyAsync(dst.p, src.p, src.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -1703,13 +1709,13 @@ struct EngineRun : Relief {
   // mz_pend), which scatter_pending() later copies into the parent's merged quadrants —
   // so the merged blocks of this level are freed before the parent's are allocated
   // (at the 64^3 grid, configs[3], the two would not fit next to each other).
-  void merged_into_targets(int l, const Chunked& M, bool pend, DBuf* CP) {
+  void merged_into_targets(int l, const Chunked& M, bool pend, Chunked* CP) {
     const DevLevel& Q = DP.lv[l];
     const int Kn = KCr[l + 1], Kq = KCc[l + 1], Kr = KCr[l], Kc = KCc[l];
     const long long MM = 4LL * Kn * Kq;
     const DevLevel::MZ& z = pend ? Q.mz_pend : Q.mz_adm;
     if (z.n == 0) return;
-    if (pend) CP->alloc(sz(z.n, Kr, Kc), s);
+    if (pend) CP->alloc(z.n, (long long)sz(1, Kr, Kc), s, false);
     const size_t per = sz(1, Kr, 2 * Kq) * sizeof(double);
     const int step = static_cast<int>(std::max<size_t>(4096, chunk_bytes() / per));
     for (int e0 = 0; e0 < z.n; e0 += step) {
@@ -1720,16 +1726,20 @@ struct EngineRun : Relief {
                 z.m + e0}});
       const Grp g{ref(Zc, 2LL * Kr * Kq, Kr, OP_N), ref(Tc[l], 2LL * Kq * Kc, 2 * Kq, OP_C), 2 * Kq, nullptr, nullptr,
                   z.col + e0};
-      if (pend) seg(CP->p, (long long)Kr * Kc, (long long)e0 * Kr * Kc, Kr, nullptr, Kr, Kc, cnt, false, {g});
+      if (pend) {
+        ochunk = CP;
+        seg(nullptr, (long long)Kr * Kc, 0, Kr, DP.iota + e0, Kr, Kc, cnt, false, {g});
+      }
       else seg(Tg[l], (long long)Kr * Kc, 0, Kr, z.out + e0, Kr, Kc, cnt, false, {g});
     }
   }
   // the compact pending case-1 values into their quadrants of the parent's merged blocks
-  void scatter_pending(int l, const DBuf& CP) {
+  void scatter_pending(int l, const Chunked& CP) {
     const DevLevel::MZ& z = DP.lv[l].mz_pend;
     if (z.n == 0) return;
     pre("scatter_quad", 0, 2LL * z.n * KCr[l] * KCc[l] * 8 * W);
-    scatter_quad_kernel<<<z.n, 256, 0, s>>>(Mg[l - 1].table.p, Mg[l - 1].shift, CP, z.out, KCr[l], KCc[l], W);
+    scatter_quad_kernel<<<z.n, 256, 0, s>>>(Mg[l - 1].table.p, Mg[l - 1].shift, CP.table.p, CP.shift, z.out,
+                                            KCr[l], KCc[l], W);
     CK(cudaGetLastError());
     post();
     launches++;
@@ -2034,26 +2044,29 @@ struct EngineRun : Relief {
 
     mark("L" + std::to_string(l) + ".assemble");
     // merged children couplings and assembled collected blocks (mmp.cpp:344-404)
-    DBuf Aa, Ab;
     Chunked Mg = std::move(this->Mg[l]);  // filled by level l+1's pending targets
     (void)Lc;
     (void)nm;
-    gather(Aa, ns, LA[l + 1], (long long)Kn * KBr1, Kn, KBr1, Q.sub_child);
-    gather(Ab, ns, RB[l + 1], (long long)KAc1 * Kq, KAc1, Kq, Q.sub_child);
+    // X = asm_a T^B_row (row Gram term 2, collect); Xc = asm_b^T T^A_col.  The 2x2 assembled
+    // blocks asm_a / asm_b are never formed: each half of X sums its two quadrant products
+    // straight from the children's collects, X rows ri = sum_ci LA[child (ri,ci)] T^B[rows ci]
+    // (Xc rows ci = sum_ri RB[child (ri,ci)]^T T^A_col[rows ri]).
+    DBuf X(sz(ns, 2 * Kn, KBr), s), Xc(sz(ns, 2 * Kq, KAc), s);
+    for (int h = 0; h < 2; ++h) {
+      seg(X, 2LL * Kn * KBr, (long long)h * Kn, 2 * Kn, nullptr, Kn, KBr, ns, false,
+          {Grp{ref(LA[l + 1], (long long)Kn * KBr1, Kn, OP_N), ref(B.Tr[l], 2LL * KBr1 * KBr, 2 * KBr1, OP_N), KBr1,
+               nullptr, Q.subq[2 * h + 0], Q.near_col},
+           Grp{ref(LA[l + 1], (long long)Kn * KBr1, Kn, OP_N), ref(B.Tr[l], 2LL * KBr1 * KBr, 2 * KBr1, OP_N, KBr1),
+               KBr1, nullptr, Q.subq[2 * h + 1], Q.near_col}});
+      seg(Xc, 2LL * Kq * KAc, (long long)h * Kq, 2 * Kq, nullptr, Kq, KAc, ns, false,
+          {Grp{ref(RB[l + 1], (long long)KAc1 * Kq, KAc1, OP_T), ref(A.Tc[l], 2LL * KAc1 * KAc, 2 * KAc1, OP_N), KAc1,
+               nullptr, Q.subq[0 + h], Q.near_row},
+           Grp{ref(RB[l + 1], (long long)KAc1 * Kq, KAc1, OP_T),
+               ref(A.Tc[l], 2LL * KAc1 * KAc, 2 * KAc1, OP_N, KAc1), KAc1, nullptr, Q.subq[2 + h], Q.near_row}});
+    }
     // still read by level l+1's deferred targets: released after the join
     retire(std::move(LA[l + 1]));
     retire(std::move(RB[l + 1]));
-
-    // X = asm_a T^B_row (row Gram term 2, collect); Xc = asm_b^T T^A_col
-    DBuf X(sz(ns, 2 * Kn, KBr), s), Xc(sz(ns, 2 * Kq, KAc), s);
-    segd(X, 2 * Kn, KBr, ns,
-         {Grp{ref(Aa, 4LL * Kn * KBr1, 2 * Kn, OP_N), ref(B.Tr[l], 2LL * KBr1 * KBr, 2 * KBr1, OP_N), 2 * KBr1,
-              nullptr, nullptr, Q.near_col}});
-    segd(Xc, 2 * Kq, KAc, ns,
-         {Grp{ref(Ab, 4LL * KAc1 * Kq, 2 * KAc1, OP_T), ref(A.Tc[l], 2LL * KAc1 * KAc, 2 * KAc1, OP_N), 2 * KAc1,
-              nullptr, nullptr, Q.near_row}});
-    Aa.release();
-    Ab.release();
 
     if (adaptive) {
       mark("L" + std::to_string(l) + ".grams");
@@ -2087,6 +2100,7 @@ struct EngineRun : Relief {
       segh(g3, 2 * Kn, n,
            {Grp{ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_N), ref(X3, 2LL * Kn * KAr, 2 * Kn, OP_H), KAr, nullptr, nullptr,
                 nullptr}});
+      paired_solves = true;
       Trunc tr = truncate(g1, g2, g3, n, 2 * Kn, A.dgr_d[l], /*defer=*/true);
       std::exception_ptr row_err;
       EigWork row_wk;
@@ -2109,6 +2123,7 @@ struct EngineRun : Relief {
         throw;
       }
       finish_async(row_th, row_err, tr, row_wk);
+      paired_solves = false;
       KCr[l] = fetch_ranks(tr, n, rcr[l]);
       KCc[l] = fetch_ranks(tc, n, rcc[l]);
       pack(tr, n, 2 * Kn, Tr[l], 2 * Kn, KCr[l]);
@@ -2155,7 +2170,7 @@ struct EngineRun : Relief {
     mark("L" + std::to_string(l) + ".targets");
     // case 1 over merged children couplings first (mmp.cpp:573-585), then the
     // triple sums of cases 2-4 accumulate onto the same stores
-    DBuf CP;
+    Chunked CP;
     merged_into_targets(l, Mg, true, &CP);  // pending targets: compact, while only Mg[l] is live
     alloc_tg(l, true);
     merged_into_targets(l, Mg, false, nullptr);

@@ -315,20 +315,28 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
       const double c = 0.5 * N::abs2(tau) * misc[36];
       const int m = n - k - 1;
       const int ncol = ncl - jl0;
-      const int tot = ncol * m;  // <= n^2: fits an int
+      // w = tau y - c v for every row i > k, once (in place of the gathered y)
+      for (int i = k + 1 + tid; i < n; i += nt) yall[i] = N::sub(N::mul(tau, yall[i]), N::scale(vloc[i], c));
+      __syncthreads();
+      const T* w = yall;
       if (SMEM || CPLX || n <= 256) {
-        for (int x = tid; x < tot; x += nt) {
-          const int q = x / m;
-          const int jl = jl0 + q, i = k + 1 + (x - q * m);
-          const int j = jl * CS + r;
-          if (j >= n) continue;
-          const T vi = vloc[i], vj = vloc[j];
-          const T wi = N::sub(N::mul(tau, yall[i]), N::scale(vi, c));
-          const T wj = N::sub(N::mul(tau, yall[j]), N::scale(vj, c));
-          T* a = slab + (size_t)jl * ld + i;
-          *a = N::sub(N::sub(*a, N::mul(vi, N::conj(wj))), N::mul(wi, N::conj(vj)));
-        }
+        // a thread owns a row i (v_i, w_i in registers) and a strided subset of the own columns;
+        // v_j, w_j are warp-uniform broadcasts
+        const int rp = m < nt ? m : nt;  // rows per pass
+        const int groups = nt / rp;
+        const int g = tid / rp;
+        if (g < groups)
+          for (int i = k + 1 + tid % rp; i < n; i += rp) {
+            const T vi = vloc[i], wi = w[i];
+            for (int jl = jl0 + g; jl < ncl; jl += groups) {
+              const int j = jl * CS + r;
+              if (j >= n) break;
+              T* a = slab + (size_t)jl * ld + i;
+              *a = N::sub(N::sub(*a, N::mul(vi, N::conj(w[j]))), N::mul(wi, N::conj(vloc[j])));
+            }
+          }
       } else {  // large real Grams in an L2-resident slab: 4 loads in flight before the stores
+        const int tot = ncol * m;  // <= n^2: fits an int
         constexpr int U = 4;
         for (int x0 = tid; x0 < tot; x0 += U * nt) {
           int ii[U], jj[U];
@@ -351,10 +359,8 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
           for (int u = 0; u < U; ++u)
             if (jj[u] >= 0) {
               const int i = ii[u], j = jj[u] * CS + r;
-              const T vi = vloc[i], vj = vloc[j];
-              const T wi = N::sub(N::mul(tau, yall[i]), N::scale(vi, c));
-              const T wj = N::sub(N::mul(tau, yall[j]), N::scale(vj, c));
-              slab[(size_t)jj[u] * ld + i] = N::sub(N::sub(av[u], N::mul(vi, N::conj(wj))), N::mul(wi, N::conj(vj)));
+              slab[(size_t)jj[u] * ld + i] =
+                  N::sub(N::sub(av[u], N::mul(vloc[i], N::conj(w[j]))), N::mul(w[i], N::conj(vloc[j])));
             }
         }
       }

@@ -622,36 +622,19 @@ __global__ void pack_basis_kernel(const double* vec, int n, double* out, int row
 // ---------------------------------------------------------------------------
 // copy compact R x C blocks cp[e] into quadrant oquad[e] & 3 of the 2R x 2C block
 // oquad[e] >> 2 of `out` (the parents' merged blocks, mmp.cpp:344-365)
-__global__ void scatter_quad_kernel(double* const* och, int osh, const double* cp, const int* oquad, int R, int Cc,
-                                    int W) {
+__global__ void scatter_quad_kernel(double* const* och, int osh, const double* const* cpch, int cpsh,
+                                    const int* oquad, int R, int Cc, int W) {
   const int e = blockIdx.x;
   const int v = oquad[e];
   const int q = v & 3;
   const long long blk = v >> 2;
   double* o = och[blk >> osh] + ((size_t)4 * R * Cc * (blk & ((1LL << osh) - 1)) + (q >> 1) * R +
                                  (size_t)(q & 1) * Cc * 2 * R) * W;
-  const double* c = cp + (size_t)e * R * Cc * W;
+  const double* c = cpch[e >> cpsh] + (size_t)(e & ((1 << cpsh) - 1)) * R * Cc * W;
   for (int x = threadIdx.x; x < R * Cc * W; x += blockDim.x) {
     const int el = x / W, w = x % W;
     const int r = el % R, col = el / R;
     o[((size_t)r + (size_t)col * 2 * R) * W + w] = c[x];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// gather 2x2 quadrants into a dense (2R x 2C) matrix; idx[4*t+q] (q = 2*ri+ci)
-__global__ void gather_quad_kernel(double* out, const double* src, long long Ss, int R, int Cc,
-                                   const int* idx, const int* remap, int W) {
-  const int t = blockIdx.x;
-  const int ld = 2 * R;
-  double* o = out + (size_t)t * 4 * R * Cc * W;
-  for (int x = threadIdx.x; x < 4 * R * Cc * W; x += blockDim.x) {
-    const int e = x / W, w = x % W;
-    const int row = e % ld, col = e / ld;
-    const int q = 2 * (row / R) + (col / Cc);
-    int s = idx[4 * t + q];
-    if (s >= 0 && remap) s = remap[s];
-    o[x] = s < 0 ? 0.0 : src[(Ss * s + (row % R) + (size_t)(col % Cc) * R) * W + w];
   }
 }
 
