@@ -2,6 +2,11 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <mutex>
+#include <exception>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <chrono>
 #include <stdexcept>
@@ -24,16 +29,25 @@ void parallel_for(int n, int threads, F&& f) {
     return;
   }
   std::atomic<int> next{0};
+  std::exception_ptr err;
+  std::mutex em;
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t)
     pool.emplace_back([&] {
-      for (;;) {
-        const int i = next.fetch_add(1);
-        if (i >= n) break;
-        f(i);
+      try {
+        for (;;) {
+          const int i = next.fetch_add(1);
+          if (i >= n) break;
+          f(i);
+        }
+      } catch (...) {  // rethrown on the calling thread (structure errors -> C-ABI error codes)
+        std::lock_guard<std::mutex> g(em);
+        if (!err) err = std::current_exception();
+        next = n;
       }
     });
   for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
 }
 
 enum Status : uint8_t { kFullTarget = 0, kAdmTarget = 1, kSubTarget = 2, kInside = 3 };
@@ -97,6 +111,11 @@ struct Builder {
     owner.push_back(o);
     csr.li.push_back(l);
     csr.ri.push_back(r);
+  }
+  void append(const Builder& b) {
+    owner.insert(owner.end(), b.owner.begin(), b.owner.end());
+    csr.li.insert(csr.li.end(), b.csr.li.begin(), b.csr.li.end());
+    csr.ri.insert(csr.ri.end(), b.csr.ri.begin(), b.csr.ri.end());
   }
   Csr done(int n_out) {
     finish_csr(csr, n_out, owner);
@@ -189,6 +208,13 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
     for (int b = 0; b < nb; ++b) L.col_blk[fill[L.bcol[b]]++] = b;  // rows ascending within a column
   }
 
+  const bool trace = std::getenv("H2B_PLAN_TRACE") != nullptr;
+  auto stamp = [&](const char* what) {
+    if (trace)
+      std::fprintf(stderr, "[plan] %-28s %.3f s\n", what,
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  };
+  stamp("levels + blocks");
   // ---- pass 1 (bottom-up): triples per level, pending and merged sets
   std::vector<std::vector<RowTriples>> rows(D + 1);
   std::vector<std::vector<std::pair<int, int>>> pend(D + 1);  // (row, col) pending pairs
@@ -210,27 +236,37 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
         return x.k < y.k || (x.k == y.k && x.j < y.j);
       });
     });
-    // case counters (mmp.cpp:307-308, 594-595)
-    for (int i = 0; i < L.n; ++i)
+    // case counters (mmp.cpp:307-308, 594-595), per row in parallel
+    std::vector<std::array<int64_t, 4>> cc(L.n);
+    parallel_for(L.n, threads, [&](int i) {
+      cc[i] = {0, 0, 0, 0};
       for (const Triple& t : rows[l][i].t) {
         const bool fa = L.bkind[t.a] != kAdm, fb = L.bkind[t.b] != kAdm;
-        const int c = leaf ? (fa ? (fb ? 0 : 1) : (fb ? 2 : 3)) : (fa ? 1 : (fb ? 2 : 3));
-        L.case_products[c]++;
-        P.total_triples++;
+        cc[i][leaf ? (fa ? (fb ? 0 : 1) : (fb ? 2 : 3)) : (fa ? 1 : (fb ? 2 : 3))]++;
       }
-    // pending candidates from triples
-    std::vector<std::pair<int, int>> cand;
-    for (int i = 0; i < L.n; ++i) {
+    });
+    for (int i = 0; i < L.n; ++i)
+      for (int c = 0; c < 4; ++c) {
+        L.case_products[c] += cc[i][c];
+        P.total_triples += cc[i][c];
+      }
+    // pending candidates from triples (per row in parallel, concatenated in row order)
+    std::vector<std::vector<std::pair<int, int>>> cand_row(L.n);
+    std::atomic<bool> full_target{false};
+    parallel_for(L.n, threads, [&](int i) {
       int last = -1;
       for (const Triple& t : rows[l][i].t) {
         if (t.k == last) continue;
         last = t.k;
         const Status s = status_of(P.lv, l, i, t.k);
-        if (s == kInside) cand.push_back({i, t.k});
-        if (!leaf && s == kFullTarget)
-          throw InvariantError("mmp: coupling contribution aimed at a full block");
+        if (s == kInside) cand_row[i].push_back({i, t.k});
+        if (!leaf && s == kFullTarget) full_target = true;
       }
-    }
+    });
+    if (full_target) throw InvariantError("mmp: coupling contribution aimed at a full block");
+    std::vector<std::pair<int, int>> cand;
+    for (auto& v : cand_row) cand.insert(cand.end(), v.begin(), v.end());
+    cand_row.clear();
     // merged pairs of the children's pending couplings (mmp.cpp:344-365)
     if (!leaf) {
       const LevelPlan& C = P.lv[l + 1];
@@ -274,6 +310,7 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
   if (D > 0 && !pend[1].empty())
     throw InvariantError("mmp: pending couplings left after the bottom-up pass");
 
+  stamp("pass 1 (triples, pending)");
   // ---- pass 2 (top-down): which subdivided blocks hold NL couplings
   for (int l = 1; l < D; ++l) {
     LevelPlan& L = P.lv[l];
@@ -304,6 +341,7 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
   for (int l = 0; l <= D; ++l)
     if (P.lv[l].nl_of_block.empty()) P.lv[l].nl_of_block.assign(P.lv[l].brow.size(), -1);
 
+  stamp("pass 2 (NL blocks)");
   // ---- pass 3: CSRs with final target numbering
   for (int l = D; l >= 1 || (l == 0 && D == 0); --l) {
     LevelPlan& L = P.lv[l];
@@ -334,64 +372,85 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
       if (s == kSubTarget) return na + np + L.nl_of_block[find_block(L, i, k)];
       return -1;
     };
-    Builder ly, lyr, lyn, xr, ww, ff, fr, rf, rr, hq, hqc;
     const int nnear = static_cast<int>(L.nearb.size());
-    std::vector<std::vector<std::pair<int, int>>> hqc_rows;  // per B near: (i, A near)
-    if (leaf) hqc_rows.resize(nnear);
-    for (int i = 0; i < L.n; ++i) {
-      const auto& tr = rows[l][i].t;
-      size_t s0 = 0;
-      while (s0 < tr.size()) {
-        size_t s1 = s0;
-        while (s1 < tr.size() && tr[s1].k == tr[s0].k) ++s1;
-        const int k = tr[s0].k;
-        const Status st = status_of(P.lv, l, i, k);
-        if (st == kFullTarget) {
-          const int o = L.kidx[find_block(L, i, k)];
-          for (size_t e = s0; e < s1; ++e) {
-            const Triple& t = tr[e];
-            const bool fa = L.bkind[t.a] == kFull, fb = L.bkind[t.b] == kFull;
-            if (fa && fb) ff.add(o, L.kidx[t.a], L.kidx[t.b]);
-            else if (fa) fr.add(o, L.kidx[t.a], L.kidx[t.b]);
-            else if (fb) rf.add(o, L.kidx[t.a], L.kidx[t.b]);
-            else rr.add(o, L.kidx[t.a], L.kidx[t.b]);
-          }
-        } else {
-          const int o = slot_of(i, k, st);
-          for (size_t e = s0; e < s1; ++e) {
-            const Triple& t = tr[e];
-            const bool ra = L.bkind[t.a] == kAdm, rb = L.bkind[t.b] == kAdm;
-            if (rb) {
-              ly.add(o, t.a, L.kidx[t.b]);
-              if (ra) lyr.add(o, L.kidx[t.a], L.kidx[t.b]);
-              else lyn.add(o, t.a, L.kidx[t.b]);
+    // rows in T contiguous chunks with private builders, concatenated in chunk (= row) order:
+    // the entries of every output come from its own row, so the lists equal the serial ones
+    struct Part {
+      Builder ly, lyr, lyn, xr, ww, ff, fr, rf, rr, hq;
+      std::vector<std::array<int, 3>> hqc;  // (B near, i, A near)
+    };
+    const int T = std::max(1, std::min(threads, L.n));
+    std::vector<Part> parts(T);
+    parallel_for(T, T, [&](int pt) {
+      Part& Pt = parts[pt];
+      const int i0 = static_cast<int>(int64_t(L.n) * pt / T), i1 = static_cast<int>(int64_t(L.n) * (pt + 1) / T);
+      for (int i = i0; i < i1; ++i) {
+        const auto& tr = rows[l][i].t;
+        size_t s0 = 0;
+        while (s0 < tr.size()) {
+          size_t s1 = s0;
+          while (s1 < tr.size() && tr[s1].k == tr[s0].k) ++s1;
+          const int k = tr[s0].k;
+          const Status st = status_of(P.lv, l, i, k);
+          if (st == kFullTarget) {
+            const int o = L.kidx[find_block(L, i, k)];
+            for (size_t e = s0; e < s1; ++e) {
+              const Triple& t = tr[e];
+              const bool fa = L.bkind[t.a] == kFull, fb = L.bkind[t.b] == kFull;
+              if (fa && fb) Pt.ff.add(o, L.kidx[t.a], L.kidx[t.b]);
+              else if (fa) Pt.fr.add(o, L.kidx[t.a], L.kidx[t.b]);
+              else if (fb) Pt.rf.add(o, L.kidx[t.a], L.kidx[t.b]);
+              else Pt.rr.add(o, L.kidx[t.a], L.kidx[t.b]);
             }
-            else if (ra) xr.add(o, L.kidx[t.a], t.b);
-            else {  // full x full at the leaf level (NL x NL never reaches here)
-              ww.add(o, L.kidx[t.a], L.kidx[t.b]);
-              if (st == kAdmTarget || st == kInside) {
-                hq.add(L.kidx[t.a], L.kidx[t.b], 0);
-                hqc_rows[L.kidx[t.b]].push_back({i, L.kidx[t.a]});
+          } else {
+            const int o = slot_of(i, k, st);
+            for (size_t e = s0; e < s1; ++e) {
+              const Triple& t = tr[e];
+              const bool ra = L.bkind[t.a] == kAdm, rb = L.bkind[t.b] == kAdm;
+              if (rb) {
+                Pt.ly.add(o, t.a, L.kidx[t.b]);
+                if (ra) Pt.lyr.add(o, L.kidx[t.a], L.kidx[t.b]);
+                else Pt.lyn.add(o, t.a, L.kidx[t.b]);
+              }
+              else if (ra) Pt.xr.add(o, L.kidx[t.a], t.b);
+              else {  // full x full at the leaf level (NL x NL never reaches here)
+                Pt.ww.add(o, L.kidx[t.a], L.kidx[t.b]);
+                if (st == kAdmTarget || st == kInside) {
+                  Pt.hq.add(L.kidx[t.a], L.kidx[t.b], 0);
+                  Pt.hqc.push_back({L.kidx[t.b], i, L.kidx[t.a]});
+                }
               }
             }
           }
+          s0 = s1;
         }
-        s0 = s1;
       }
-    }
-    L.ly = ly.done(nt);
-    L.lyr = lyr.done(nt);
-    L.lyn = lyn.done(nt);
-    L.xr = xr.done(nt);
-    L.ww = ww.done(nt);
+    });
+    Builder hqc;
+    std::vector<std::vector<std::pair<int, int>>> hqc_rows;  // per B near: (i, A near)
     if (leaf) {
-      L.ff = ff.done(nnear);
-      L.fr = fr.done(nnear);
-      L.rf = rf.done(nnear);
-      L.rr = rr.done(nnear);
+      hqc_rows.resize(nnear);
+      for (Part& Pt : parts)
+        for (const auto& h : Pt.hqc) hqc_rows[h[0]].push_back({h[1], h[2]});
+    }
+    // the ten lists: concatenated in row order and counting-sorted by output, one per thread
+    Builder Part::*which[10] = {&Part::ly, &Part::lyr, &Part::lyn, &Part::xr, &Part::ww,
+                                &Part::ff, &Part::fr, &Part::rf, &Part::rr, &Part::hq};
+    Csr* dst[10] = {&L.ly, &L.lyr, &L.lyn, &L.xr, &L.ww, &L.ff, &L.fr, &L.rf, &L.rr, &L.hq};
+    const int nout[10] = {nt, nt, nt, nt, nt, nnear, nnear, nnear, nnear, nnear};
+    parallel_for(leaf ? 10 : 5, threads, [&](int w) {
+      Builder all;
+      for (Part& Pt : parts) {
+        all.append(Pt.*which[w]);
+        Pt.*which[w] = Builder{};
+      }
+      *dst[w] = all.done(nout[w]);
+    });
+    parts.clear();
+    if (trace && leaf) stamp("  leaf lists");
+    if (leaf) {
       // hq entries per A near block were added in (i, k asc, j asc) order:
       // per (i,j) the k's are ascending
-      L.hq = hq.done(nnear);
       for (int b = 0; b < nnear; ++b) {
         auto& v = hqc_rows[b];
         std::sort(v.begin(), v.end());
@@ -399,6 +458,7 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
       }
       L.hqc = hqc.done(nnear);
     }
+    if (trace && leaf) stamp("  leaf hqc");
     // per-cluster near blocks by row / column (block order)
     {
       Builder rn, cn;
@@ -463,8 +523,14 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
     }
     rows[l].clear();
     rows[l].shrink_to_fit();
+    if (trace) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "  level %d done", l);
+      stamp(buf);
+    }
     if (l == 0) break;
   }
+  stamp("pass 3 (CSRs)");
   P.build_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return P;
