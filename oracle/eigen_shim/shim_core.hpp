@@ -1,0 +1,756 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// A minimal, eagerly evaluated stand-in for the subset of the Eigen 3 API that
+// the reference's MMP path uses (proj/core/{include,src}: dense.hpp,
+// cluster_tree.cpp, block_tree.cpp, geometry.cpp, h2_matrix.cpp,
+// truncation.cpp, mmp.cpp, metrics.cpp).  Eigen itself is not in this image;
+// with this header tree on the include path (`-I oracle/eigen_shim`) the
+// reference's own, unmodified source files compile into oracle/_ref/ (recipe:
+// oracle/Makefile, target `ref`), so the restatement in oracle/ can be checked
+// against the reference's code run here.
+//
+// Design: no expression templates.  Matrix<S, R, C> owns column-major storage;
+// block expressions (block/topRows/segment/row/col/…) are strided views that
+// read through and, when taken from a mutable object, write through
+// (`m.block(..) += s`, `z.topRows(k).noalias() = …`).  Every other operation
+// evaluates immediately into a dynamic Matrix.  Products go to OpenBLAS (the
+// scipy wheel's, as in the oracle) so rounding matches the oracle's gemm;
+// SelfAdjointEigenSolver calls LAPACK ?syevd/?heevd (lower triangle, ascending
+// eigenvalues, like Eigen's).  Eigen's own tridiagonal QR produces other
+// eigenvector signs/rotations inside degenerate eigenspaces; every parity
+// check compares products, which those choices do not change.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstddef>
+#include <cstring>
+#include <initializer_list>
+#include <limits>
+#include <stdexcept>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+extern "C" {
+void scipy_cblas_dgemm(int order, int ta, int tb, int m, int n, int k, double alpha, const double* a, int lda,
+                       const double* b, int ldb, double beta, double* c, int ldc);
+void scipy_cblas_zgemm(int order, int ta, int tb, int m, int n, int k, const void* alpha, const void* a, int lda,
+                       const void* b, int ldb, const void* beta, void* c, int ldc);
+void scipy_dsyevd_(const char* jobz, const char* uplo, const int* n, double* a, const int* lda, double* w,
+                   double* work, const int* lwork, int* iwork, const int* liwork, int* info, size_t, size_t);
+void scipy_zheevd_(const char* jobz, const char* uplo, const int* n, void* a, const int* lda, double* w, void* work,
+                   const int* lwork, double* rwork, const int* lrwork, int* iwork, const int* liwork, int* info,
+                   size_t, size_t);
+}
+
+namespace Eigen {
+
+using Index = std::ptrdiff_t;
+inline constexpr int Dynamic = -1;
+enum ComputationInfo { Success = 0, NumericalIssue = 1, NoConvergence = 2, InvalidInput = 3 };
+enum DecompositionOptions { ComputeEigenvectors = 0x40, EigenvaluesOnly = 0x80 };
+
+namespace internal {
+template <class S>
+struct is_cplx : std::false_type {};
+template <class T>
+struct is_cplx<std::complex<T>> : std::true_type {};
+template <class S>
+struct real_of {
+  using type = S;
+};
+template <class T>
+struct real_of<std::complex<T>> {
+  using type = T;
+};
+template <class S>
+inline S conj(const S& x) {
+  if constexpr (is_cplx<S>::value)
+    return std::conj(x);
+  else
+    return x;
+}
+template <class S>
+inline double abs2(const S& x) {
+  if constexpr (is_cplx<S>::value)
+    return std::norm(x);
+  else
+    return static_cast<double>(x) * static_cast<double>(x);
+}
+}  // namespace internal
+
+template <class S, int R, int C>
+class Matrix;
+template <class P>
+class View;
+template <class T>
+class CommaInit;
+template <class S>
+struct ArrayOf;
+
+template <class S>
+using MatX = Matrix<S, Dynamic, Dynamic>;
+
+template <class D>
+struct traits;
+template <class S, int R, int C>
+struct traits<Matrix<S, R, C>> {
+  using Scalar = S;
+};
+template <class P>
+struct traits<View<P>> {
+  using Scalar = std::remove_cv_t<std::remove_pointer_t<P>>;
+};
+
+// comma initializer (`m << a, b, c`): fills row by row, like Eigen's
+template <class T>
+class CommaInit {
+ public:
+  template <class S>
+  CommaInit(T& t, const S& s) : t_(t) {
+    put(s);
+  }
+  template <class S>
+  CommaInit& operator,(const S& s) {
+    put(s);
+    return *this;
+  }
+
+ private:
+  template <class S>
+  void put(const S& s) {
+    t_.at(k_ / t_.cols(), k_ % t_.cols()) = s;
+    ++k_;
+  }
+  T& t_;
+  Index k_ = 0;
+};
+
+// coefficient-wise comparisons of .array() (only what the reference's tests use)
+template <class S>
+struct ArrayOf {
+  Matrix<S, Dynamic, Dynamic> m;
+  struct Bools {
+    std::vector<bool> b;
+    bool all() const { return std::all_of(b.begin(), b.end(), [](bool x) { return x; }); }
+    bool any() const { return std::any_of(b.begin(), b.end(), [](bool x) { return x; }); }
+  };
+  template <class F>
+  ArrayOf map(F f) const {
+    ArrayOf o{m};
+    for (Index k = 0; k < m.size(); ++k) o.m(k) = f(m(k));
+    return o;
+  }
+  template <class F>
+  Bools cmp(const ArrayOf& o, F f) const {
+    Bools r;
+    for (Index k = 0; k < m.size(); ++k) r.b.push_back(f(m(k), o.m(k)));
+    return r;
+  }
+  ArrayOf operator-(const S& s) const { return map([&](const S& x) { return x - s; }); }
+  ArrayOf operator+(const S& s) const { return map([&](const S& x) { return x + s; }); }
+  Bools operator>=(const ArrayOf& o) const { return cmp(o, [](const S& a, const S& b) { return a >= b; }); }
+  Bools operator<=(const ArrayOf& o) const { return cmp(o, [](const S& a, const S& b) { return a <= b; }); }
+  Bools operator>(const ArrayOf& o) const { return cmp(o, [](const S& a, const S& b) { return a > b; }); }
+  Bools operator<(const ArrayOf& o) const { return cmp(o, [](const S& a, const S& b) { return a < b; }); }
+};
+
+// ---------------------------------------------------------------------------
+// read-only interface shared by matrices and views (CRTP); D provides rows(),
+// cols(), ld() and ptr() (S* or const S*, column-major with leading dimension ld)
+template <class D>
+class DenseBase {
+ public:
+  using scalar_t = typename traits<D>::Scalar;
+  const D& derived() const { return static_cast<const D&>(*this); }
+  D& derived() { return static_cast<D&>(*this); }
+
+  Index size() const { return derived().rows() * derived().cols(); }
+  auto coeff(Index i, Index j) const { return derived().at(i, j); }
+
+  // ---- views --------------------------------------------------------------
+  auto block(Index i, Index j, Index r, Index c) const { return mkview(cptr() + i * is() + j * ld(), r, c); }
+  auto block(Index i, Index j, Index r, Index c) { return mkview(derived().ptr() + i * is() + j * ld(), r, c); }
+#define H2SHIM_VIEWS(CONSTQ, P)                                                                       \
+  auto topRows(Index n) CONSTQ { return mkview(P, n, cols()); }                                       \
+  auto bottomRows(Index n) CONSTQ { return mkview(P + (rows() - n) * is(), n, cols()); }             \
+  auto middleRows(Index i, Index n) CONSTQ { return mkview(P + i * is(), n, cols()); }               \
+  auto leftCols(Index n) CONSTQ { return mkview(P, rows(), n); }                                      \
+  auto rightCols(Index n) CONSTQ { return mkview(P + (cols() - n) * ld(), rows(), n); }              \
+  auto middleCols(Index j, Index n) CONSTQ { return mkview(P + j * ld(), rows(), n); }               \
+  auto topLeftCorner(Index r, Index c) CONSTQ { return mkview(P, r, c); }                             \
+  auto topRightCorner(Index r, Index c) CONSTQ { return mkview(P + (cols() - c) * ld(), r, c); }     \
+  auto bottomLeftCorner(Index r, Index c) CONSTQ { return mkview(P + (rows() - r) * is(), r, c); }   \
+  auto bottomRightCorner(Index r, Index c) CONSTQ {                                                   \
+    return mkview(P + (rows() - r) * is() + (cols() - c) * ld(), r, c);                              \
+  }                                                                                                   \
+  auto diagonal() CONSTQ {                                                                            \
+    using Q = std::remove_pointer_t<decltype(P)>;                                                     \
+    return View<Q*>(P, std::min(rows(), cols()), 1, ld(), is() + ld());                               \
+  }                                                                                                   \
+  auto col(Index j) CONSTQ { return mkview(P + j * ld(), rows(), 1); }                               \
+  auto row(Index i) CONSTQ { return mkview(P + i * is(), 1, cols()); }                               \
+  auto segment(Index i, Index n) CONSTQ { return vec_view(P, i, n); }                                 \
+  auto head(Index n) CONSTQ { return vec_view(P, 0, n); }                                             \
+  auto tail(Index n) CONSTQ { return vec_view(P, size() - n, n); }
+  H2SHIM_VIEWS(const, cptr())
+  H2SHIM_VIEWS(, derived().ptr())
+#undef H2SHIM_VIEWS
+
+  // ---- eager read-only operations -----------------------------------------
+  auto eval() const { return MatX<scalar_t>(derived()); }
+  auto transpose() const {
+    MatX<scalar_t> o(cols(), rows());
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) o(j, i) = coeff(i, j);
+    return o;
+  }
+  auto conjugate() const { return unary([](const scalar_t& x) { return internal::conj(x); }); }
+  auto adjoint() const {
+    MatX<scalar_t> o(cols(), rows());
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) o(j, i) = internal::conj(coeff(i, j));
+    return o;
+  }
+  auto real() const { return unary_r([](const scalar_t& x) { return std::real(x); }); }
+  auto imag() const { return unary_r([](const scalar_t& x) { return std::imag(x); }); }
+  auto cwiseAbs() const { return unary_r([](const scalar_t& x) { return std::abs(x); }); }
+  auto cwiseAbs2() const { return unary_r([](const scalar_t& x) { return internal::abs2(x); }); }
+  auto cwiseMax(const scalar_t& s) const { return unary([&](const scalar_t& x) { return std::max(x, s); }); }
+  auto cwiseMin(const scalar_t& s) const { return unary([&](const scalar_t& x) { return std::min(x, s); }); }
+  template <class E>
+  auto cwiseMax(const DenseBase<E>& o) const {
+    return binary(o, [](const scalar_t& a, const scalar_t& b) { return std::max(a, b); });
+  }
+  template <class E>
+  auto cwiseMin(const DenseBase<E>& o) const {
+    return binary(o, [](const scalar_t& a, const scalar_t& b) { return std::min(a, b); });
+  }
+  template <class E>
+  auto cwiseProduct(const DenseBase<E>& o) const {
+    return binary(o, [](const scalar_t& a, const scalar_t& b) { return a * b; });
+  }
+  scalar_t maxCoeff() const {
+    scalar_t m = coeff(0, 0);
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) m = std::max(m, coeff(i, j));
+    return m;
+  }
+  scalar_t minCoeff() const {
+    scalar_t m = coeff(0, 0);
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) m = std::min(m, coeff(i, j));
+    return m;
+  }
+  scalar_t sum() const {
+    scalar_t s(0);
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) s += coeff(i, j);
+    return s;
+  }
+  scalar_t trace() const {
+    scalar_t s(0);
+    for (Index i = 0; i < std::min(rows(), cols()); ++i) s += coeff(i, i);
+    return s;
+  }
+  double squaredNorm() const {
+    double s = 0.0;
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) s += internal::abs2(coeff(i, j));
+    return s;
+  }
+  double norm() const { return std::sqrt(squaredNorm()); }
+  bool isZero(double prec = 1e-12) const {
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i)
+        if (std::abs(coeff(i, j)) > prec) return false;
+    return true;
+  }
+  bool allFinite() const {
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i)
+        if (!std::isfinite(std::real(coeff(i, j))) || !std::isfinite(std::imag(coeff(i, j)))) return false;
+    return true;
+  }
+  template <class E>
+  bool isApprox(const DenseBase<E>& o, double prec = 1e-12) const {
+    double d = 0.0;
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) d += internal::abs2(coeff(i, j) - o.coeff(i, j));
+    return std::sqrt(d) <= prec * std::min(norm(), o.norm());
+  }
+  auto array() const { return ArrayOf<scalar_t>{MatX<scalar_t>(derived())}; }
+  struct FullPivLU {
+    MatX<scalar_t> m;
+    // rank with Eigen's default threshold: |pivot| > eps * min(rows, cols) * |max pivot|
+    Index rank() const {
+      MatX<scalar_t> a = m;
+      const Index r = a.rows(), c = a.cols(), n = std::min(r, c);
+      double maxpiv = 0.0;
+      Index rk = 0;
+      for (Index k = 0; k < n; ++k) {
+        Index pi = k, pj = k;
+        double best = -1.0;
+        for (Index j = k; j < c; ++j)
+          for (Index i = k; i < r; ++i)
+            if (std::abs(a(i, j)) > best) best = std::abs(a(i, j)), pi = i, pj = j;
+        if (k == 0) maxpiv = best;
+        if (best <= std::numeric_limits<double>::epsilon() * n * maxpiv || best == 0.0) break;
+        ++rk;
+        for (Index j = 0; j < c; ++j) std::swap(a(k, j), a(pi, j));
+        for (Index i = 0; i < r; ++i) std::swap(a(i, k), a(i, pj));
+        for (Index i = k + 1; i < r; ++i) {
+          const scalar_t f = a(i, k) / a(k, k);
+          for (Index j = k; j < c; ++j) a(i, j) -= f * a(k, j);
+        }
+      }
+      return rk;
+    }
+  };
+  FullPivLU fullPivLu() const { return {MatX<scalar_t>(derived())}; }
+  // rowwise().reverse(): column order reversed; colwise().reverse(): row order reversed
+  struct Wise {
+    const D& m;
+    bool rowwise;
+    auto reverse() const {
+      MatX<scalar_t> o(m.rows(), m.cols());
+      for (Index j = 0; j < m.cols(); ++j)
+        for (Index i = 0; i < m.rows(); ++i)
+          o(i, j) = rowwise ? m.coeff(i, m.cols() - 1 - j) : m.coeff(m.rows() - 1 - i, j);
+      return o;
+    }
+  };
+  Wise rowwise() const { return {derived(), true}; }
+  Wise colwise() const { return {derived(), false}; }
+  auto reverse() const {
+    MatX<scalar_t> o(rows(), cols());
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) o(i, j) = coeff(rows() - 1 - i, cols() - 1 - j);
+    return o;
+  }
+  template <class E>
+  scalar_t dot(const DenseBase<E>& o) const {
+    scalar_t s(0);
+    for (Index i = 0; i < size(); ++i) s += internal::conj(lin(i)) * o.lin(i);
+    return s;
+  }
+
+  // linear (vector) access
+  auto lin(Index k) const {
+    if (cols() == 1) return coeff(k, 0);
+    if (rows() == 1) return coeff(0, k);
+    return coeff(k % rows(), k / rows());
+  }
+  auto x() const { return lin(0); }
+  auto y() const { return lin(1); }
+  auto z() const { return lin(2); }
+
+  Index rows() const { return derived().rows(); }
+  Index cols() const { return derived().cols(); }
+  Index ld() const { return derived().ld(); }
+  Index is() const { return derived().is(); }
+
+ protected:
+  const scalar_t* cptr() const { return derived().ptr(); }
+  template <class Q>
+  View<Q*> mkview(Q* p, Index r, Index c) const {
+    return View<Q*>(p, r, c, ld(), is());
+  }
+  template <class Q>
+  View<Q*> vec_view(Q* p, Index i, Index n) const {
+    if (cols() == 1) return View<Q*>(p + i * is(), n, 1, ld(), is());
+    return View<Q*>(p + i * ld(), 1, n, ld(), is());
+  }
+  template <class F>
+  auto unary(F f) const {
+    MatX<scalar_t> o(rows(), cols());
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) o(i, j) = f(coeff(i, j));
+    return o;
+  }
+  template <class F>
+  auto unary_r(F f) const {
+    MatX<typename internal::real_of<scalar_t>::type> o(rows(), cols());
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) o(i, j) = f(coeff(i, j));
+    return o;
+  }
+  template <class E, class F>
+  auto binary(const DenseBase<E>& b, F f) const {
+    if (b.rows() != rows() || b.cols() != cols()) throw std::logic_error("eigen shim: size mismatch");
+    MatX<scalar_t> o(rows(), cols());
+    for (Index j = 0; j < cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) o(i, j) = f(coeff(i, j), b.coeff(i, j));
+    return o;
+  }
+};
+
+// write-through helpers for mutable matrices and views
+template <class D, class E>
+void assign_into(D& dst, const DenseBase<E>& src, int mode /*0 =, 1 +=, 2 -=*/) {
+  if (src.rows() != dst.rows() || src.cols() != dst.cols())
+    throw std::logic_error("eigen shim: assignment size mismatch");
+  // evaluate first: the source may alias the destination
+  const MatX<typename D::Scalar> tmp(src);
+  auto* p = dst.ptr();
+  const Index ld = dst.ld(), is = dst.is();
+  for (Index j = 0; j < dst.cols(); ++j)
+    for (Index i = 0; i < dst.rows(); ++i) {
+      auto& v = p[i * is + j * ld];
+      if (mode == 0)
+        v = tmp(i, j);
+      else if (mode == 1)
+        v += tmp(i, j);
+      else
+        v -= tmp(i, j);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// strided view (P = S* writable, const S* read-only)
+template <class P>
+class View : public DenseBase<View<P>> {
+ public:
+  using Scalar = std::remove_cv_t<std::remove_pointer_t<P>>;
+  using RealScalar = typename internal::real_of<Scalar>::type;
+  View(P p, Index r, Index c, Index ld, Index is = 1) : p_(p), r_(r), c_(c), ld_(ld), is_(is) {}
+  View(const View&) = default;
+  Index rows() const { return r_; }
+  Index cols() const { return c_; }
+  Index ld() const { return ld_; }
+  Index is() const { return is_; }
+  P ptr() const { return p_; }
+  auto& at(Index i, Index j) const { return p_[i * is_ + j * ld_]; }
+  auto& operator()(Index i, Index j) const { return at(i, j); }
+  auto& operator()(Index k) const { return c_ == 1 ? p_[k * is_] : p_[k * ld_]; }
+  auto& operator[](Index k) const { return (*this)(k); }
+
+  View& operator=(const View& o) {
+    assign_into(*this, o, 0);
+    return *this;
+  }
+  template <class E>
+  View& operator=(const DenseBase<E>& o) {
+    assign_into(*this, o, 0);
+    return *this;
+  }
+  template <class E>
+  View& operator+=(const DenseBase<E>& o) {
+    assign_into(*this, o, 1);
+    return *this;
+  }
+  template <class E>
+  View& operator-=(const DenseBase<E>& o) {
+    assign_into(*this, o, 2);
+    return *this;
+  }
+  View& operator*=(const Scalar& s) {
+    for (Index j = 0; j < c_; ++j)
+      for (Index i = 0; i < r_; ++i) at(i, j) *= s;
+    return *this;
+  }
+  View& noalias() { return *this; }
+  View& setConstant(const Scalar& s) {
+    for (Index j = 0; j < c_; ++j)
+      for (Index i = 0; i < r_; ++i) at(i, j) = s;
+    return *this;
+  }
+  View& setZero() { return setConstant(Scalar(0)); }
+  CommaInit<View> operator<<(const Scalar& s) { return CommaInit<View>(*this, s); }
+
+ private:
+  P p_;
+  Index r_, c_, ld_, is_;
+};
+
+// ---------------------------------------------------------------------------
+template <class S, int R, int C>
+class Matrix : public DenseBase<Matrix<S, R, C>> {
+ public:
+  using Scalar = S;
+  using RealScalar = typename internal::real_of<S>::type;
+  static constexpr int RowsAtCompileTime = R, ColsAtCompileTime = C;
+
+  Matrix() : r_(R > 0 ? R : 0), c_(C > 0 ? C : 0), v_(static_cast<size_t>(r_ * c_), S(0)) {}
+  Matrix(Index r, Index c)
+    requires(R == Dynamic || C == Dynamic)
+      : r_(r), c_(c), v_(static_cast<size_t>(r * c), S(0)) {}
+  explicit Matrix(Index n)
+    requires((R == Dynamic) != (C == Dynamic))
+      : r_(R == 1 ? 1 : n), c_(C == 1 ? 1 : n), v_(static_cast<size_t>(n), S(0)) {}
+  Matrix(const S& a, const S& b)
+    requires(R > 0 && C > 0 && R * C == 2)
+      : r_(R), c_(C), v_{a, b} {}
+  Matrix(const S& a, const S& b, const S& c)
+    requires(R > 0 && C > 0 && R * C == 3)
+      : r_(R), c_(C), v_{a, b, c} {}
+  Matrix(const Matrix&) = default;
+  Matrix(Matrix&&) noexcept = default;
+  template <class E>
+  Matrix(const DenseBase<E>& o) : r_(o.rows()), c_(o.cols()), v_(static_cast<size_t>(r_ * c_)) {
+    check_shape();
+    for (Index j = 0; j < c_; ++j)
+      for (Index i = 0; i < r_; ++i) v_[i + j * r_] = o.coeff(i, j);
+  }
+  Matrix& operator=(const Matrix&) = default;
+  Matrix& operator=(Matrix&&) noexcept = default;
+  template <class E>
+  Matrix& operator=(const DenseBase<E>& o) {
+    Matrix tmp(o);  // o may view this matrix
+    *this = std::move(tmp);
+    return *this;
+  }
+  template <class E>
+  Matrix& operator+=(const DenseBase<E>& o) {
+    assign_into(*this, o, 1);
+    return *this;
+  }
+  template <class E>
+  Matrix& operator-=(const DenseBase<E>& o) {
+    assign_into(*this, o, 2);
+    return *this;
+  }
+  Matrix& operator*=(const S& s) {
+    for (auto& x : v_) x *= s;
+    return *this;
+  }
+  Matrix& operator/=(const S& s) {
+    for (auto& x : v_) x /= s;
+    return *this;
+  }
+  Matrix& noalias() { return *this; }
+
+  static Matrix Zero(Index r, Index c) { return Matrix(r, c); }
+  static Matrix Zero(Index n)
+    requires((R == Dynamic) != (C == Dynamic))
+  {
+    return Matrix(n);
+  }
+  static Matrix Zero() { return Matrix(); }
+  static Matrix Constant(Index r, Index c, const S& s) {
+    Matrix m(r, c);
+    std::fill(m.v_.begin(), m.v_.end(), s);
+    return m;
+  }
+  static Matrix Ones(Index r, Index c) { return Constant(r, c, S(1)); }
+  static Matrix Identity(Index r, Index c) {
+    Matrix m(r, c);
+    for (Index i = 0; i < std::min(r, c); ++i) m(i, i) = S(1);
+    return m;
+  }
+
+  Index rows() const { return r_; }
+  Index cols() const { return c_; }
+  Index ld() const { return r_; }
+  Index is() const { return 1; }
+  S& at(Index i, Index j) { return v_[i + j * r_]; }
+  const S& at(Index i, Index j) const { return v_[i + j * r_]; }
+  S* ptr() { return v_.data(); }
+  const S* ptr() const { return v_.data(); }
+  S* data() { return v_.data(); }
+  const S* data() const { return v_.data(); }
+  S& operator()(Index i, Index j) { return v_[i + j * r_]; }
+  const S& operator()(Index i, Index j) const { return v_[i + j * r_]; }
+  S& operator()(Index k) { return v_[k]; }
+  const S& operator()(Index k) const { return v_[k]; }
+  S& operator[](Index k) { return v_[k]; }
+  const S& operator[](Index k) const { return v_[k]; }
+  S& x() { return v_[0]; }
+  S& y() { return v_[1]; }
+  S& z() { return v_[2]; }
+  const S& x() const { return v_[0]; }
+  const S& y() const { return v_[1]; }
+  const S& z() const { return v_[2]; }
+  void resize(Index r, Index c) {
+    r_ = r;
+    c_ = c;
+    v_.assign(static_cast<size_t>(r * c), S(0));
+  }
+  void resize(Index n) { resize(R == 1 ? 1 : n, R == 1 ? n : 1); }
+  void conservativeResize(Index r, Index c) {
+    Matrix m(r, c);
+    for (Index j = 0; j < std::min(c, c_); ++j)
+      for (Index i = 0; i < std::min(r, r_); ++i) m(i, j) = (*this)(i, j);
+    *this = std::move(m);
+  }
+  Matrix& setZero() {
+    std::fill(v_.begin(), v_.end(), S(0));
+    return *this;
+  }
+  Matrix& setZero(Index r, Index c) {
+    resize(r, c);
+    return *this;
+  }
+  Matrix& setConstant(const S& s) {
+    std::fill(v_.begin(), v_.end(), s);
+    return *this;
+  }
+  CommaInit<Matrix> operator<<(const S& s) { return CommaInit<Matrix>(*this, s); }
+  Matrix& setIdentity() {
+    *this = Identity(r_, c_);
+    return *this;
+  }
+
+ private:
+  void check_shape() const {
+    if ((R > 0 && r_ != R) || (C > 0 && c_ != C)) throw std::logic_error("eigen shim: fixed-size mismatch");
+  }
+  Index r_, c_;
+  std::vector<S> v_;
+};
+
+// ---------------------------------------------------------------------------
+// arithmetic (eager)
+namespace internal {
+// Products whose inner dimensions disagree are an eigen_assert in Eigen, compiled out under
+// NDEBUG (undefined behaviour); one reference unit test builds such an operand on purpose
+// (test_mmp.cpp:40-48, zero-width leaf basis under an unchanged transfer) and checks only the
+// result's shape.  The shim returns zeros of the (lhs.rows x rhs.cols) shape and counts it.
+inline long long& shape_mismatches() {
+  static long long n = 0;
+  return n;
+}
+template <class S>
+MatX<S> gemm(const MatX<S>& a, const MatX<S>& b) {
+  MatX<S> c(a.rows(), b.cols());
+  if (a.cols() != b.rows()) {
+    ++shape_mismatches();
+    return c;
+  }
+  const int m = static_cast<int>(a.rows()), n = static_cast<int>(b.cols()), k = static_cast<int>(a.cols());
+  if (m == 0 || n == 0 || k == 0) return c;
+  const int lda = std::max(1, m), ldb = std::max(1, k), ldc = std::max(1, m);
+  if constexpr (is_cplx<S>::value) {
+    const S one(1), zero(0);
+    scipy_cblas_zgemm(102, 111, 111, m, n, k, &one, a.data(), lda, b.data(), ldb, &zero, c.data(), ldc);
+  } else {
+    scipy_cblas_dgemm(102, 111, 111, m, n, k, 1.0, a.data(), lda, b.data(), ldb, 0.0, c.data(), ldc);
+  }
+  return c;
+}
+template <class T>
+inline constexpr bool is_scalar_v = std::is_arithmetic_v<T> || is_cplx<T>::value;
+}  // namespace internal
+
+template <class A, class B>
+auto operator*(const DenseBase<A>& a, const DenseBase<B>& b) {
+  using S = typename DenseBase<A>::scalar_t;
+  static_assert(std::is_same_v<S, typename DenseBase<B>::scalar_t>, "eigen shim: mixed scalar product");
+  return internal::gemm<S>(MatX<S>(a), MatX<S>(b));
+}
+template <class A, class T>
+  requires internal::is_scalar_v<T>
+auto operator*(const DenseBase<A>& a, const T& s) {
+  using S = typename DenseBase<A>::scalar_t;
+  MatX<S> o(a);
+  o *= S(s);
+  return o;
+}
+template <class A, class T>
+  requires internal::is_scalar_v<T>
+auto operator*(const T& s, const DenseBase<A>& a) {
+  return a * s;
+}
+template <class A, class T>
+  requires internal::is_scalar_v<T>
+auto operator/(const DenseBase<A>& a, const T& s) {
+  using S = typename DenseBase<A>::scalar_t;
+  MatX<S> o(a);
+  o /= S(s);
+  return o;
+}
+template <class A, class B>
+auto operator+(const DenseBase<A>& a, const DenseBase<B>& b) {
+  using S = typename DenseBase<A>::scalar_t;
+  MatX<S> o(a);
+  o += b;
+  return o;
+}
+template <class A, class B>
+auto operator-(const DenseBase<A>& a, const DenseBase<B>& b) {
+  using S = typename DenseBase<A>::scalar_t;
+  MatX<S> o(a);
+  o -= b;
+  return o;
+}
+template <class A>
+auto operator-(const DenseBase<A>& a) {
+  using S = typename DenseBase<A>::scalar_t;
+  MatX<S> o(a);
+  o *= S(-1);
+  return o;
+}
+
+using MatrixXd = Matrix<double, Dynamic, Dynamic>;
+using MatrixXcd = Matrix<std::complex<double>, Dynamic, Dynamic>;
+using VectorXd = Matrix<double, Dynamic, 1>;
+using VectorXcd = Matrix<std::complex<double>, Dynamic, 1>;
+using Vector2d = Matrix<double, 2, 1>;
+using Vector3d = Matrix<double, 3, 1>;
+
+// ---------------------------------------------------------------------------
+// SelfAdjointEigenSolver: LAPACK ?syevd / ?heevd on the lower triangle
+template <class MatrixType>
+class SelfAdjointEigenSolver {
+ public:
+  using Scalar = typename MatrixType::Scalar;
+  using RealVectorType = Matrix<double, Dynamic, 1>;
+
+  SelfAdjointEigenSolver() = default;
+  template <class E>
+  explicit SelfAdjointEigenSolver(const DenseBase<E>& a, int options = ComputeEigenvectors) {
+    compute(a, options);
+  }
+  template <class E>
+  SelfAdjointEigenSolver& compute(const DenseBase<E>& a, int options = ComputeEigenvectors) {
+    vec_ = MatrixType(a);
+    const int n = static_cast<int>(vec_.rows());
+    val_ = RealVectorType(n);
+    info_ = InvalidInput;
+    if (vec_.rows() != vec_.cols()) return *this;
+    if (n == 0) {
+      info_ = Success;
+      return *this;
+    }
+    const char* jobz = (options & EigenvaluesOnly) ? "N" : "V";
+    int info = 0, lwork = -1, liwork = -1, iwq = 0;
+    if constexpr (internal::is_cplx<Scalar>::value) {
+      int lrwork = -1;
+      Scalar wq;
+      double rwq;
+      scipy_zheevd_(jobz, "L", &n, vec_.data(), &n, val_.data(), &wq, &lwork, &rwq, &lrwork, &iwq, &liwork, &info,
+                    1, 1);
+      lwork = static_cast<int>(std::real(wq));
+      lrwork = static_cast<int>(rwq);
+      liwork = iwq;
+      std::vector<Scalar> work(std::max(1, lwork));
+      std::vector<double> rwork(std::max(1, lrwork));
+      std::vector<int> iwork(std::max(1, liwork));
+      scipy_zheevd_(jobz, "L", &n, vec_.data(), &n, val_.data(), work.data(), &lwork, rwork.data(), &lrwork,
+                    iwork.data(), &liwork, &info, 1, 1);
+    } else {
+      double wq;
+      scipy_dsyevd_(jobz, "L", &n, vec_.data(), &n, val_.data(), &wq, &lwork, &iwq, &liwork, &info, 1, 1);
+      lwork = static_cast<int>(wq);
+      liwork = iwq;
+      std::vector<double> work(std::max(1, lwork));
+      std::vector<int> iwork(std::max(1, liwork));
+      scipy_dsyevd_(jobz, "L", &n, vec_.data(), &n, val_.data(), work.data(), &lwork, iwork.data(), &liwork, &info,
+                    1, 1);
+    }
+    info_ = info == 0 ? Success : NoConvergence;
+    return *this;
+  }
+  ComputationInfo info() const { return info_; }
+  const RealVectorType& eigenvalues() const { return val_; }
+  const MatrixType& eigenvectors() const { return vec_; }
+
+ private:
+  MatrixType vec_;
+  RealVectorType val_;
+  ComputationInfo info_ = InvalidInput;
+};
+
+}  // namespace Eigen

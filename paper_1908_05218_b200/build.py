@@ -109,6 +109,10 @@ def build_oracle(force: bool = False) -> Path | None:
     if force:
         subprocess.run(["make", "-s", "-C", str(odir), "clean"], check=False)
     _run(cmd)
+    # the reference's own MMP path (unmodified sources + oracle/eigen_shim) and its unit tests, only
+    # where /root/reference exists (this container; the GPU box never needs them)
+    if Path("/root/reference/proj/core/src/mmp.cpp").exists():
+        _run(["make", "-s", "-C", str(odir), f"PY={sys.executable}", "ref", "ref-tests"])
     return odir / "_build" / "liboracle.so"
 
 
