@@ -22,6 +22,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <complex>
 #include <cstddef>
@@ -612,8 +613,23 @@ inline long long& shape_mismatches() {
   static long long n = 0;
   return n;
 }
+// Instrumentation for the sliced reference arm of bench.py (oracle/ref_driver.cpp): multiply-
+// accumulates executed by products and the nominal 9 n^3 per eigensolve (the reference's own
+// counting rule, mmp.cpp:67-80), and a cooperative abort that unwinds a running product at its
+// next product (the reference itself has no cancellation point).
+inline std::atomic<long long>& mac_counter() {
+  static std::atomic<long long> n{0};
+  return n;
+}
+struct Aborted {};
+inline std::atomic<bool>& abort_flag() {
+  static std::atomic<bool> f{false};
+  return f;
+}
 template <class S>
 MatX<S> gemm(const MatX<S>& a, const MatX<S>& b) {
+  if (abort_flag().load(std::memory_order_relaxed)) throw Aborted{};
+  mac_counter().fetch_add(static_cast<long long>(a.rows()) * a.cols() * b.cols(), std::memory_order_relaxed);
   MatX<S> c(a.rows(), b.cols());
   if (a.cols() != b.rows()) {
     ++shape_mismatches();
@@ -707,6 +723,7 @@ class SelfAdjointEigenSolver {
   SelfAdjointEigenSolver& compute(const DenseBase<E>& a, int options = ComputeEigenvectors) {
     vec_ = MatrixType(a);
     const int n = static_cast<int>(vec_.rows());
+    internal::mac_counter().fetch_add(9LL * n * n * n, std::memory_order_relaxed);
     val_ = RealVectorType(n);
     info_ = InvalidInput;
     if (vec_.rows() != vec_.cols()) return *this;

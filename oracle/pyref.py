@@ -3,9 +3,11 @@
 ctypes wrapper of oracle/_ref/libh2ref.so: the REFERENCE's own MMP-path sources
 (/root/reference/proj/core/src, unmodified) compiled here against
 oracle/eigen_shim (Eigen is absent from this image), driven by
-oracle/ref_driver.cpp.  Used only by tools/make_ref_golden.py to write
-tests/golden/ref_cases.npz; /root/reference does not exist on the GPU box, so
-no test or bench imports this module.
+oracle/ref_driver.cpp.  Used by tools/make_ref_golden.py (writes
+tests/golden/ref_cases.npz, here) and by bench.py's reference arm
+(`--impl reference`: SlicedReference times the reference's own mmp() on the
+bench workload).  The prebuilt .so travels to the GPU box with the snapshot;
+/root/reference itself is never read at run time.
 """
 from __future__ import annotations
 
@@ -42,6 +44,13 @@ def lib() -> C.CDLL:
                                         C.POINTER(C.c_int)]
         L.h2r_free.argtypes = [C.c_void_p]
         L.h2r_shape_mismatches.restype = C.c_longlong
+        L.h2r_sliced_start.restype = C.c_void_p
+        L.h2r_sliced_start.argtypes = [C.POINTER(h2c_matrix), C.POINTER(h2c_matrix), C.c_double, C.c_int,
+                                       C.POINTER(C.c_int)]
+        L.h2r_sliced_step.argtypes = [C.c_void_p, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.h2r_sliced_stop.argtypes = [C.c_void_p]
+        L.h2r_mac_counter.restype = C.c_longlong
         _lib = L
     return _lib
 
@@ -120,3 +129,37 @@ class RefCase:
 
 def shape_mismatches() -> int:
     return lib().h2r_shape_mismatches()
+
+
+def available() -> bool:
+    return LIBPATH.exists()
+
+
+class SlicedReference:
+    """The reference's own mmp() (single-threaded, mmp.hpp:58-66) run back to back on operands given
+    as flat descriptors (converted into the reference's types, block tree rebuilt by the reference
+    and checked against the descriptor's).  step(seconds) -> (wall seconds, reference MACs in the
+    window — the shim counts exactly MmpReport.flops' rule —, products completed, their flops)."""
+
+    def __init__(self, a, b, eps: float, adaptive: bool = True):
+        self._a, self._b = a, b  # the descriptors must outlive the engine
+        self._da, self._db = a.desc(), b.desc()
+        code = C.c_int(0)
+        self._h = lib().h2r_sliced_start(C.byref(self._da), C.byref(self._da) if b is a else C.byref(self._db),
+                                         eps, int(adaptive), C.byref(code))
+        if not self._h:
+            raise RuntimeError(f"reference error {code.value}: {lib().h2r_last_error().decode()}")
+
+    def step(self, seconds: float):
+        el, macs, prods, pf = C.c_double(), C.c_int64(), C.c_int64(), C.c_int64()
+        if lib().h2r_sliced_step(self._h, seconds, C.byref(el), C.byref(macs), C.byref(prods), C.byref(pf)):
+            raise RuntimeError(lib().h2r_last_error().decode())
+        return el.value, int(macs.value), int(prods.value), int(pf.value)
+
+    def close(self) -> None:
+        if self._h:
+            lib().h2r_sliced_stop(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

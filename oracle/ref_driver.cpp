@@ -341,3 +341,200 @@ extern "C" {
 /* products whose inner dimensions disagreed (Eigen's compiled-out assert; must stay 0 for real cases) */
 long long h2r_shape_mismatches(void) { return Eigen::internal::shape_mismatches(); }
 }
+
+// ---------------------------------------------------------------------------
+// Sliced reference arm of bench.py (`--impl reference`): the reference's own mmp()
+// (single-threaded, as documented at mmp.hpp:58-66) run back to back on the bench
+// workload, with its operands converted from the flat descriptors into the
+// reference's types.  Progress is read from the Eigen shim's MAC counter (products +
+// 9 n^3 per eigensolve, the reference's counting rule), so any time window of a
+// running product yields a rate; completed products report their exact flops.
+#include <chrono>
+#include <thread>
+
+extern "C" void scipy_openblas_set_num_threads(int);
+
+namespace {
+
+std::shared_ptr<const ClusterTree> tree_from_desc(const h2c_tree& d) {
+  auto t = std::make_shared<ClusterTree>();
+  t->clusters.resize(d.n_clusters);
+  t->depth = d.depth;
+  t->leafsize = d.leafsize;
+  t->levels.assign(d.depth + 1, {});
+  for (int c = 0; c < d.n_clusters; ++c) {
+    Cluster& cl = t->clusters[c];
+    cl.id = c;
+    cl.parent = d.parent[c];
+    cl.level = d.level[c];
+    cl.begin = d.begin[c];
+    cl.end = d.end[c];
+    cl.child = {d.child0[c], d.child1[c]};
+    if (d.bbox)
+      for (int k = 0; k < 3; ++k) {
+        cl.bbox_min[k] = d.bbox[6 * size_t(c) + k];
+        cl.bbox_max[k] = d.bbox[6 * size_t(c) + 3 + k];
+      }
+    t->levels[cl.level].push_back(c);
+  }
+  for (auto& lv : t->levels)
+    std::sort(lv.begin(), lv.end(), [&](int a, int b) { return t->clusters[a].begin < t->clusters[b].begin; });
+  t->perm.assign(d.perm, d.perm + d.n_points);
+  t->inv_perm.assign(d.n_points, 0);
+  for (int p = 0; p < d.n_points; ++p) t->inv_perm[d.perm[p]] = p;
+  return t;
+}
+
+template <class S>
+DenseMatrix<S> read_mat(const h2c_matrix& d, int64_t off, Index r, Index c) {
+  DenseMatrix<S> m(r, c);
+  if (r * c) std::memcpy(static_cast<void*>(m.data()), reinterpret_cast<const S*>(d.values) + off, sizeof(S) * r * c);
+  return m;
+}
+
+template <class S>
+H2Matrix<S> h2_from_desc(const h2c_matrix& d, std::shared_ptr<const ClusterTree> tree,
+                         std::shared_ptr<const BlockTree> st) {
+  H2Matrix<S> h;
+  h.tree = tree;
+  h.structure = st;
+  const int nc = static_cast<int>(tree->clusters.size());
+  for (int side = 0; side < 2; ++side) {
+    ClusterBasis<S>& b = side == 0 ? h.row_basis : h.col_basis;
+    const int32_t* rk = side == 0 ? d.row_rank : d.col_rank;
+    const uint8_t* dg = side == 0 ? d.row_degenerate : d.col_degenerate;
+    const int64_t* off = side == 0 ? d.row_offset : d.col_offset;
+    b.resize(nc);
+    for (int c = 0; c < nc; ++c) {
+      b.rank[c] = rk[c];
+      b.degenerate[c] = dg[c];
+      const Cluster& cl = tree->clusters[c];
+      if (off[c] < 0) continue;
+      if (cl.is_leaf())
+        b.leaf[c] = read_mat<S>(d, off[c], cl.size(), rk[c]);
+      else
+        b.transfer[c] = read_mat<S>(d, off[c], rk[cl.child[0]] + rk[cl.child[1]], rk[c]);
+    }
+  }
+  const h2c_blocks& bd = *d.blocks;
+  for (int64_t k = 0; k < bd.n_blocks; ++k) {
+    const BlockKey key{bd.row[k], bd.col[k]};
+    if (bd.kind[k] == H2C_ADMISSIBLE)
+      h.coupling[key] = read_mat<S>(d, d.block_offset[k], d.row_rank[key.row], d.col_rank[key.col]);
+    else if (bd.kind[k] == H2C_INADMISSIBLE_LEAF)
+      h.full[key] =
+          read_mat<S>(d, d.block_offset[k], tree->clusters[key.row].size(), tree->clusters[key.col].size());
+  }
+  return h;
+}
+
+struct SlicedBase {
+  virtual ~SlicedBase() = default;
+  std::thread th;
+  std::atomic<long long> products{0};
+  std::atomic<long long> product_flops{0};
+  std::string error;
+};
+
+template <class S>
+struct Sliced : SlicedBase {
+  H2Matrix<S> A, B;
+  bool same = false;
+  double eps = 0.0;
+  bool adaptive = true;
+  void loop() {
+    try {
+      for (;;) {
+        const MmpResult<S> r = adaptive ? mmp(A, same ? A : B, eps) : formatted_mmp(A, same ? A : B);
+        product_flops += r.report.flops;
+        ++products;
+      }
+    } catch (const Eigen::internal::Aborted&) {
+    } catch (const std::exception& e) {
+      error = e.what();
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+/* Convert the operands (flat descriptors, same tree/blocks) into the reference's types and start
+ * the reference's products back to back on a worker thread (BLAS single-threaded, like Eigen
+ * without OpenMP).  Returns nullptr on error; *code as h2r_run. */
+void* h2r_sliced_start(const h2c_matrix* a, const h2c_matrix* b, double eps, int adaptive, int* code) {
+  *code = 0;
+  try {
+    if (a->tree != b->tree || a->blocks != b->blocks)
+      throw ConfigError("mmp: operands must share cluster trees and block structure");
+    scipy_openblas_set_num_threads(1);
+    auto tree = tree_from_desc(*a->tree);
+    auto st = build_block_tree(tree, tree, a->blocks->eta);
+    // the reference's partition must be the one the descriptors carry
+    FlatBlocks fb;
+    flatten_blocks(*st, fb);
+    const h2c_blocks& d = *a->blocks;
+    if (fb.row.size() != size_t(d.n_blocks) || !std::equal(fb.row.begin(), fb.row.end(), d.row) ||
+        !std::equal(fb.col.begin(), fb.col.end(), d.col) || !std::equal(fb.kind.begin(), fb.kind.end(), d.kind))
+      throw InvariantError("reference block tree differs from the descriptor's");
+    auto start = [&](auto tag) -> SlicedBase* {
+      using S = decltype(tag);
+      auto s = std::make_unique<Sliced<S>>();
+      s->A = h2_from_desc<S>(*a, tree, st);
+      s->same = a == b || (a->values == b->values && a->row_offset == b->row_offset);
+      if (!s->same) s->B = h2_from_desc<S>(*b, tree, st);
+      s->eps = eps;
+      s->adaptive = adaptive != 0;
+      Eigen::internal::abort_flag() = false;
+      Sliced<S>* raw = s.get();
+      s->th = std::thread([raw] { raw->loop(); });
+      return s.release();
+    };
+    if (a->scalar == H2C_COMPLEX) return start(Complex{});
+    return start(Real{});
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    *code = 2;
+  } catch (const InvariantError& e) {
+    g_err = e.what();
+    *code = 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    *code = 1;
+  }
+  return nullptr;
+}
+
+/* Let the product run for `seconds`; returns the elapsed wall time, the MACs counted in the window
+ * and the number of products completed so far (and their exact reference flops). */
+int h2r_sliced_step(void* h, double seconds, double* elapsed, int64_t* macs, int64_t* products,
+                    int64_t* product_flops) {
+  auto* s = static_cast<SlicedBase*>(h);
+  const long long m0 = Eigen::internal::mac_counter().load();
+  const auto t0 = std::chrono::steady_clock::now();
+  std::this_thread::sleep_for(std::chrono::duration<double>(seconds));
+  const long long m1 = Eigen::internal::mac_counter().load();
+  *elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *macs = m1 - m0;
+  *products = s->products.load();
+  *product_flops = s->product_flops.load();
+  if (!s->error.empty()) {
+    g_err = s->error;
+    return 1;
+  }
+  return 0;
+}
+
+void h2r_sliced_stop(void* h) {
+  auto* s = static_cast<SlicedBase*>(h);
+  Eigen::internal::abort_flag() = true;
+  if (s->th.joinable()) s->th.join();
+  Eigen::internal::abort_flag() = false;
+  delete s;
+}
+
+/* MACs counted by the shim since load (for checking the counter against MmpReport.flops) */
+long long h2r_mac_counter(void) { return Eigen::internal::mac_counter().load(); }
+
+}  // extern "C"

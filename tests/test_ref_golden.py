@@ -120,3 +120,24 @@ def test_gpu_matches_reference(i):
     # the device MVP / relative_error against the reference's metric (metrics.cpp:37-55)
     e = P.relative_error(A, A, r.product, 3, ctx)
     assert abs(e - m["relative_error_seed3"]) <= 1e-6 * m["relative_error_seed3"] + 10 * max(m["eps"], 1e-13)
+
+
+def test_reference_arm_counts_the_reference_flops():
+    """bench.py --impl reference: the shim's MAC counter over complete products equals the
+    reference's own MmpReport.flops (so time windows of a running product give its true rate)."""
+    from oracle import pyref as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    m = META[5]
+    A = build_operand(m)
+    S = R.SlicedReference(A, A, m["eps"])
+    total_macs, prods = 0, 0
+    try:
+        for _ in range(40):
+            _, macs, prods, pflops = S.step(0.25)
+            total_macs += macs
+            if prods >= 1:
+                break
+    finally:
+        S.close()
+    assert prods >= 1 and pflops == prods * int(Z["c5_rep_flops"])
