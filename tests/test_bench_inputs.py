@@ -48,3 +48,45 @@ def test_bench_operands_small(name):
         assert A.scalar == P.H2C_COMPLEX and B is A
     if name in ("cfg3", "cfg4"):
         assert B is not A
+
+
+def _recompression_case(kind):
+    from oracle import pyoracle as O  # checker only
+    if kind == "helmholtz":
+        n, leaf, eps = 4096, 64, 1e-4
+        pts = bench.sphere_points(n) * 0.5  # ~4 wavelengths across
+    else:
+        n, leaf, eps = 4096, 32, 1e-6
+        pts = O.geometry("random_cloud", seed=1, n=n)
+    t = O.build_cluster_tree(pts, leaf)
+    s = O.build_block_tree(t, 1.0)
+    orders = bench.helmholtz_orders(t, hi=7) if kind == "helmholtz" else 4
+    kap = bench.KAPPA if kind == "helmholtz" else 0.0
+    A0 = P.build_chebyshev(t, s, pts, orders, kernel=kind, kappa=kap)
+    Ar = P.build_chebyshev(t, s, pts, orders, kernel=kind, kappa=kap, eps_recompress=eps)
+    D0 = O.h2_to_dense(A0)
+    Aref = O.build_h2(D0, s, eps)  # the reference's rule (h2_matrix.cpp:83-181) on the dense operand
+    return O, D0, Ar, Aref
+
+
+def _check_recompression(kind):
+    O, D0, Ar, Aref = _recompression_case(kind)
+    assert np.array_equal(Ar.row_rank, Aref.row_rank) and np.array_equal(Ar.col_rank, Aref.col_rank)
+    assert np.array_equal(Ar.row_degenerate, Aref.row_degenerate)
+    Dr, Dref = O.h2_to_dense(Ar), O.h2_to_dense(Aref)
+    assert np.linalg.norm(Dr - Dref) <= 1e-11 * np.linalg.norm(D0)
+
+
+@pytest.mark.parametrize("kind", ["laplace", "helmholtz"])
+def test_recompression_matches_the_reference_rule(kind):
+    """The constructor's recompression (construct.cpp, host path here) equals the reference's own
+    build_h2 (oracle restatement, pinned to the reference by tests/test_ref_golden.py) applied to
+    the dense interpolation operand: equal ranks, same matrix to round-off."""
+    _check_recompression(kind)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["laplace", "helmholtz"])
+def test_device_recompression_matches_the_reference_rule(kind):
+    """Same with the constructor's device passes (construct_dev.cu) active."""
+    _check_recompression(kind)
