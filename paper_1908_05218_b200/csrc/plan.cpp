@@ -224,17 +224,35 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
     const bool leaf = l == D;
     rows[l].resize(L.n);
     parallel_for(L.n, threads, [&](int i) {
-      auto& out = rows[l][i].t;
-      for (int ba = L.row_ptr[i]; ba < L.row_ptr[i + 1]; ++ba) {
-        const int j = L.bcol[ba];
-        for (int bb = L.row_ptr[j]; bb < L.row_ptr[j + 1]; ++bb) {
-          if (!leaf && L.bkind[ba] == kSub && L.bkind[bb] == kSub) continue;  // mmp.cpp:593
-          out.push_back({L.bcol[bb], j, ba, bb});
+      // bucket (counting) sort by target column k: row i's blocks come in ascending j, so each
+      // bucket fills in ascending j — the (k, j) order without sorting the triples themselves
+      thread_local std::vector<int32_t> at;
+      thread_local std::vector<int32_t> touched;
+      if (at.size() < size_t(L.n)) at.assign(L.n, 0);
+      touched.clear();
+      auto each = [&](auto&& f) {
+        for (int ba = L.row_ptr[i]; ba < L.row_ptr[i + 1]; ++ba) {
+          const int j = L.bcol[ba];
+          for (int bb = L.row_ptr[j]; bb < L.row_ptr[j + 1]; ++bb) {
+            if (!leaf && L.bkind[ba] == kSub && L.bkind[bb] == kSub) continue;  // mmp.cpp:593
+            f(L.bcol[bb], j, ba, bb);
+          }
         }
-      }
-      std::sort(out.begin(), out.end(), [](const Triple& x, const Triple& y) {
-        return x.k < y.k || (x.k == y.k && x.j < y.j);
+      };
+      each([&](int k, int, int, int) {
+        if (at[k]++ == 0) touched.push_back(k);
       });
+      std::sort(touched.begin(), touched.end());
+      int32_t total = 0;
+      for (int k : touched) {
+        const int32_t c = at[k];
+        at[k] = total;
+        total += c;
+      }
+      auto& out = rows[l][i].t;
+      out.resize(total);
+      each([&](int k, int j, int ba, int bb) { out[at[k]++] = {k, j, ba, bb}; });
+      for (int k : touched) at[k] = 0;
     });
     // case counters (mmp.cpp:307-308, 594-595), per row in parallel
     std::vector<std::array<int64_t, 4>> cc(L.n);
@@ -315,14 +333,14 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
   for (int l = 1; l < D; ++l) {
     LevelPlan& L = P.lv[l];
     std::vector<uint8_t> has(L.brow.size(), 0);
-    for (int i = 0; i < L.n; ++i) {
+    parallel_for(L.n, threads, [&](int i) {  // block (i, k) belongs to row i: rows write disjoint flags
       int last = -1;
       for (const Triple& t : rows[l][i].t) {
         if (t.k == last) continue;
         last = t.k;
         if (status_of(P.lv, l, i, t.k) == kSubTarget) has[find_block(L, i, t.k)] = 1;
       }
-    }
+    });
     if (l > 1) {  // children of the parent level's NL blocks (mmp.cpp:641-645)
       const LevelPlan& U = P.lv[l - 1];
       for (int32_t b : U.nl_block)
@@ -426,6 +444,7 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
         }
       }
     });
+    if (trace) stamp("    parts");
     Builder hqc;
     std::vector<std::vector<std::pair<int, int>>> hqc_rows;  // per B near: (i, A near)
     if (leaf) {
@@ -438,16 +457,60 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
                                 &Part::ff, &Part::fr, &Part::rf, &Part::rr, &Part::hq};
     Csr* dst[10] = {&L.ly, &L.lyr, &L.lyn, &L.xr, &L.ww, &L.ff, &L.fr, &L.rf, &L.rr, &L.hq};
     const int nout[10] = {nt, nt, nt, nt, nt, nnear, nnear, nnear, nnear, nnear};
-    parallel_for(leaf ? 10 : 5, threads, [&](int w) {
+    // Every list but hq is owned by targets numbered in (row, col) order inside three ranges
+    // (admissible, pending, NL; one range for the full-target lists), and every target's entries
+    // come from its own row, i.e. from one part: each part copies its entries of range c straight
+    // to the final position (ranges in order, parts in row order inside a range) and counts its
+    // own targets' row pointers — no concatenation, no sort, parallel over parts.
+    for (int w = 0; w < (leaf ? 9 : 5); ++w) {
+      const int no = nout[w];
+      const int c0 = w < 5 ? na : no, c1 = w < 5 ? na + np : no;
+      auto cat = [&](int32_t o) { return o < c0 ? 0 : (o < c1 ? 1 : 2); };
+      std::vector<std::array<size_t, 3>> cnt(T);
+      parallel_for(T, threads, [&](int pt) {
+        cnt[pt] = {0, 0, 0};
+        for (int32_t o : (parts[pt].*which[w]).owner) cnt[pt][cat(o)]++;
+      });
+      std::vector<std::array<size_t, 3>> at(T);
+      size_t run = 0;
+      for (int c = 0; c < 3; ++c)
+        for (int pt = 0; pt < T; ++pt) {
+          at[pt][c] = run;
+          run += cnt[pt][c];
+        }
+      if (run > size_t(INT32_MAX))
+        throw std::length_error("structure plan: " + std::to_string(run) +
+                                " entries in one CSR list exceed the int32 index range");
+      Csr& out = *dst[w];
+      out.li.resize(run);
+      out.ri.resize(run);
+      out.ptr.assign(no + 1, 0);
+      parallel_for(T, threads, [&](int pt) {
+        Builder& B = parts[pt].*which[w];
+        auto pos = at[pt];
+        for (size_t e = 0; e < B.owner.size(); ++e) {
+          const size_t d = pos[cat(B.owner[e])]++;
+          out.li[d] = B.csr.li[e];
+          out.ri[d] = B.csr.ri[e];
+          out.ptr[B.owner[e] + 1]++;  // the target's entries all come from this part
+        }
+        B = Builder{};
+      });
+      for (int o = 0; o < no; ++o) out.ptr[o + 1] += out.ptr[o];
+    }
+    if (leaf) {  // hq is owned by A's near block (i, j): not ordered along the rows -> general sort
       Builder all;
       for (Part& Pt : parts) {
-        all.append(Pt.*which[w]);
-        Pt.*which[w] = Builder{};
+        all.append(Pt.hq);
+        Pt.hq = Builder{};
       }
-      *dst[w] = all.done(nout[w]);
-    });
+      L.hq = all.done(nnear);
+    }
     parts.clear();
-    if (trace && leaf) stamp("  leaf lists");
+    if (trace) {
+      stamp("    lists");
+      for (int w = 0; w < (leaf ? 10 : 5); ++w) std::fprintf(stderr, "      list %d: %zu entries\n", w, dst[w]->li.size());
+    }
     if (leaf) {
       // hq entries per A near block were added in (i, k asc, j asc) order:
       // per (i,j) the k's are ascending
@@ -471,14 +534,16 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
       L.row_near = rn.done(L.n);
       L.col_near = cn.done(L.n);
     }
+    if (trace) stamp("    near");
     if (!leaf) {
       const int nm = static_cast<int>(L.merged_row.size());
       L.merged_target.resize(nm);
       Builder mg, rm, cm;
-      std::vector<int32_t> order(nm);
-      for (int m = 0; m < nm; ++m) {
+      parallel_for(nm, threads, [&](int m) {
         const Status s = status_of(P.lv, l, L.merged_row[m], L.merged_col[m]);
         L.merged_target[m] = slot_of(L.merged_row[m], L.merged_col[m], s);
+      });
+      for (int m = 0; m < nm; ++m) {
         mg.add(L.merged_target[m], m, L.merged_col[m]);
         rm.add(L.merged_row[m], m, m);
       }
@@ -501,6 +566,7 @@ Plan build_plan(const h2c_tree& tree, const h2c_blocks& blocks, int threads) {
       }
       L.row_merged = rm.done(L.n);
       L.col_merged = cm.done(L.n);
+      if (trace) stamp("    merged");
       // children of subdivided blocks
       const LevelPlan& C = P.lv[l + 1];
       L.sub_child.assign(4 * nnear, -1);
