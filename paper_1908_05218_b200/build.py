@@ -83,7 +83,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
             _run(["g++", *CXX_FLAGS, "-c", str(s), "-o", str(o)])
         objs.append(o)
     if force or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-lcusolver", "-lcublas", *_host_blas(),
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", *_host_blas(),
               "-Xcompiler", "-pthread"])
     return LIB
 

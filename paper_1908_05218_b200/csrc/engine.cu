@@ -23,7 +23,6 @@
 // G1 = sum_{j,k} (F F)(F F)^H is evaluated as sum_j F_ij (sum_k F_jk F_jk^H) F_ij^H.
 #include <cuda_runtime.h>
 #include <cuda.h>
-#include <cusolverDn.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
@@ -1278,7 +1277,7 @@ struct EngineRun : Relief {
     DBuf G;  // eigensolve input (deferred library solve / kept until the solve is joined)
     DBuf hV, hZ, hSlab;  // heev workspaces
     DVec<int> fail;      // heev: a QL iteration did not converge
-    bool side = false;   // solved on side stream 1 (joined in finish_async)
+    bool side = false;   // solved on side stream 1 (joined in finish_side)
     int n = 0, count = 0;
   };
   Trunc truncate(DBuf& g1, DBuf& g2, DBuf& g3, int count, int n, const DVec<uint8_t>& opdeg, bool defer = false) {
@@ -1316,18 +1315,8 @@ struct EngineRun : Relief {
     t.vec.alloc(sz(count, n, n), s);
     t.val.alloc(size_t(count) * n, s);
     t.rank.alloc(count, s);
-    if (use_library) {  // A/B only: cuSOLVER's batched solver + eig_finalize
-      if (defer) {
-        t.G = std::move(G);  // solved later by solve_async (concurrently with the column side)
-        t.n = n;
-        t.count = count;
-      } else {
-        library_eig(G, count, n, t);
-      }
-      return t;
-    }
     // the engine's own solver (heev.cuh); a deferred (row-side) solve runs on side stream 1,
-    // concurrently with the column side, and is joined in finish_async
+    // concurrently with the column side, and is joined in finish_side
     cudaStream_t st = s;
     if (defer) {
       st = static_cast<cudaStream_t>(ctx.side_stream(1));
@@ -1342,8 +1331,6 @@ struct EngineRun : Relief {
 
   // the upper levels' row and column truncations run concurrently (side stream 1 + main)
   bool paired_solves = false;
-  // H2B_EIG_LIBRARY=1: cuSOLVER XsyevBatched instead of heev_kernel (A/B runs)
-  const bool use_library = std::getenv("H2B_EIG_LIBRARY") != nullptr;
 
   // Batched Hermitian eigensolver + truncation rule (heev.cuh).  Placement per launch, from
   // tools/heev_bench.cu on the B200 (profiles/r02/heev_*.txt):
@@ -1433,98 +1420,14 @@ struct EngineRun : Relief {
   // Runs a deferred library eigensolve on side stream 1 in a host thread, so
   // the row and column eigensolves of a level overlap (cuSOLVER's batched
   // solver is launch-latency bound).
-  // Library eigensolver buffers, allocated on the calling (main) thread from the
-  // main-stream arena so a solve on a side stream never needs pool memory
-  // outside it; released on the main thread after the solve has completed.
-  struct EigWork {
-    DBuf V, w, work;
-    DVec<int> info;
-    size_t dev_bytes = 0, host_bytes = 0;
-  };
-  static void cusolver_check(cusolverStatus_t st, const char* what) {
-    if (st != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string("cuSOLVER ") + what + " failed: " + std::to_string(int(st)));
-  }
-  void prepare_eig(EigWork& wk, int count, int n, cusolverDnHandle_t h) {
-    wk.V.alloc(sz(count, n, n), s);
-    wk.w.alloc(size_t(count) * n, s);
-    wk.info.alloc(count, s);
-    const cudaDataType dt = cplx ? CUDA_C_64F : CUDA_R_64F;
-    cusolver_check(cusolverDnXsyevBatched_bufferSize(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt,
-                                                     wk.V.p, n, CUDA_R_64F, wk.w.p, dt, &wk.dev_bytes, &wk.host_bytes,
-                                                     count),
-                   "syevBatched_bufferSize");
-    wk.work.alloc(wk.dev_bytes / sizeof(double) + 2, s);
-  }
-
-  // Runs a deferred library eigensolve on side stream 1 in a host thread, so
-  // the row and column eigensolves of a level overlap (cuSOLVER's batched
-  // solver is launch-latency bound).
-  std::thread solve_async(Trunc& t, EigWork& wk, std::exception_ptr& err) {
-    if (!t.G.p || t.side || !use_library) return std::thread();
-    cudaStream_t st = static_cast<cudaStream_t>(ctx.side_stream(1));
-    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.side_solver(1));
-    prepare_eig(wk, t.count, t.n, h);
-    CK(cudaEventRecord(ev_fork, s));
-    CK(cudaStreamWaitEvent(st, ev_fork, 0));
-    CK(cudaSetDevice(ctx.device()));
-    return std::thread([this, &t, &wk, &err, st, h] {
-      try {
-        CK(cudaSetDevice(ctx.device()));
-        library_eig_on(t.G, t.count, t.n, t, st, h, wk);
-      } catch (...) {
-        err = std::current_exception();
-      }
-    });
-  }
-  void finish_async(std::thread& th, std::exception_ptr& err, Trunc& t, EigWork& wk) {
-    if (th.joinable()) th.join();  // the solve ended with a synchronize of its stream
-    if (err) std::rethrow_exception(err);
-    if (t.side) {  // heev on side stream 1: the main stream waits for it
+  // joins the row-side eigensolve (heev on side stream 1): the main stream waits for it
+  void finish_side(Trunc& t) {
+    if (t.side) {
       CK(cudaEventRecord(ev_side, static_cast<cudaStream_t>(ctx.side_stream(1))));
       CK(cudaStreamWaitEvent(s, ev_side, 0));
       t.side = false;
     }
     t.G.release();
-    wk = EigWork{};
-  }
-
-  // A/B only (H2B_EIG_LIBRARY=1): cuSOLVER batched solver (upper levels, where C's
-  // ranks grow): batched Hermitian eigensolver from cuSOLVER, then the same
-  // truncation rule on the device.
-  void library_eig(const DBuf& G, int count, int n, Trunc& t) {
-    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(ctx.solver());
-    EigWork wk;
-    prepare_eig(wk, count, n, h);
-    library_eig_on(G, count, n, t, s, h, wk);
-  }
-  void library_eig_on(const DBuf& G, int count, int n, Trunc& t, cudaStream_t s, cusolverDnHandle_t h, EigWork& wk) {
-    const bool main_thread = s == this->s;
-    CK(cudaMemcpyAsync(wk.V.p, G.p, sz(count, n, n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    const cudaDataType dt = cplx ? CUDA_C_64F : CUDA_R_64F;
-    if (main_thread) pre("syev_batched", 0);
-    {
-      std::vector<char> hwork(wk.host_bytes + 1);
-      cusolver_check(cusolverDnXsyevBatched(h, nullptr, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dt, wk.V.p,
-                                            n, CUDA_R_64F, wk.w.p, dt, wk.work.p, wk.dev_bytes, hwork.data(),
-                                            wk.host_bytes, wk.info.p, count),
-                     "syevBatched");
-      CK(cudaStreamSynchronize(s));  // host workspace lifetime
-      std::vector<int> hinfo(count);
-      CK(cudaMemcpy(hinfo.data(), wk.info.p, count * sizeof(int), cudaMemcpyDeviceToHost));
-      for (int b = 0; b < count; ++b)
-        if (hinfo[b] != 0)
-          throw std::logic_error("svd_truncate_gram: eigendecomposition failed (syev info " + std::to_string(hinfo[b]) + ")");
-    }
-    if (main_thread) post();  // library kernels are not counted in `launches`
-    if (main_thread) pre("eig_finalize", 0);
-    if (cplx)
-      eig_finalize_kernel<true><<<count, 256, 0, s>>>(G, wk.V, wk.w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
-    else
-      eig_finalize_kernel<false><<<count, 256, 0, s>>>(G, wk.V, wk.w, n, jp_eps(), t.vec, t.val, t.rank.p, t.degen.p);
-    CK(cudaGetLastError());
-    if (main_thread) post();
-    launches++;
-    CK(cudaStreamSynchronize(s));  // the buffers are released by the main thread after this
   }
   double jp_eps() const { return adaptive ? eps : 0.5; }
 
@@ -2102,9 +2005,6 @@ struct EngineRun : Relief {
                 nullptr}});
       paired_solves = true;
       Trunc tr = truncate(g1, g2, g3, n, 2 * Kn, A.dgr_d[l], /*defer=*/true);
-      std::exception_ptr row_err;
-      EigWork row_wk;
-      std::thread row_th = solve_async(tr, row_wk, row_err);
       // column transfer Gram (mmp.cpp:459-512)
       DBuf c1(sz(n, 2 * Kq, 2 * Kq), s), c2(sz(n, 2 * Kq, 2 * Kq), s), c3(sz(n, 2 * Kq, 2 * Kq), s);
       segh(c1, 2 * Kq, n,
@@ -2115,14 +2015,8 @@ struct EngineRun : Relief {
       segh(c3, 2 * Kq, n,
            {Grp{ref(X3c, 2LL * Kq * KBc, 2 * Kq, OP_N), ref(X3c, 2LL * Kq * KBc, 2 * Kq, OP_H), KBc, nullptr, nullptr,
                 nullptr}});
-      Trunc tc;
-      try {
-        tc = truncate(c1, c2, c3, n, 2 * Kq, B.dgc_d[l]);
-      } catch (...) {
-        if (row_th.joinable()) row_th.join();
-        throw;
-      }
-      finish_async(row_th, row_err, tr, row_wk);
+      Trunc tc = truncate(c1, c2, c3, n, 2 * Kq, B.dgc_d[l]);
+      finish_side(tr);
       paired_solves = false;
       KCr[l] = fetch_ranks(tr, n, rcr[l]);
       KCc[l] = fetch_ranks(tc, n, rcc[l]);
@@ -2573,16 +2467,6 @@ Context::Context(int device) : device_(device) {
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
 }
 
-void* Context::solver() {
-  if (!solver_) {
-    cusolverDnHandle_t h;
-    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
-    cusolverDnSetStream(h, static_cast<cudaStream_t>(stream_));
-    solver_ = h;
-  }
-  return solver_;
-}
-
 // Auxiliary stream on a green context with H2B_AUX_SMS SMs (0 / unset or >= the
 // device's count: no partition, the default — on cfg2 the partition measured no
 // better than stream priorities alone, profiles/r01/ab_defer_partition.txt).
@@ -2630,34 +2514,23 @@ void* Context::make_aux_stream(int priority) {
 }
 
 void* Context::side_stream(int i) {
-  side_solver(i);
-  return side_streams_[i];
-}
-
-void* Context::side_solver(int i) {
-  if (side_solvers_.empty()) {
+  if (side_streams_.empty()) {
     int least = 0, greatest = 0;
     CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     for (int k = 0; k < kSideStreams; ++k) {
       cudaStream_t st = k == 0 ? static_cast<cudaStream_t>(make_aux_stream(least)) : nullptr;
       if (!st) CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, k == 0 ? least : greatest));
-      cusolverDnHandle_t h;
-      if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
-      cusolverDnSetStream(h, st);
       side_streams_.push_back(st);
-      side_solvers_.push_back(h);
     }
   }
-  return side_solvers_[i];
+  return side_streams_[i];
 }
 
 Context::~Context() {
   if (stream_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
-  for (void* h : side_solvers_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(h));
   for (void* st : side_streams_) cudaStreamDestroy(static_cast<cudaStream_t>(st));
   if (green_ctx_ && green_destroy_)
     reinterpret_cast<decltype(&cuGreenCtxDestroy)>(green_destroy_)(static_cast<CUgreenCtx>(green_ctx_));
-  if (solver_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_));
   dplan_.reset();
   if (stream_) {
     cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
@@ -2771,7 +2644,11 @@ Arena* Context::arena() {
     const size_t reserve = size_t(4) << 30;
     if (fr > reserve + (size_t(4) << 30)) {
       auto* a = new Arena;
-      if (a->init(fr - reserve)) D.arena = a;
+      size_t want = fr - reserve;
+      // H2B_ARENA_GB caps the arena (ncu's kernel replay saves and restores device memory and
+      // needs room for its copy; the product then runs with the eviction path if it must)
+      if (const char* e = std::getenv("H2B_ARENA_GB")) want = std::min(want, size_t(std::atof(e) * double(size_t(1) << 30)));
+      if (a->init(want)) D.arena = a;
       else delete a;
     }
   }

@@ -88,10 +88,9 @@ class Context {
   void to_dense(const std::shared_ptr<DevOperand>& a, double* out);
   void* stream() const { return stream_; }
   int device() const { return device_; }
-  void* solver();  // cusolverDn handle bound to the stream (lazy)
   struct Arena* arena();  // large-buffer arena of the device, shared by every Context (lazy)
   std::recursive_mutex& call_mutex();  // serialises calls on the device (process-wide)
-  // side streams with their own cusolverDn handles.  0: auxiliary stream of
+  // side streams.  0: auxiliary stream of
   // the off-critical-path work (leaf full targets, deferred coupling-target
   // sums) at low priority, optionally bound to a green context holding a
   // subset of the SMs (H2B_AUX_SMS) so the critical path keeps SMs of its own;
@@ -99,7 +98,6 @@ class Context {
   static constexpr int kSideStreams = 2;
   int aux_sms() const { return aux_sms_; }
   void* side_stream(int i);
-  void* side_solver(int i);
   void* make_aux_stream(int priority);
   int64_t last_kernel_launches() const { return launches_; }
   std::shared_ptr<PinnedPool> pinned = std::make_shared<PinnedPool>();
@@ -111,8 +109,7 @@ class Context {
   friend struct EngineRun;
   int device_;
   void* stream_ = nullptr;
-  void* solver_ = nullptr;
-  std::vector<void*> side_streams_, side_solvers_;
+  std::vector<void*> side_streams_;
   void* green_ctx_ = nullptr;
   void* green_destroy_ = nullptr;
   int aux_sms_ = 0;  // SMs of the auxiliary stream's green context (0: whole device)

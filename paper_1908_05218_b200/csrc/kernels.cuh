@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
 
 // ---------------------------------------------------------------------------
 // seg_add: out_t = sum_{e in seg(t)} in[idx_e]   (elements = matrix size in doubles)
-__global__ void seg_add_kernel(double* out, long long Os, const double* in, long long Is,
+static __global__ void seg_add_kernel(double* out, long long Os, const double* in, long long Is,
                                const int* ptr, const int* idx, long long elems, int accumulate) {
   const int t = blockIdx.x;
   const int e0 = ptr[t], e1 = ptr[t + 1];
@@ -566,47 +566,9 @@ __global__ void __launch_bounds__(256) gram_combine_grid_kernel(const double* g1
 }
 
 // ---------------------------------------------------------------------------
-// Finalize a library eigendecomposition (ascending eigenvalues, eigenvectors
-// in columns) into the truncation output of jacobi_kernel: clamp at 0, sort
-// descending, strict threshold, >= 1 vector, e_1 for exactly-zero Grams
-// (truncation.cpp:23-45).
-template <bool CPLX>
-__global__ void eig_finalize_kernel(const double* G, const double* V, const double* w, int n, double eps,
-                                    double* vec_out, double* val_out, int* rank_out, uint8_t* degen_io) {
-  constexpr int W = CPLX ? 2 : 1;
-  const int b = blockIdx.x;
-  const double* g = G + (size_t)b * n * n * W;
-  const double* v = V + (size_t)b * n * n * W;
-  const double* wb = w + (size_t)b * n;
-  __shared__ int nz;
-  if (threadIdx.x == 0) nz = 0;
-  __syncthreads();
-  int mine = 0;
-  for (int x = threadIdx.x; x < n * n * W; x += blockDim.x) mine |= g[x] != 0.0;
-  if (__syncthreads_or(mine) && threadIdx.x == 0) nz = 1;
-  __syncthreads();
-  const double top = fmax(wb[n - 1], 0.0);
-  const bool unit = !nz || !(top > 0.0);
-  double* vo = vec_out + (size_t)b * n * n * W;
-  // descending order = reversed ascending order (ties keep LAPACK's order reversed, as Eigen's reverse())
-  for (int x = threadIdx.x; x < n * n * W; x += blockDim.x) {
-    const int e = x / W, q = x % W;
-    const int r = e % n, c = e / n;
-    vo[x] = unit ? ((q == 0 && r == 0 && c == 0) ? 1.0 : 0.0) : v[(r + (size_t)(n - 1 - c) * n) * W + q];
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) val_out[(size_t)b * n + i] = fmax(wb[n - 1 - i], 0.0);
-  if (threadIdx.x == 0) {
-    int r = 0;
-    while (r < n && fmax(wb[n - 1 - r], 0.0) > eps * top) ++r;
-    rank_out[b] = unit ? 1 : (r < 1 ? 1 : r);
-    degen_io[b] = (unit ? 1 : 0) | degen_io[b];
-  }
-}
-
-// ---------------------------------------------------------------------------
 // pack sorted eigenvectors (n x n) into a padded basis (rows x KC), zeroing
 // columns at and beyond the rank
-__global__ void pack_basis_kernel(const double* vec, int n, double* out, int rows, int kc,
+static __global__ void pack_basis_kernel(const double* vec, int n, double* out, int rows, int kc,
                                   const int* rank, int W) {
   const int b = blockIdx.x;
   const int r = rank[b];
@@ -622,7 +584,7 @@ __global__ void pack_basis_kernel(const double* vec, int n, double* out, int row
 // ---------------------------------------------------------------------------
 // copy compact R x C blocks cp[e] into quadrant oquad[e] & 3 of the 2R x 2C block
 // oquad[e] >> 2 of `out` (the parents' merged blocks, mmp.cpp:344-365)
-__global__ void scatter_quad_kernel(double* const* och, int osh, const double* const* cpch, int cpsh,
+static __global__ void scatter_quad_kernel(double* const* och, int osh, const double* const* cpch, int cpsh,
                                     const int* oquad, int R, int Cc, int W) {
   const int e = blockIdx.x;
   const int v = oquad[e];
@@ -645,7 +607,7 @@ struct CopyJob {
   double* dst;
   int rows, cols, sld, dld;
 };
-__global__ void copy_jobs_kernel(const CopyJob* jobs, int W) {
+static __global__ void copy_jobs_kernel(const CopyJob* jobs, int W) {
   const CopyJob j = jobs[blockIdx.x];
   const long long total = (long long)j.rows * j.cols * W;
   for (long long x = threadIdx.x; x < total; x += blockDim.x) {
@@ -657,7 +619,7 @@ __global__ void copy_jobs_kernel(const CopyJob* jobs, int W) {
 }
 
 // MVP: original-order vectors <-> leaf blocks in tree order (padded)
-__global__ void mvp_gather_kernel(const double* X, int N, int nv, const int* perm, const int* beg, const int* size,
+static __global__ void mvp_gather_kernel(const double* X, int N, int nv, const int* perm, const int* beg, const int* size,
                                   double* XL, int NL, int NV, int W) {
   const int p = blockIdx.x;
   double* o = XL + (size_t)p * NL * NV * W;
@@ -667,7 +629,7 @@ __global__ void mvp_gather_kernel(const double* X, int N, int nv, const int* per
     o[(r + (size_t)v * NL) * W + w] = X[(perm[beg[p] + r] + (size_t)v * N) * W + w];
   }
 }
-__global__ void mvp_scatter_kernel(const double* YL, int NL, int NV, const int* perm, const int* beg, const int* size,
+static __global__ void mvp_scatter_kernel(const double* YL, int NL, int NV, const int* perm, const int* beg, const int* size,
                                    double* Y, int N, int nv, int W) {
   const int p = blockIdx.x;
   const double* i_ = YL + (size_t)p * NL * NV * W;
@@ -680,12 +642,12 @@ __global__ void mvp_scatter_kernel(const double* YL, int NL, int NV, const int* 
 
 // identity matrices (formatted product: P = I, mmp.cpp:280-283)
 // columns c0 .. c0+cw-1 of the N x N identity into a zeroed N x cw panel
-__global__ void unit_columns_kernel(double* X, int N, int c0, int cw, int W) {
+static __global__ void unit_columns_kernel(double* X, int N, int c0, int cw, int W) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < cw) X[(size_t(c0 + j) + size_t(j) * N) * W] = 1.0;
 }
 
-__global__ void set_identity_kernel(double* out, int n, int ld, const int* rank, int W) {
+static __global__ void set_identity_kernel(double* out, int n, int ld, const int* rank, int W) {
   const int b = blockIdx.x;
   double* o = out + (size_t)b * n * ld * W;
   for (int x = threadIdx.x; x < n * ld * W; x += blockDim.x) {

@@ -287,11 +287,10 @@ def test_device_constructor_matches_host(name, monkeypatch):
         assert rel(dd, dh) <= 1e-11, rel(dd, dh)
 
 
-@pytest.mark.parametrize("knob", ["H2B_CPLX4M", "H2B_NO_STRIPS_SMALL", "H2B_STRIPS_24", "H2B_EIG_LIBRARY"])
+@pytest.mark.parametrize("knob", ["H2B_CPLX4M", "H2B_NO_STRIPS_SMALL", "H2B_STRIPS_24"])
 @pytest.mark.parametrize("name", ["cfg3", "cfg5"])
 def test_small_tile_kernels_match_oracle(ctx, name, knob, monkeypatch):
-    """The A/B variants (4-product complex DMMA, strip splits, cuSOLVER instead of the engine's
-    eigensolver) on the small-rank bench constructions: oracle parity, bit-identical repeats and
+    """The A/B variants (4-product complex DMMA, strip splits) on the small-rank bench constructions: oracle parity, bit-identical repeats and
     the same ranks as the default path."""
     import bench
     _, _, _, A, B = bench.build_operands(name, 4096)

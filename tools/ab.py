@@ -25,7 +25,7 @@ else:
     s = P.build_block_tree(t, t, 1.0)
     A = B = P.build_chebyshev(t, s, pts, order)
     specs = sys.argv[5:]
-KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_EIG_LIBRARY", "H2B_NO_STRIPS", "H2B_CPLX4M", "H2B_SYM_T64",
+KNOBS = ("H2B_AUX_SMS", "H2B_NO_DEFER", "H2B_NO_STRIPS", "H2B_CPLX4M", "H2B_SYM_T64",
          "H2B_NO_STRIPS_SMALL", "H2B_STRIPS_24", "H2B_STRIPS_SMALL_MAX")
 for spec in specs:
     label, _, kv = spec.partition(":")
