@@ -4,10 +4,15 @@
 // the product path).  flatten()/unflatten() translate to the C-ABI layout.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
+#include <new>
+#include <thread>
+#include <utility>
 #include <vector>
 
 #include "h2mmp/block_tree.hpp"
@@ -44,15 +49,35 @@ struct H2Matrix {
 
 namespace detail {
 
-// Flat copy of an H2Matrix in the layout of h2c_types.h (owning buffers).
+// Flat copy of an H2Matrix in the layout of h2c_types.h (owning buffers).  The values live in one
+// uninitialised allocation (no zero fill of several GB) filled by parallel copies.
 template <class Scalar>
 struct Flat {
   std::vector<int32_t> row_rank, col_rank;
   std::vector<uint8_t> row_dg, col_dg;
   std::vector<int64_t> row_off, col_off, block_off;
-  std::vector<Scalar> values;
+  struct FreeDeleter {
+    void operator()(void* p) const { std::free(p); }
+  };
+  std::unique_ptr<Scalar, FreeDeleter> values;
   h2c_matrix desc{};
 };
+
+// f(k) for k in [0, n) on the host's hardware threads (contiguous ranges)
+template <class F>
+void parallel_ranges(int64_t n, F&& f) {
+  const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), n / 64));
+  if (nt <= 1) {
+    for (int64_t k = 0; k < n; ++k) f(k);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int64_t w = 0; w < nt; ++w)
+    th.emplace_back([&, w] {
+      for (int64_t k = n * w / nt; k < n * (w + 1) / nt; ++k) f(k);
+    });
+  for (auto& x : th) x.join();
+}
 
 template <class Scalar>
 Flat<Scalar> flatten(const H2Matrix<Scalar>& h) {
@@ -60,10 +85,12 @@ Flat<Scalar> flatten(const H2Matrix<Scalar>& h) {
   const BlockTree& bt = *h.structure;
   const int nc = static_cast<int>(t.clusters.size());
   Flat<Scalar> f;
+  // pass 1: offsets and sources; pass 2: parallel copies into one allocation
+  std::vector<std::pair<const DenseMatrix<Scalar>*, int64_t>> jobs;
   int64_t n = 0;
   auto add = [&](const DenseMatrix<Scalar>& m) {
     const int64_t at = n;
-    f.values.insert(f.values.end(), m.data(), m.data() + m.size());
+    jobs.emplace_back(&m, at);
     n += m.size();
     return at;
   };
@@ -90,9 +117,16 @@ Flat<Scalar> flatten(const H2Matrix<Scalar>& h) {
     if (d.kind[k] == H2C_ADMISSIBLE) f.block_off[k] = add(h.coupling.at(key));
     else if (d.kind[k] == H2C_INADMISSIBLE_LEAF) f.block_off[k] = add(h.full.at(key));
   }
+  f.values.reset(static_cast<Scalar*>(std::malloc(std::max<size_t>(1, sizeof(Scalar) * static_cast<size_t>(n)))));
+  if (!f.values) throw std::bad_alloc();
+  Scalar* dst = f.values.get();
+  parallel_ranges(static_cast<int64_t>(jobs.size()), [&](int64_t k) {
+    const DenseMatrix<Scalar>& m = *jobs[k].first;
+    if (m.size()) std::memcpy(static_cast<void*>(dst + jobs[k].second), m.data(), sizeof(Scalar) * m.size());
+  });
   f.desc = h2c_matrix{&t.desc, &bt.desc, is_complex_v<Scalar> ? H2C_COMPLEX : H2C_REAL, f.row_rank.data(),
                       f.col_rank.data(), f.row_dg.data(), f.col_dg.data(), f.row_off.data(), f.col_off.data(),
-                      f.block_off.data(), reinterpret_cast<const double*>(f.values.data()), n};
+                      f.block_off.data(), reinterpret_cast<const double*>(dst), n};
   return f;
 }
 
@@ -111,6 +145,14 @@ H2Matrix<Scalar> unflatten(const h2c_matrix& d, std::shared_ptr<const ClusterTre
   h.structure = std::move(structure);
   const ClusterTree& t = *h.tree;
   const int nc = static_cast<int>(t.clusters.size());
+  // pass 1 (serial): the containers and the (destination, offset, shape) of every matrix;
+  // pass 2 (parallel): allocate and copy
+  struct Job {
+    DenseMatrix<Scalar>* dst;
+    int64_t off;
+    Index r, c;
+  };
+  std::vector<Job> jobs;
   for (int side = 0; side < 2; ++side) {
     ClusterBasis<Scalar>& b = side == 0 ? h.row_basis : h.col_basis;
     const int32_t* rk = side == 0 ? d.row_rank : d.col_rank;
@@ -122,18 +164,22 @@ H2Matrix<Scalar> unflatten(const h2c_matrix& d, std::shared_ptr<const ClusterTre
       b.degenerate[c] = dg[c];
       const Cluster& cl = t.clusters[c];
       if (off[c] < 0) continue;
-      if (cl.is_leaf()) b.leaf[c] = read<Scalar>(d, off[c], cl.size(), rk[c]);
-      else b.transfer[c] = read<Scalar>(d, off[c], rk[cl.child[0]] + rk[cl.child[1]], rk[c]);
+      if (cl.is_leaf()) jobs.push_back({&b.leaf[c], off[c], cl.size(), rk[c]});
+      else jobs.push_back({&b.transfer[c], off[c], rk[cl.child[0]] + rk[cl.child[1]], rk[c]});
     }
   }
   const h2c_blocks& bd = h.structure->desc;
   for (int64_t k = 0; k < bd.n_blocks; ++k) {
     const BlockKey key{bd.row[k], bd.col[k]};
     if (bd.kind[k] == H2C_ADMISSIBLE)
-      h.coupling[key] = read<Scalar>(d, d.block_offset[k], d.row_rank[key.row], d.col_rank[key.col]);
+      jobs.push_back({&h.coupling[key], d.block_offset[k], d.row_rank[key.row], d.col_rank[key.col]});
     else if (bd.kind[k] == H2C_INADMISSIBLE_LEAF)
-      h.full[key] = read<Scalar>(d, d.block_offset[k], t.clusters[key.row].size(), t.clusters[key.col].size());
+      jobs.push_back({&h.full[key], d.block_offset[k], t.clusters[key.row].size(), t.clusters[key.col].size()});
   }
+  parallel_ranges(static_cast<int64_t>(jobs.size()), [&](int64_t k) {
+    const Job& j = jobs[k];
+    *j.dst = read<Scalar>(d, j.off, j.r, j.c);
+  });
   return h;
 }
 

@@ -58,16 +58,17 @@ struct SegParams {
   SegGroup g[kMaxGroups];
 };
 
-// address of output t's block (W = scalars per element)
-__device__ __forceinline__ double* seg_out_ptr(const SegParams& p, int t, int W) {
-  long long blk, extra = 0;
+// storage word of output t: oquad[t] (block << 2 | quadrant), omap[t] or t itself
+__device__ __forceinline__ int seg_out_word(const SegParams& p, int t) {
+  return p.oquad ? p.oquad[t] : (p.omap ? p.omap[t] : t);
+}
+// address of the output block with storage word v (W = scalars per element)
+__device__ __forceinline__ double* seg_out_ptr(const SegParams& p, int v, int W) {
+  long long blk = v, extra = 0;
   if (p.oquad) {
-    const int v = p.oquad[t];
     const int q = v & 3;
     blk = v >> 2;
     extra = (q >> 1) * p.qm + (long long)((q & 1) * p.qn) * p.Old;
-  } else {
-    blk = p.omap ? p.omap[t] : t;
   }
   if (p.och)
     return p.och[blk >> p.osh] + (p.Os * (blk & ((1LL << p.osh) - 1)) + p.Ooff + extra) * W;
@@ -127,6 +128,27 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// operand indices of entries [qb, qb + cap) of output t's concatenated entry list (groups in
+// order) into shared memory; ge = (e0, e1) per group.  Out of line: the refill inside the copy path
+// is rare and must not raise the register pressure of the main loop.
+static __device__ __noinline__ void seg_fill_idx(const SegParams& p, int t, int qb, int tid, int nt, int cap,
+                                                 const int* ge, int* s_li, int* s_ri) {
+  for (int x = tid; x < cap; x += nt) {
+    int q = qb + x;
+    for (int g = 0; g < p.ngroups; ++g) {
+      const int cnt = ge[2 * g + 1] - ge[2 * g];
+      if (q < cnt) {
+        const SegGroup& G = p.g[g];
+        const int e = ge[2 * g] + q;
+        s_li[x] = G.ptr ? G.li[e] : (G.li ? G.li[t] : t);
+        s_ri[x] = G.ptr ? G.ri[e] : (G.ri ? G.ri[t] : t);
+        break;
+      }
+      q -= cnt;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // seg_gemm v3: the v2 pipeline with the per-chunk integer work taken out of the
 // loop (profiles/r01/ncu_seg_gemm2_8x4_source.txt: v2 issued ~10 integer /
@@ -144,7 +166,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // s_b = b + bi: P = sum s_a b, R = sum a d_b, Q = sum ai s_b; Re = P - Q, Im = P + R
 // (3 DMMAs instead of 4, one more accumulator set).
 template <int TM, int TN, bool CPLX, int KC_ = 8, int ST_ = 4, int WM_ = 2, int WN_ = 2, bool G3 = false>
-__global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegParams p) {
+__global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const __grid_constant__ SegParams p) {
   using C = Seg2Cfg<TM, TN, CPLX, KC_, ST_, WM_, WN_>;
   constexpr int NT = C::NT;
   constexpr int KC = C::KC, W = C::W, ST = C::STAGES;
@@ -196,8 +218,43 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
       for (int j = 0; j < C::FN; ++j) acci[i][j][0] = acci[i][j][1] = 0.0;
   }
 
+  // ---- index prefetch: the CSR ranges of every group, the output's storage word and the first
+  // kIdx entries' operand indices are fetched in two parallel rounds (ranges, then indices) into
+  // shared memory, instead of one dependent global load per group and per entry in the copy path
+  // (a 2-group, 2-entry output paid ptr -> li -> data -> ptr -> li -> data -> omap -> C: six
+  // serial round trips; now ranges -> indices -> data, with the accumulate lines prefetched)
+  // (not in the 64 x 64 complex 3-product instantiation: its 192 accumulator registers leave no
+  // room, and with >= 16 chunks per entry its index loads are hidden by the pipeline anyway)
+  constexpr bool PF = !(CPLX && G3 && TM == 64 && TN == 64);
+  constexpr int kIdx = PF ? 64 : 1;
+  __shared__ int s_ge[PF ? 2 * kMaxGroups + 1 : 1];  // e0, e1 per group; [2 kMaxGroups] output word
+  __shared__ int s_li[kIdx], s_ri[kIdx];
+  if constexpr (PF) {
+    if (tid < 2 * p.ngroups) {
+      const int* ptr = p.g[tid >> 1].ptr;
+      s_ge[tid] = ptr ? ptr[t + (tid & 1)] : (tid & 1);
+    } else if (tid == 2 * kMaxGroups) {
+      s_ge[2 * kMaxGroups] = seg_out_word(p, t);
+    }
+    __syncthreads();
+  }
+  auto fill_idx = [&](int qb) { seg_fill_idx(p, t, qb, tid, NT, kIdx, s_ge, s_li, s_ri); };
+  if constexpr (PF) {
+    fill_idx(0);
+    if (p.accumulate) {  // the accumulate target's lines into L2 while the operands are fetched
+      const char* Ob = reinterpret_cast<const char*>(seg_out_ptr(p, s_ge[2 * kMaxGroups], W));
+      const int rows = min(TM, p.M - m0), cols = min(TN, p.N - n0);
+      const int lpc = (rows * 8 * W + 127) / 128;  // 128-byte lines per column
+      for (int x = tid; x < cols * lpc; x += NT) {
+        const char* a = Ob + ((long long)(m0 + (long long)(n0 + x / lpc) * p.Old)) * 8 * W + (x % lpc) * 128;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
+    __syncthreads();
+  }
+
   // ---- copy (producer) state: one chunk ahead of the consumer by ST-1 -------
-  int ig = 0, ie = 0, ie1 = 0, ikc = 0, inkc = 1;
+  int ig = 0, ie = 0, ie1 = 0, ikc = 0, inkc = 1, iq = 0, iqb = 0;
   bool iv = false;
   const double* lsrc[LPT];
   const double* rsrc[RPT];
@@ -205,13 +262,13 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
   bool lok[LPT], rok[RPT];
   long long lstep = 0, rstep = 0;
   auto range = [&](int g, int& e0, int& e1) {
-    const int* ptr = p.g[g].ptr;
-    if (ptr) {
-      e0 = ptr[t];
-      e1 = ptr[t + 1];
+    if constexpr (PF) {
+      e0 = s_ge[2 * g];
+      e1 = s_ge[2 * g + 1];
     } else {
-      e0 = 0;
-      e1 = 1;
+      const int* ptr = p.g[g].ptr;
+      e0 = ptr ? ptr[t] : 0;
+      e1 = ptr ? ptr[t + 1] : 1;
     }
   };
   auto setup_group = [&](int g) {  // per-thread copy geometry of group g
@@ -252,10 +309,20 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
     rstep = (rt ? (long long)KC * G.Rld : (long long)KC) * W;
     inkc = G.K / KC;
   };
-  auto setup_entry = [&]() {  // source pointers of entry ie of group ig
+  auto setup_entry = [&]() {  // source pointers of entry ie of group ig (the iq-th of the output)
     const SegGroup& G = p.g[ig];
     int l, r;
-    if (G.ptr) {
+    if constexpr (PF) {
+      if (iq - iqb == kIdx) {  // index cache exhausted (uniform over the CTA): next kIdx entries
+        __syncthreads();
+        iqb = iq;
+        fill_idx(iqb);
+        __syncthreads();
+      }
+      l = s_li[iq - iqb];
+      r = s_ri[iq - iqb];
+      ++iq;
+    } else if (G.ptr) {
       l = G.li[ie];
       r = G.ri[ie];
     } else {
@@ -408,7 +475,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
   }
   cp_async_wait<0>();
 
-  double* Op = seg_out_ptr(p, t, W);
+  double* Op = seg_out_ptr(p, PF ? s_ge[2 * kMaxGroups] : seg_out_word(p, t), W);
 #pragma unroll
   for (int i = 0; i < C::FM; ++i)
 #pragma unroll
