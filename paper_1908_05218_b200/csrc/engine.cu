@@ -918,6 +918,7 @@ struct EngineRun : Relief {
   };
   std::vector<Evicted> evicted;
   bool leaf_done = false;
+  bool splitting = false;
   Relief* prev_relief = nullptr;
   bool evict(DBuf& b, bool operand) {
     if (!b.p) return false;
@@ -945,6 +946,7 @@ struct EngineRun : Relief {
     if (!leaf_done) return false;
     if (evict(const_cast<DBuf&>(A.F), true)) return true;
     if (evict(const_cast<DBuf&>(B.F), true)) return true;
+    if (splitting) return false;  // the split accumulates into C's leaf stores
     if (evict(F, false)) return true;
     if (evict(Tg[D], false)) return true;
     return false;
@@ -1148,6 +1150,11 @@ struct EngineRun : Relief {
       const int64_t ent = g.csr ? g.csr->entries : n_out;
       bytes += ent * (int64_t(M) * g.K + int64_t(g.K) * N) * 8 * W;
     }
+    {
+      double ch = 0;
+      for (const Grp& g : gs) ch += double(g.csr ? g.csr->entries : n_out) * (g.K / 8);
+      cur_chunks = ch / n_out;
+    }
     pre("seg_gemm", macs, bytes);
     if (sym && (M != N || acc)) throw std::logic_error("seg: symmetric launch needs a square, fresh output");
     // Outputs wider than one 64 tile whose last tile row / column would be at
@@ -1214,8 +1221,52 @@ struct EngineRun : Relief {
     };
     return cost(32, 0.75) < cost(64, 1.0) ? 32 : 64;
   }
+  // seg_small (kernels.cuh): one warp per output, for outputs of at most 12 m8n8 fragments (e.g.
+  // 24 x 32; a 32 x 32 output needs 126 registers per lane and measured slower than seg_gemm3).
+  // Real products: sums of at most 4 8-deep k-chunks per output on average (48 for outputs of one
+  // or two fragments) - beyond that seg_gemm3's asynchronous pipeline wins; complex products
+  // (16-byte fragment loads): every such output.  profiles/r02/ab_seg_small.txt;
+  // H2B_SMALL_MAXCH overrides the chunk bound (0 disables the kernel).
+  const int small_max_chunks = [] {
+    const char* e = std::getenv("H2B_SMALL_MAXCH");
+    return e ? std::atoi(e) : -1;
+  }();
+  bool use_small(const SegParams& sp) const {
+    const int M = sp.M, N = sp.N;
+    if (sp.sym || M > 32 || N > 32 || M % 8 != 0 || N % 8 != 0 || M * N > 32 * 24) return false;
+    if (small_max_chunks >= 0) return cur_chunks <= small_max_chunks;
+    if (cplx) return true;
+    return cur_chunks <= (M * N <= 128 ? 48 : 4);
+  }
+  double cur_chunks = 1e30;  // average k-chunks per output of the launch being issued
+  template <int FM, int FN>
+  void launch_small_cfg(const SegParams& sp) {
+    const dim3 grid((sp.n_out + 3) / 4);
+    if (cplx) seg_small_kernel<FM, FN, true><<<grid, 128, 0, s>>>(sp);
+    else seg_small_kernel<FM, FN, false><<<grid, 128, 0, s>>>(sp);
+    CK(cudaGetLastError());
+    launches++;
+  }
+  template <int FM>
+  void launch_small_n(const SegParams& sp) {
+    switch (sp.N / 8) {
+      case 1: launch_small_cfg<FM, 1>(sp); break;
+      case 2: launch_small_cfg<FM, 2>(sp); break;
+      case 3: launch_small_cfg<FM, 3>(sp); break;
+      default: launch_small_cfg<FM, 4>(sp); break;
+    }
+  }
   void launch_tiles(const SegParams& sp) {
     const int M = sp.M, N = sp.N;
+    if (use_small(sp)) {
+      switch (M / 8) {
+        case 1: launch_small_n<1>(sp); break;
+        case 2: launch_small_n<2>(sp); break;
+        case 3: launch_small_n<3>(sp); break;
+        default: launch_small_n<4>(sp); break;
+      }
+      return;
+    }
     int TM = M <= 8 ? 8 : M <= 16 ? 16 : (M <= 32 ? 32 : 64);
     int TN = N <= 8 ? 8 : N <= 16 ? 16 : (N <= 32 ? 32 : 64);
     if (sp.sym && !sym_t64 && M > 32) TM = TN = sym_tile(M);
@@ -1335,9 +1386,9 @@ struct EngineRun : Relief {
   // Batched Hermitian eigensolver + truncation rule (heev.cuh).  Placement per launch, from
   // tools/heev_bench.cu on the B200 (profiles/r02/heev_*.txt):
   //  * n <= 96 (leaf Grams): one CTA per Gram, Gram in shared memory (2-3 CTAs per SM);
-  //  * many Grams (>= 64, or >= 32 with n <= 400: the batched middle levels): one CTA per Gram
-  //    with the Gram in a global (L2-resident) slab and ~20-50 KB of shared memory, so several
-  //    Grams share an SM and hide each other's latency-bound phases;
+  //  * 24 Grams or more (the batched middle levels): the Gram in a global (L2-resident) slab and
+  //    ~20-50 KB of shared memory, one CTA per Gram when there are enough Grams to fill the SMs,
+  //    else a cluster of 2-4 CTAs per Gram (column slabs, one wave of CTAs);
   //  * few large Grams: a cluster of CS CTAs per Gram (CS the smallest power of two whose
   //    column slabs fit the CTAs' shared memory, <= 16; global slabs beyond).
   // Workspaces come from the main-stream arena before the fork.
@@ -1355,11 +1406,15 @@ struct EngineRun : Relief {
       CS = 16;
       smem = false;
     }
-    // the row and column solves of a level run concurrently: size the decision on both
+    // the row and column solves of a level run concurrently: size the decision on both.
+    // From 24 Grams on, global slabs with the largest power-of-two cluster that still gives one
+    // wave of CTAs (eff * CS <= 160): e.g. 32 Grams of n = 624 take 26 ms with CS = 4 against
+    // 63 ms on 16-CTA shared-memory clusters and 79 ms with one CTA each; 64 Grams of n = 576
+    // 41 ms with CS = 2 against 72 ms with CS = 1 (profiles/r02/heev_sweep.txt).
     const int eff = paired_solves ? 2 * count : count;
-    const bool many = eff >= 64 || (eff >= 32 && n <= 400);
-    if (n > 96 && many) {
+    if (n > 96 && eff >= 24) {
       CS = 1;
+      while (CS < 16 && eff * CS * 2 <= 160) CS *= 2;
       smem = false;
     }
     const HeevLayout L(n, CS, cplx, smem);
@@ -2080,6 +2135,7 @@ struct EngineRun : Relief {
   void split() {
     join();
     restore(false);  // C's evicted leaf stores receive split contributions
+    splitting = true;
     mark("split");
     for (int l = 1; l < D; ++l) {
       const LevelPlan& L = P.lv[l];

@@ -58,17 +58,16 @@ struct SegParams {
   SegGroup g[kMaxGroups];
 };
 
-// storage word of output t: oquad[t] (block << 2 | quadrant), omap[t] or t itself
-__device__ __forceinline__ int seg_out_word(const SegParams& p, int t) {
-  return p.oquad ? p.oquad[t] : (p.omap ? p.omap[t] : t);
-}
-// address of the output block with storage word v (W = scalars per element)
-__device__ __forceinline__ double* seg_out_ptr(const SegParams& p, int v, int W) {
-  long long blk = v, extra = 0;
+// address of output t's block (W = scalars per element)
+__device__ __forceinline__ double* seg_out_ptr(const SegParams& p, int t, int W) {
+  long long blk, extra = 0;
   if (p.oquad) {
+    const int v = p.oquad[t];
     const int q = v & 3;
     blk = v >> 2;
     extra = (q >> 1) * p.qm + (long long)((q & 1) * p.qn) * p.Old;
+  } else {
+    blk = p.omap ? p.omap[t] : t;
   }
   if (p.och)
     return p.och[blk >> p.osh] + (p.Os * (blk & ((1LL << p.osh) - 1)) + p.Ooff + extra) * W;
@@ -128,27 +127,6 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// operand indices of entries [qb, qb + cap) of output t's concatenated entry list (groups in
-// order) into shared memory; ge = (e0, e1) per group.  Out of line: the refill inside the copy path
-// is rare and must not raise the register pressure of the main loop.
-static __device__ __noinline__ void seg_fill_idx(const SegParams& p, int t, int qb, int tid, int nt, int cap,
-                                                 const int* ge, int* s_li, int* s_ri) {
-  for (int x = tid; x < cap; x += nt) {
-    int q = qb + x;
-    for (int g = 0; g < p.ngroups; ++g) {
-      const int cnt = ge[2 * g + 1] - ge[2 * g];
-      if (q < cnt) {
-        const SegGroup& G = p.g[g];
-        const int e = ge[2 * g] + q;
-        s_li[x] = G.ptr ? G.li[e] : (G.li ? G.li[t] : t);
-        s_ri[x] = G.ptr ? G.ri[e] : (G.ri ? G.ri[t] : t);
-        break;
-      }
-      q -= cnt;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // seg_gemm v3: the v2 pipeline with the per-chunk integer work taken out of the
 // loop (profiles/r01/ncu_seg_gemm2_8x4_source.txt: v2 issued ~10 integer /
@@ -166,7 +144,7 @@ static __device__ __noinline__ void seg_fill_idx(const SegParams& p, int t, int 
 // s_b = b + bi: P = sum s_a b, R = sum a d_b, Q = sum ai s_b; Re = P - Q, Im = P + R
 // (3 DMMAs instead of 4, one more accumulator set).
 template <int TM, int TN, bool CPLX, int KC_ = 8, int ST_ = 4, int WM_ = 2, int WN_ = 2, bool G3 = false>
-__global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const __grid_constant__ SegParams p) {
+__global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegParams p) {
   using C = Seg2Cfg<TM, TN, CPLX, KC_, ST_, WM_, WN_>;
   constexpr int NT = C::NT;
   constexpr int KC = C::KC, W = C::W, ST = C::STAGES;
@@ -218,43 +196,8 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const __grid_
       for (int j = 0; j < C::FN; ++j) acci[i][j][0] = acci[i][j][1] = 0.0;
   }
 
-  // ---- index prefetch: the CSR ranges of every group, the output's storage word and the first
-  // kIdx entries' operand indices are fetched in two parallel rounds (ranges, then indices) into
-  // shared memory, instead of one dependent global load per group and per entry in the copy path
-  // (a 2-group, 2-entry output paid ptr -> li -> data -> ptr -> li -> data -> omap -> C: six
-  // serial round trips; now ranges -> indices -> data, with the accumulate lines prefetched)
-  // (not in the 64 x 64 complex 3-product instantiation: its 192 accumulator registers leave no
-  // room, and with >= 16 chunks per entry its index loads are hidden by the pipeline anyway)
-  constexpr bool PF = !(CPLX && G3 && TM == 64 && TN == 64);
-  constexpr int kIdx = PF ? 64 : 1;
-  __shared__ int s_ge[PF ? 2 * kMaxGroups + 1 : 1];  // e0, e1 per group; [2 kMaxGroups] output word
-  __shared__ int s_li[kIdx], s_ri[kIdx];
-  if constexpr (PF) {
-    if (tid < 2 * p.ngroups) {
-      const int* ptr = p.g[tid >> 1].ptr;
-      s_ge[tid] = ptr ? ptr[t + (tid & 1)] : (tid & 1);
-    } else if (tid == 2 * kMaxGroups) {
-      s_ge[2 * kMaxGroups] = seg_out_word(p, t);
-    }
-    __syncthreads();
-  }
-  auto fill_idx = [&](int qb) { seg_fill_idx(p, t, qb, tid, NT, kIdx, s_ge, s_li, s_ri); };
-  if constexpr (PF) {
-    fill_idx(0);
-    if (p.accumulate) {  // the accumulate target's lines into L2 while the operands are fetched
-      const char* Ob = reinterpret_cast<const char*>(seg_out_ptr(p, s_ge[2 * kMaxGroups], W));
-      const int rows = min(TM, p.M - m0), cols = min(TN, p.N - n0);
-      const int lpc = (rows * 8 * W + 127) / 128;  // 128-byte lines per column
-      for (int x = tid; x < cols * lpc; x += NT) {
-        const char* a = Ob + ((long long)(m0 + (long long)(n0 + x / lpc) * p.Old)) * 8 * W + (x % lpc) * 128;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-      }
-    }
-    __syncthreads();
-  }
-
   // ---- copy (producer) state: one chunk ahead of the consumer by ST-1 -------
-  int ig = 0, ie = 0, ie1 = 0, ikc = 0, inkc = 1, iq = 0, iqb = 0;
+  int ig = 0, ie = 0, ie1 = 0, ikc = 0, inkc = 1;
   bool iv = false;
   const double* lsrc[LPT];
   const double* rsrc[RPT];
@@ -262,13 +205,13 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const __grid_
   bool lok[LPT], rok[RPT];
   long long lstep = 0, rstep = 0;
   auto range = [&](int g, int& e0, int& e1) {
-    if constexpr (PF) {
-      e0 = s_ge[2 * g];
-      e1 = s_ge[2 * g + 1];
+    const int* ptr = p.g[g].ptr;
+    if (ptr) {
+      e0 = ptr[t];
+      e1 = ptr[t + 1];
     } else {
-      const int* ptr = p.g[g].ptr;
-      e0 = ptr ? ptr[t] : 0;
-      e1 = ptr ? ptr[t + 1] : 1;
+      e0 = 0;
+      e1 = 1;
     }
   };
   auto setup_group = [&](int g) {  // per-thread copy geometry of group g
@@ -309,20 +252,10 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const __grid_
     rstep = (rt ? (long long)KC * G.Rld : (long long)KC) * W;
     inkc = G.K / KC;
   };
-  auto setup_entry = [&]() {  // source pointers of entry ie of group ig (the iq-th of the output)
+  auto setup_entry = [&]() {  // source pointers of entry ie of group ig
     const SegGroup& G = p.g[ig];
     int l, r;
-    if constexpr (PF) {
-      if (iq - iqb == kIdx) {  // index cache exhausted (uniform over the CTA): next kIdx entries
-        __syncthreads();
-        iqb = iq;
-        fill_idx(iqb);
-        __syncthreads();
-      }
-      l = s_li[iq - iqb];
-      r = s_ri[iq - iqb];
-      ++iq;
-    } else if (G.ptr) {
+    if (G.ptr) {
       l = G.li[ie];
       r = G.ri[ie];
     } else {
@@ -475,7 +408,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const __grid_
   }
   cp_async_wait<0>();
 
-  double* Op = seg_out_ptr(p, PF ? s_ge[2 * kMaxGroups] : seg_out_word(p, t), W);
+  double* Op = seg_out_ptr(p, t, W);
 #pragma unroll
   for (int i = 0; i < C::FM; ++i)
 #pragma unroll
@@ -510,6 +443,136 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const __grid_
             Op[off] = v;
             if (mirror) Op[offt] = v;
           }
+        }
+      }
+}
+
+// ---------------------------------------------------------------------------
+// seg_small: the same segmented product for outputs of at most 32 x 32 with few k-chunks (the
+// small-rank target sums, projections and split products of configs[2] / configs[4]).  ncu of
+// seg_gemm3 on those launches (profiles/r02/ncu/l12_targets_cfg3_*): ~940 warp instructions per
+// warp around 16 DMMAs - the CTA-wide cp.async pipeline, its barriers and the copy geometry are
+// all overhead there, and the launch is instruction-issue bound at ~50 % of the HBM rate.  Here
+// ONE WARP owns one output (4 outputs per CTA, no shared memory, no barriers): every lane loads
+// its m8n8k4 fragment elements straight from global memory (element (m, k) of op(L) at
+// m * sm + k * sk, so all four operand layouts share one body; a quarter-warp reads 32-64
+// contiguous bytes: whole sectors), 8 k per step so 2 (FM + FN) loads are in flight before the
+// DMMAs.  M = 8 FM and N = 8 FN exactly (all padded dimensions are multiples of 8).  Complex
+// products in the 4-product form (two accumulator sets: these launches are not DMMA bound).
+template <int FM, int FN, bool CPLX>
+__global__ void __launch_bounds__(128) seg_small_kernel(const SegParams p) {
+  constexpr int W = CPLX ? 2 : 1;
+  const int lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (t >= p.n_out) return;
+
+  double acc[FM][FN][2];
+  double acci[CPLX ? FM : 1][CPLX ? FN : 1][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) {
+      acc[i][j][0] = acc[i][j][1] = 0.0;
+      if constexpr (CPLX) acci[i][j][0] = acci[i][j][1] = 0.0;
+    }
+
+#pragma unroll 1
+  for (int g = 0; g < p.ngroups; ++g) {
+    const SegGroup& G = p.g[g];
+    int e0 = 0, e1 = 1;
+    if (G.ptr) {
+      e0 = G.ptr[t];
+      e1 = G.ptr[t + 1];
+    }
+    if (e0 >= e1) continue;
+    const bool lt = G.opL == OP_T || G.opL == OP_H;
+    const bool rt = G.opR == OP_T || G.opR == OP_H;
+    const double cl = (G.opL == OP_H || G.opL == OP_C) ? -1.0 : 1.0;
+    const double cr = (G.opR == OP_H || G.opR == OP_C) ? -1.0 : 1.0;
+    // element strides (in scalars): op(L)(m, k) at m * lsm + k * lsk, op(R)(k, n) at k * rsk + n * rsn
+    // (ints: a matrix of the product has far fewer than 2^31 scalars)
+    const int lsm = (lt ? G.Lld : 1) * W, lsk = (lt ? 1 : G.Lld) * W;
+    const int rsk = (rt ? G.Rld : 1) * W, rsn = (rt ? 1 : G.Rld) * W;
+    const int aoff = gq * lsm + tq * lsk, boff = tq * rsk + gq * rsn;
+    int l = G.ptr ? G.li[e0] : (G.li ? G.li[t] : t);
+    int r = G.ptr ? G.ri[e0] : (G.ri ? G.ri[t] : t);
+#pragma unroll 1
+    for (int e = e0; e < e1; ++e) {
+      const double* Lp = (G.Lch ? G.Lch[l >> G.Lsh] + (G.Ls * (l & ((1 << G.Lsh) - 1)) + G.Loff) * W
+                                : G.L + (G.Ls * l + G.Loff) * W) + aoff;
+      const double* Rp = (G.Rch ? G.Rch[r >> G.Rsh] + (G.Rs * (r & ((1 << G.Rsh) - 1)) + G.Roff) * W
+                                : G.R + (G.Rs * r + G.Roff) * W) + boff;
+      if (e + 1 < e1) {  // next entry's indices while this entry's operands are fetched
+        l = G.li[e + 1];
+        r = G.ri[e + 1];
+      }
+#pragma unroll 1
+      for (int kk = 0; kk < G.K; kk += 8) {
+        if constexpr (CPLX) {
+          double2 a[2][FM], b[2][FN];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+              a[h][i] = *reinterpret_cast<const double2*>(Lp + 8 * i * lsm + (kk + 4 * h) * lsk);
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+              b[h][j] = *reinterpret_cast<const double2*>(Rp + (kk + 4 * h) * rsk + 8 * j * rsn);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+              for (int j = 0; j < FN; ++j) {
+                const double ar = a[h][i].x, ai = cl * a[h][i].y, br = b[h][j].x, bi = cr * b[h][j].y;
+                dmma(acc[i][j][0], acc[i][j][1], ar, br);
+                dmma(acc[i][j][0], acc[i][j][1], -ai, bi);
+                dmma(acci[i][j][0], acci[i][j][1], ar, bi);
+                dmma(acci[i][j][0], acci[i][j][1], ai, br);
+              }
+        } else {
+          double a[2][FM], b[2][FN];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int i = 0; i < FM; ++i) a[h][i] = Lp[8 * i * lsm + (kk + 4 * h) * lsk];
+#pragma unroll
+            for (int j = 0; j < FN; ++j) b[h][j] = Rp[(kk + 4 * h) * rsk + 8 * j * rsn];
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+              for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[h][i], b[h][j]);
+        }
+      }
+    }
+  }
+
+  double* Op = seg_out_ptr(p, t, W);
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const long long off = (8 * i + gq) + (long long)(8 * j + 2 * tq + q) * p.Old;
+        if constexpr (CPLX) {
+          double2 v = make_double2(acc[i][j][q], acci[i][j][q]);
+          double2* o = reinterpret_cast<double2*>(Op + 2 * off);
+          if (p.accumulate) {
+            const double2 c = *o;
+            v.x += c.x;
+            v.y += c.y;
+          }
+          *o = v;
+        } else {
+          double v = acc[i][j][q];
+          if (p.accumulate) v += Op[off];
+          Op[off] = v;
         }
       }
 }
