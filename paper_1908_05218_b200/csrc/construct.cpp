@@ -30,11 +30,14 @@ namespace h2b {
 
 namespace {
 
+// f(k) for k in [0, n) on `threads` threads, dynamically scheduled in chunks (fixed_chunk > 0:
+// that many per grab - 1 for loops whose iterations differ widely in cost)
 template <class F>
-void pfor(int64_t n, int threads, F&& f) {
+void pfor(int64_t n, int threads, F&& f, int64_t fixed_chunk = 0) {
   threads = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(threads, n)));
   std::atomic<int64_t> next{0};
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(64, n / (8 * int64_t(threads))));
+  const int64_t chunk =
+      fixed_chunk > 0 ? fixed_chunk : std::max<int64_t>(1, std::min<int64_t>(64, n / (8 * int64_t(threads))));
   auto work = [&] {
     for (;;) {
       const int64_t i = next.fetch_add(chunk);
@@ -380,10 +383,13 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
   // kernel value at distance r
   auto G = [&](double r) -> S {
     const double f = 1.0 / (4.0 * M_PI * r);
-    if constexpr (cplx)
-      return S(f * std::cos(kappa * r), -f * std::sin(kappa * r));
-    else
+    if constexpr (cplx) {
+      double sn, cs;
+      ::sincos(kappa * r, &sn, &cs);
+      return S(f * cs, -f * sn);
+    } else {
       return S(f);
+    }
   };
   (void)kernel;
   // 2. couplings in the orthonormal coordinates: S_ts = R_t K(xi_t, xi_s) R_s^T (recomputed
@@ -511,6 +517,37 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
             dev.reset();
             zown.clear();
           }
+        }
+      }
+      if (zown.empty() && static_cast<int64_t>(ids.size()) < 8 * int64_t(threads)) {
+        // Host path on a level with few clusters (the upper levels, whose blocks are the expensive
+        // ones): parallel over the level's blocks instead of its clusters, in bounded batches;
+        // each cluster's sum still runs in its block order.
+        zown.resize(ids.size());
+        std::vector<std::pair<int, int64_t>> items;
+        for (size_t qi = 0; qi < ids.size(); ++qi) {
+          zown[qi] = M<S>(Qb[ids[qi]].c, Qb[ids[qi]].c);
+          for (int64_t q : by_row[ids[qi]]) items.emplace_back(static_cast<int>(qi), q);
+        }
+        const size_t budget = size_t(2) << 30;  // bytes of per-block Grams alive at once
+        for (size_t pos = 0; pos < items.size();) {
+          size_t end = pos, bytes = 0;
+          while (end < items.size() && (end == pos || bytes < budget)) {
+            const size_t rk = Qb[ids[items[end].first]].c;
+            bytes += rk * rk * sizeof(S);
+            ++end;
+          }
+          std::vector<M<S>> gs(end - pos);
+          pfor(static_cast<int64_t>(end - pos), threads, [&](int64_t i) {
+            const M<S> Sq = coupling_raw(items[pos + i].second);
+            gemm(kN, kC, Sq, Sq, gs[i]);
+          }, 1);
+          for (size_t i = pos; i < end; ++i) {
+            M<S>& z = zown[items[i].first];
+            const M<S>& g = gs[i - pos];
+            for (size_t x = 0; x < z.d.size(); ++x) z.d[x] += g.d[x];
+          }
+          pos = end;
         }
       }
       pfor(static_cast<int64_t>(ids.size()), threads, [&](int64_t qi) {
@@ -645,8 +682,14 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
     }
   }
   if (!dev_done) {
-    pfor(static_cast<int64_t>(adm.size()), threads, [&](int64_t a) {
-      const int64_t q = adm[a];
+    // the few upper-level blocks (k up to 729) cost ~10^4 leaf-level blocks each: heaviest first,
+    // one block per grab
+    std::vector<int64_t> order(adm);
+    std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+      return int64_t(cb[b.row[x]].k()) * cb[b.col[x]].k() > int64_t(cb[b.row[y]].k()) * cb[b.col[y]].k();
+    });
+    pfor(static_cast<int64_t>(order.size()), threads, [&](int64_t a) {
+      const int64_t q = order[a];
       M<S> Sq = coupling_raw(q);
       if (rc) {
         M<S> PS;
@@ -654,7 +697,7 @@ std::unique_ptr<HostH2> chebyshev_impl(const h2c_tree& t, const h2c_blocks& b, c
         gemm(kN, kT, PS, P[b.col[q]], Sq);
       }
       std::copy(Sq.d.begin(), Sq.d.end(), V + out->block_off[q]);
-    });
+    }, 1);
   }
   tick("couplings");
   pfor(b.n_blocks, threads, [&](int64_t q) {

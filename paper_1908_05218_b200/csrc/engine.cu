@@ -1386,7 +1386,7 @@ struct EngineRun : Relief {
   // Batched Hermitian eigensolver + truncation rule (heev.cuh).  Placement per launch, from
   // tools/heev_bench.cu on the B200 (profiles/r02/heev_*.txt):
   //  * n <= 96 (leaf Grams): one CTA per Gram, Gram in shared memory (2-3 CTAs per SM);
-  //  * 24 Grams or more (the batched middle levels): the Gram in a global (L2-resident) slab and
+  //  * 12 Grams or more (the batched middle levels): the Gram in a global (L2-resident) slab and
   //    ~20-50 KB of shared memory, one CTA per Gram when there are enough Grams to fill the SMs,
   //    else a cluster of 2-4 CTAs per Gram (column slabs, one wave of CTAs);
   //  * few large Grams: a cluster of CS CTAs per Gram (CS the smallest power of two whose
@@ -1407,12 +1407,12 @@ struct EngineRun : Relief {
       smem = false;
     }
     // the row and column solves of a level run concurrently: size the decision on both.
-    // From 24 Grams on, global slabs with the largest power-of-two cluster that still gives one
+    // From 12 Grams on, global slabs with the largest power-of-two cluster that still gives one
     // wave of CTAs (eff * CS <= 160): e.g. 32 Grams of n = 624 take 26 ms with CS = 4 against
     // 63 ms on 16-CTA shared-memory clusters and 79 ms with one CTA each; 64 Grams of n = 576
     // 41 ms with CS = 2 against 72 ms with CS = 1 (profiles/r02/heev_sweep.txt).
     const int eff = paired_solves ? 2 * count : count;
-    if (n > 96 && eff >= 24) {
+    if (n > 96 && eff >= 12) {
       CS = 1;
       while (CS < 16 && eff * CS * 2 <= 160) CS *= 2;
       smem = false;

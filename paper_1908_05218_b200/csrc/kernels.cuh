@@ -462,30 +462,54 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
 template <int FM, int FN, bool CPLX>
 __global__ void __launch_bounds__(128) seg_small_kernel(const SegParams p) {
   constexpr int W = CPLX ? 2 : 1;
+  constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (t >= p.n_out) return;
 
+  // Lane g fetches group g's CSR range and the operand indices of its first entry, all groups at
+  // once (two parallel rounds instead of a dependent range -> index pair per group inside the
+  // loop); the values reach the other lanes by shuffle.
+  int me0 = 0, me1 = 0, ml = 0, mr = 0;
+  if (lane < p.ngroups) {
+    const SegGroup& G = p.g[lane];
+    me0 = G.ptr ? G.ptr[t] : 0;
+    me1 = G.ptr ? G.ptr[t + 1] : 1;
+    if (me0 < me1) {
+      ml = G.ptr ? G.li[me0] : (G.li ? G.li[t] : t);
+      mr = G.ptr ? G.ri[me0] : (G.ri ? G.ri[t] : t);
+    }
+  }
+  double* Op = seg_out_ptr(p, t, W);
+
+  // the accumulators start from C when the launch accumulates: the read overlaps the operand
+  // fetches and the epilogue only stores
   double acc[FM][FN][2];
   double acci[CPLX ? FM : 1][CPLX ? FN : 1][2];
 #pragma unroll
   for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < FN; ++j) {
-      acc[i][j][0] = acc[i][j][1] = 0.0;
-      if constexpr (CPLX) acci[i][j][0] = acci[i][j][1] = 0.0;
-    }
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const long long off = (8 * i + gq) + (long long)(8 * j + 2 * tq + q) * p.Old;
+        if constexpr (CPLX) {
+          double2 c = make_double2(0.0, 0.0);
+          if (p.accumulate) c = *reinterpret_cast<const double2*>(Op + 2 * off);
+          acc[i][j][q] = c.x;
+          acci[i][j][q] = c.y;
+        } else {
+          acc[i][j][q] = p.accumulate ? Op[off] : 0.0;
+        }
+      }
 
 #pragma unroll 1
   for (int g = 0; g < p.ngroups; ++g) {
-    const SegGroup& G = p.g[g];
-    int e0 = 0, e1 = 1;
-    if (G.ptr) {
-      e0 = G.ptr[t];
-      e1 = G.ptr[t + 1];
-    }
+    const int e0 = __shfl_sync(kFull, me0, g), e1 = __shfl_sync(kFull, me1, g);
+    int l = __shfl_sync(kFull, ml, g), r = __shfl_sync(kFull, mr, g);
     if (e0 >= e1) continue;
+    const SegGroup& G = p.g[g];
     const bool lt = G.opL == OP_T || G.opL == OP_H;
     const bool rt = G.opR == OP_T || G.opR == OP_H;
     const double cl = (G.opL == OP_H || G.opL == OP_C) ? -1.0 : 1.0;
@@ -495,8 +519,6 @@ __global__ void __launch_bounds__(128) seg_small_kernel(const SegParams p) {
     const int lsm = (lt ? G.Lld : 1) * W, lsk = (lt ? 1 : G.Lld) * W;
     const int rsk = (rt ? G.Rld : 1) * W, rsn = (rt ? 1 : G.Rld) * W;
     const int aoff = gq * lsm + tq * lsk, boff = tq * rsk + gq * rsn;
-    int l = G.ptr ? G.li[e0] : (G.li ? G.li[t] : t);
-    int r = G.ptr ? G.ri[e0] : (G.ri ? G.ri[t] : t);
 #pragma unroll 1
     for (int e = e0; e < e1; ++e) {
       const double* Lp = (G.Lch ? G.Lch[l >> G.Lsh] + (G.Ls * (l & ((1 << G.Lsh) - 1)) + G.Loff) * W
@@ -515,10 +537,10 @@ __global__ void __launch_bounds__(128) seg_small_kernel(const SegParams p) {
           for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int i = 0; i < FM; ++i)
-              a[h][i] = *reinterpret_cast<const double2*>(Lp + 8 * i * lsm + (kk + 4 * h) * lsk);
+              a[h][i] = __ldg(reinterpret_cast<const double2*>(Lp + 8 * i * lsm + (kk + 4 * h) * lsk));
 #pragma unroll
             for (int j = 0; j < FN; ++j)
-              b[h][j] = *reinterpret_cast<const double2*>(Rp + (kk + 4 * h) * rsk + 8 * j * rsn);
+              b[h][j] = __ldg(reinterpret_cast<const double2*>(Rp + (kk + 4 * h) * rsk + 8 * j * rsn));
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h)
@@ -537,9 +559,9 @@ __global__ void __launch_bounds__(128) seg_small_kernel(const SegParams p) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
 #pragma unroll
-            for (int i = 0; i < FM; ++i) a[h][i] = Lp[8 * i * lsm + (kk + 4 * h) * lsk];
+            for (int i = 0; i < FM; ++i) a[h][i] = __ldg(Lp + 8 * i * lsm + (kk + 4 * h) * lsk);
 #pragma unroll
-            for (int j = 0; j < FN; ++j) b[h][j] = Rp[(kk + 4 * h) * rsk + 8 * j * rsn];
+            for (int j = 0; j < FN; ++j) b[h][j] = __ldg(Rp + (kk + 4 * h) * rsk + 8 * j * rsn);
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h)
@@ -552,7 +574,6 @@ __global__ void __launch_bounds__(128) seg_small_kernel(const SegParams p) {
     }
   }
 
-  double* Op = seg_out_ptr(p, t, W);
 #pragma unroll
   for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -560,20 +581,8 @@ __global__ void __launch_bounds__(128) seg_small_kernel(const SegParams p) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const long long off = (8 * i + gq) + (long long)(8 * j + 2 * tq + q) * p.Old;
-        if constexpr (CPLX) {
-          double2 v = make_double2(acc[i][j][q], acci[i][j][q]);
-          double2* o = reinterpret_cast<double2*>(Op + 2 * off);
-          if (p.accumulate) {
-            const double2 c = *o;
-            v.x += c.x;
-            v.y += c.y;
-          }
-          *o = v;
-        } else {
-          double v = acc[i][j][q];
-          if (p.accumulate) v += Op[off];
-          Op[off] = v;
-        }
+        if constexpr (CPLX) *reinterpret_cast<double2*>(Op + 2 * off) = make_double2(acc[i][j][q], acci[i][j][q]);
+        else Op[off] = acc[i][j][q];
       }
 }
 
