@@ -1098,7 +1098,7 @@ struct EngineRun : Relief {
     sp.M = M;
     sp.N = N;
     sp.n_out = n_out;
-    sp.accumulate = acc ? 1 : 0;
+    sp.accumulate = acc ? (c_prefetch ? 3 : 1) : 0;
     int ng = 0;
     for (const Grp& g : gs) {
       const int64_t entries = g.csr ? g.csr->entries : n_out;
@@ -1200,6 +1200,8 @@ struct EngineRun : Relief {
     }
     post();
   }
+  // accumulating launches prefetch their output tile to L2 (H2B_NO_CPREFETCH=1: A/B)
+  const bool c_prefetch = std::getenv("H2B_NO_CPREFETCH") == nullptr;
   const bool no_strips = std::getenv("H2B_NO_STRIPS") != nullptr;  // A/B: single launch per product
   const bool strips_small = std::getenv("H2B_NO_STRIPS_SMALL") == nullptr;
   const bool strips_24 = std::getenv("H2B_STRIPS_24") != nullptr;
@@ -1388,7 +1390,7 @@ struct EngineRun : Relief {
   //  * n <= 96 (leaf Grams): one CTA per Gram, Gram in shared memory (2-3 CTAs per SM);
   //  * 12 Grams or more (the batched middle levels): the Gram in a global (L2-resident) slab and
   //    ~20-50 KB of shared memory, one CTA per Gram when there are enough Grams to fill the SMs,
-  //    else a cluster of 2-4 CTAs per Gram (column slabs, one wave of CTAs);
+  //    else a cluster of 2 or 4 CTAs per Gram (column slabs, one wave of CTAs);
   //  * few large Grams: a cluster of CS CTAs per Gram (CS the smallest power of two whose
   //    column slabs fit the CTAs' shared memory, <= 16; global slabs beyond).
   // Workspaces come from the main-stream arena before the fork.
@@ -1407,14 +1409,16 @@ struct EngineRun : Relief {
       smem = false;
     }
     // the row and column solves of a level run concurrently: size the decision on both.
-    // From 12 Grams on, global slabs with the largest power-of-two cluster that still gives one
-    // wave of CTAs (eff * CS <= 160): e.g. 32 Grams of n = 624 take 26 ms with CS = 4 against
-    // 63 ms on 16-CTA shared-memory clusters and 79 ms with one CTA each; 64 Grams of n = 576
-    // 41 ms with CS = 2 against 72 ms with CS = 1 (profiles/r02/heev_sweep.txt).
+    // From 12 Grams on, global slabs with the largest power-of-two cluster of at most 4 CTAs that
+    // still gives one wave of CTAs (eff * CS <= 160): e.g. 32 Grams of n = 624 take 26 ms with
+    // CS = 4 against 63 ms on 16-CTA shared-memory clusters and 79 ms with one CTA each; 64 Grams
+    // of n = 576 41 ms with CS = 2 against 72 ms with CS = 1; 16 Grams of n = 464 13 ms with CS = 4
+    // against 18 ms with CS = 8 and 22 ms on 16-CTA shared-memory clusters (8-CTA global-slab
+    // clusters never won; profiles/r02/heev_sweep.txt, heev_sweep2.txt).
     const int eff = paired_solves ? 2 * count : count;
     if (n > 96 && eff >= 12) {
       CS = 1;
-      while (CS < 16 && eff * CS * 2 <= 160) CS *= 2;
+      while (CS < 4 && eff * CS * 2 <= 160) CS *= 2;
       smem = false;
     }
     const HeevLayout L(n, CS, cplx, smem);

@@ -44,7 +44,7 @@ struct SegParams {
   const int* omap;     // storage index of output t (nullptr = t)
   int M, N;            // output dims (padded)
   int n_out;
-  int accumulate;      // out (+)= sum
+  int accumulate;      // out (+)= sum (bit 0); bit 1: prefetch the output tile to L2 first
   int sym;             // Hermitian output (Gram): only tiles m0 >= n0 are computed, mirrored
   int ngroups;
   // optional quadrant scatter (children targets written straight into their
@@ -194,6 +194,18 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) seg_gemm3_kernel(const SegPara
     for (int i = 0; i < C::FM; ++i)
 #pragma unroll
       for (int j = 0; j < C::FN; ++j) acci[i][j][0] = acci[i][j][1] = 0.0;
+  }
+
+  // accumulating launches: the output tile's lines go to L2 now, so the epilogue's read of C
+  // overlaps the operand fetches instead of starting a second DRAM round trip after the last DMMA
+  if (p.accumulate & 2) {
+    const char* Ob = reinterpret_cast<const char*>(seg_out_ptr(p, t, W));
+    const int rows = min(TM, p.M - m0), cols = min(TN, p.N - n0);
+    const int lpc = (rows * 8 * W + 127) / 128;  // 128-byte lines per column
+    for (int x = tid; x < cols * lpc; x += NT) {
+      const char* a = Ob + (m0 + (long long)(n0 + x / lpc) * p.Old) * (8 * W) + (x % lpc) * 128;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
   }
 
   // ---- copy (producer) state: one chunk ahead of the consumer by ST-1 -------

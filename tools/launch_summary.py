@@ -22,7 +22,7 @@ def phase(r):
     m = re.search(r'<default domain>:([^:"]+):([^:"]+)', r[ni])
     if m:
         return m.group(1) + ":" + m.group(2)
-    return "(library) " + re.sub(r"\(.*", "", r[ki])[:60]
+    return "(outside the product: input constructor) " + re.sub(r"\(.*", "", r[ki])[:60]
 
 
 tot, cnt = collections.Counter(), collections.Counter()
