@@ -267,9 +267,21 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
           const T* __restrict__ cj = slab + (size_t)jl * ld;
           if (SMEM) {
             for (int i = k + 1 + tl; i < n; i += ts) acc = N::cfma(cj[i], vloc[i], acc);
-          } else {  // L2-resident slab: 4 loads in flight per lane
+          } else {  // L2-resident slab: 8 loads in flight per lane
             T a1 = N::zero(), a2 = N::zero(), a3 = N::zero();
             int i = k + 1 + tl;
+            for (; i + 7 * ts < n; i += 8 * ts) {
+              const T b0 = cj[i], b1 = cj[i + ts], b2 = cj[i + 2 * ts], b3 = cj[i + 3 * ts];
+              const T b4 = cj[i + 4 * ts], b5 = cj[i + 5 * ts], b6 = cj[i + 6 * ts], b7 = cj[i + 7 * ts];
+              acc = N::cfma(b0, vloc[i], acc);
+              a1 = N::cfma(b1, vloc[i + ts], a1);
+              a2 = N::cfma(b2, vloc[i + 2 * ts], a2);
+              a3 = N::cfma(b3, vloc[i + 3 * ts], a3);
+              acc = N::cfma(b4, vloc[i + 4 * ts], acc);
+              a1 = N::cfma(b5, vloc[i + 5 * ts], a1);
+              a2 = N::cfma(b6, vloc[i + 6 * ts], a2);
+              a3 = N::cfma(b7, vloc[i + 7 * ts], a3);
+            }
             for (; i + 3 * ts < n; i += 4 * ts) {
               const T b0 = cj[i], b1 = cj[i + ts], b2 = cj[i + 2 * ts], b3 = cj[i + 3 * ts];
               acc = N::cfma(b0, vloc[i], acc);
@@ -335,9 +347,9 @@ __global__ void __launch_bounds__(512) heev_kernel(const HeevParams p) {
               *a = N::sub(N::sub(*a, N::mul(vi, N::conj(w[j]))), N::mul(wi, N::conj(vloc[j])));
             }
           }
-      } else {  // large real Grams in an L2-resident slab: 4 loads in flight before the stores
+      } else {  // large real Grams in an L2-resident slab: 8 loads in flight before the stores
         const int tot = ncol * m;  // <= n^2: fits an int
-        constexpr int U = 4;
+        constexpr int U = 8;
         for (int x0 = tid; x0 < tot; x0 += U * nt) {
           int ii[U], jj[U];
           T av[U];
