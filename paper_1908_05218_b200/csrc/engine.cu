@@ -1217,11 +1217,15 @@ struct EngineRun : Relief {
   const bool sym_t64 = std::getenv("H2B_SYM_T64") != nullptr;
   static int sym_tile(int M) {
     if (M <= 32) return M <= 16 ? 16 : 32;
+    static const double eff32 = [] {  // relative efficiency of the 32-tile kernel (H2B_SYM_EFF32: A/B)
+      const char* e = std::getenv("H2B_SYM_EFF32");
+      return e ? std::atof(e) : 0.75;
+    }();
     auto cost = [&](int T, double eff) {
       const double t = (M + T - 1) / T;
       return t * (t + 1) / 2 * T * T / eff;
     };
-    return cost(32, 0.75) < cost(64, 1.0) ? 32 : 64;
+    return cost(32, eff32) < cost(64, 1.0) ? 32 : 64;
   }
   // seg_small (kernels.cuh): one warp per output, for outputs of at most 12 m8n8 fragments (e.g.
   // 24 x 32; a 32 x 32 output needs 126 registers per lane and measured slower than seg_gemm3).
