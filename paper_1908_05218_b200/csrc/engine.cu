@@ -1215,12 +1215,17 @@ struct EngineRun : Relief {
   // takes 6 tiles of 32 (6,144 padded elements) instead of 3 of 64 (12,288, 26 % useful).
   // H2B_SYM_T64=1 restores the plain rule.
   const bool sym_t64 = std::getenv("H2B_SYM_T64") != nullptr;
-  static int sym_tile(int M) {
+  // relative efficiency assumed for the 32-tile kernel: 0.75 for real products (round 1, neutral
+  // either way); 1.0 for complex ones - the 3-product 64 x 64 instantiation runs 2 CTAs per SM at
+  // 249 registers, the 32 x 32 one 5, and lower triangles of 32-tiles carry up to 25 % less padding:
+  // configs[4] 1.566 -> 1.538 s (profiles/r02/ab_small_maxch_sym_tile.json).  H2B_SYM_EFF32: A/B.
+  static int sym_tile(int M, bool cplx) {
     if (M <= 32) return M <= 16 ? 16 : 32;
-    static const double eff32 = [] {  // relative efficiency of the 32-tile kernel (H2B_SYM_EFF32: A/B)
+    static const double eff_env = [] {
       const char* e = std::getenv("H2B_SYM_EFF32");
-      return e ? std::atof(e) : 0.75;
+      return e ? std::atof(e) : 0.0;
     }();
+    const double eff32 = eff_env > 0.0 ? eff_env : (cplx ? 1.0 : 0.75);
     auto cost = [&](int T, double eff) {
       const double t = (M + T - 1) / T;
       return t * (t + 1) / 2 * T * T / eff;
@@ -1275,7 +1280,7 @@ struct EngineRun : Relief {
     }
     int TM = M <= 8 ? 8 : M <= 16 ? 16 : (M <= 32 ? 32 : 64);
     int TN = N <= 8 ? 8 : N <= 16 ? 16 : (N <= 32 ? 32 : 64);
-    if (sp.sym && !sym_t64 && M > 32) TM = TN = sym_tile(M);
+    if (sp.sym && !sym_t64 && M > 32) TM = TN = sym_tile(M, cplx);
     const int tm_ = (M + TM - 1) / TM;
     const int tiles = sp.sym ? tm_ * (tm_ + 1) / 2 : tm_ * ((N + TN - 1) / TN);
     if (TM == 8 || TN == 8) {
@@ -1467,7 +1472,12 @@ struct EngineRun : Relief {
       CK(cudaLaunchKernelEx(&cfg, kern, hp));
     };
     const bool main = st == s;
-    if (main) pre("heev", 0);
+    // profile estimate: ~8/3 n^3 MACs per Gram (tridiagonalisation + back-transformation) over
+    // ~n^3 scalars of trailing-matrix traffic (two reads and one write per Householder step):
+    // 0.67 flop/B, a memory-bound kernel by the roofline model (its passes are L2 / latency bound)
+    if (main)
+      pre("heev", int64_t(count) * int64_t(8.0 / 3.0 * double(n) * n * n),
+          int64_t(count) * int64_t(double(n) * n * n) * 8 * W);
     if (cplx) {
       if (smem) go(heev_kernel<true, true>);
       else go(heev_kernel<true, false>);
