@@ -112,6 +112,25 @@ class Arena {
     used_[at] = bytes;
     return static_cast<char*>(base_) + at;
   }
+  // the exact range [p, p + bytes) if it is free (an evicted buffer returning to its own place,
+  // so repeated products see the same layout), else nullptr
+  void* alloc_at(void* p, size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    std::lock_guard<std::mutex> g(mu_);
+    reclaim_locked(false);
+    if (!owns(p)) return nullptr;
+    const size_t off = static_cast<char*>(p) - static_cast<char*>(base_);
+    auto it = free_.upper_bound(off);
+    if (it == free_.begin()) return nullptr;
+    --it;
+    const size_t b0 = it->first, sz = it->second;
+    if (b0 > off || b0 + sz < off + bytes) return nullptr;
+    free_.erase(it);
+    if (off > b0) free_[b0] = off - b0;
+    if (b0 + sz > off + bytes) free_[off + bytes] = b0 + sz - (off + bytes);
+    used_[off] = bytes;
+    return p;
+  }
   // (total free bytes, largest free block)
   std::pair<size_t, size_t> stats() {
     std::lock_guard<std::mutex> g(mu_);
@@ -260,6 +279,15 @@ struct DBuf {
       o.arena = nullptr;
     }
     return *this;
+  }
+  // takes over an arena block obtained by the caller (Arena::alloc_at)
+  void adopt(double* ptr, size_t doubles, cudaStream_t st, Arena* a) {
+    release();
+    p = ptr;
+    n = doubles;
+    s = st;
+    arena = a;
+    aux = false;
   }
   void alloc(size_t doubles, cudaStream_t st, bool zero = false) {
     release();
@@ -915,6 +943,7 @@ struct EngineRun : Relief {
     double* host;
     size_t bytes, n;
     bool operand;
+    double* home;  // where the buffer lived in the arena (nullptr: not an arena block)
   };
   std::vector<Evicted> evicted;
   bool leaf_done = false;
@@ -928,7 +957,7 @@ struct EngineRun : Relief {
       if (s_aux) CK(cudaStreamSynchronize(s_aux));
     }
     CK(cudaStreamSynchronize(s));
-    Evicted e{&b, nullptr, b.n * sizeof(double), b.n, operand};
+    Evicted e{&b, nullptr, b.n * sizeof(double), b.n, operand, b.arena ? b.p : nullptr};
     size_t got = 0;
     e.host = ctx.pinned->take(e.bytes, &got);
     CK(cudaMemcpyAsync(e.host, b.p, e.bytes, cudaMemcpyDeviceToHost, s));
@@ -958,7 +987,13 @@ struct EngineRun : Relief {
         ++i;
         continue;
       }
-      {
+      // back to its own place when that is free again, so the next product on these operands
+      // finds the arena laid out as the first one did (a drifting operand fragmented it: the
+      // fourth consecutive configs[3] product at 64^3 failed to place a 21 GB target store)
+      void* home = (e.home && t_arena) ? t_arena->alloc_at(e.home, e.n * sizeof(double)) : nullptr;
+      if (home) {
+        e.buf->adopt(static_cast<double*>(home), e.n, s, t_arena);
+      } else {
         HighScope long_lived;
         e.buf->alloc(e.n, s);
       }
