@@ -16,14 +16,17 @@ eps = 1e-4.  `--config cfg1..cfg4` run the other BASELINE configurations.
           buffers (H2D of A, D2H of C inside the timed region); the first
           (cold) call of a fresh context is reported next to it.
 
-`--impl reference` times the CPU oracle (the C++ restatement of the
-reference's mmp.cpp; the reference itself needs Eigen, absent here) on the SAME
-configuration and N, with every host core (oracle/product_engine.cpp, bit-
-identical to the single-thread restatement): each step is a consecutive
-time slice of one running product (products run back to back), value = the
-reference MACs counted in the timed slices / their wall time.  Its inputs come
-from the CPU-only generator oracle/_build/libh2inputs.so; it never maps the
-B200 library or touches the GPU.
+`--impl reference` times the reference's OWN mmp() (oracle/_ref/libh2ref.so: the
+reference's unmodified MMP-path sources compiled against the Eigen-subset shim,
+oracle/eigen_shim; single-threaded as the reference is) on the SAME
+configuration and N: each step is a consecutive time window of products
+running back to back, value = the reference MACs counted in the timed windows /
+their wall time.  If that library is missing, the all-cores oracle restatement
+(oracle/product_engine.cpp, bit-identical to the reference in ranks and counters)
+stands in (kind "port").  Its inputs come from the CPU-only generator
+oracle/_build/libh2inputs.so (cached on disk after the first construction:
+~12 min for configs[4] on 16 cores); it never maps the B200 library or touches
+the GPU.
 """
 from __future__ import annotations
 

@@ -948,6 +948,7 @@ struct EngineRun : Relief {
   std::vector<Evicted> evicted;
   bool leaf_done = false;
   bool splitting = false;
+  bool restore_operands = true;  // false: the operands were uploaded for this call only
   Relief* prev_relief = nullptr;
   bool evict(DBuf& b, bool operand) {
     if (!b.p) return false;
@@ -1003,10 +1004,42 @@ struct EngineRun : Relief {
       evicted.erase(evicted.begin() + i);
     }
   }
+  // every device buffer of the product itself (C's stores, bases, per-level factors)
+  void release_product() {
+    Vr.release();
+    Vc.release();
+    F.release();
+    for (auto* v : {&Tr, &Tc, &Tg, &Bp, &PA, &PB, &LA, &RB, &hold})
+      for (DBuf& b : *v) b.release();
+    for (Chunked& m : Mg) m.release();
+  }
   ~EngineRun() {
     // deferred work may still read held buffers (error paths): drain it first
     if (s_aux) cudaStreamSynchronize(s_aux);
     try {
+      // Evicted operand blocks come back only now, after the product's own buffers are gone
+      // (the result has been downloaded by then): their home blocks are free again, so the
+      // operands stay where they were uploaded and the next product on them finds the arena
+      // laid out as this one did.
+      if (!evicted.empty()) {
+        bool operands = false;
+        for (const Evicted& e : evicted) operands |= e.operand;
+        if (operands && restore_operands) {
+          release_product();
+          cudaStreamSynchronize(s);
+          if (t_arena) t_arena->reclaim(true);
+        }
+      }
+      if (!restore_operands) {  // per-call operands (h2c_mmp): they are freed next, nothing to bring back
+        for (size_t i = 0; i < evicted.size();) {
+          if (evicted[i].operand) {
+            ctx.pinned->give(evicted[i].host, evicted[i].bytes);
+            evicted.erase(evicted.begin() + i);
+          } else {
+            ++i;
+          }
+        }
+      }
       restore(true);  // operands stay resident across calls
       restore(false);
     } catch (...) {
@@ -2234,7 +2267,7 @@ struct EngineRun : Relief {
       for (int l = D - 1; l >= 1; --l) upper_level(l);
       split();
       join();
-      restore(true);
+      // evicted operand blocks are restored by the destructor, after C has been downloaded
     } catch (const CudaError& e) {
       throw CudaError(std::string(e.what()) + " [phase " + phase + "]");
     }
@@ -2898,6 +2931,7 @@ void Context::mmp(const h2c_matrix& a, const h2c_matrix& b, double eps, int adap
   CK(cudaEventRecord(e0, s));
   EngineRun R(*this, P, *dplan_, *A, *B, eps, adaptive != 0, s);
   R.profiling = profile;
+  R.restore_operands = false;
   R.run();
   CK(cudaEventRecord(e1, s));
   if (trace) CK(cudaStreamSynchronize(s));
